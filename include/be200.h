@@ -1,0 +1,191 @@
+/*
+ * be200.h — C ABI of the B200-native best-effort serving hot path.
+ *
+ * The reference (`besteffort`, pure Python + numpy) has no FFI layer: its
+ * "interface" is the Python call surface in pkg/src/besteffort.  Each entry
+ * point below replaces one piece of that surface for a whole batch of
+ * independent environments (one environment = one reference `ClusterSim`
+ * driven by one `run_eval` / `run_training` loop):
+ *
+ *   be_env_create / be_env_destroy   ClusterSim.__init__          simcore.py:72-84
+ *   be_env_reset                     ClusterSim(tiers) (re-create) evalkit.py:189-191
+ *   be_env_step                      advance + observe + encode +  evalkit.py:185-205,
+ *                                    forward/argmax + submit        simcore.py:94-157
+ *   be_env_drain                     ClusterSim.drain              simcore.py:151-153
+ *   be_rollout_greedy                run_eval (whole trace)        evalkit.py:154-209
+ *   be_qnet_route_f64                select_action / argmax(forward) policy.py:111-132
+ *   be_reduce_eval                   windowed + threshold_counts,  evalkit.py:217-241,
+ *                                    miss_fractions_by_rate        evalkit.py:61-68
+ *   be_trace_gen_stable              gen_stable (Philox, on device) workload.py:120-141
+ *   be_learner_*                     train_step / _StepKernel /    trainer.py:211-290
+ *                                    Adam                          trainer.py:177-199
+ *   be_replay_*                      ReplayBuffer                  trainer.py:101-163
+ *
+ * Conventions
+ *  - All data pointers are DEVICE pointers (e.g. torch.Tensor.data_ptr()),
+ *    borrowed, caller-owned and valid until `stream` reaches the call.
+ *    `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Handles own their device state; no allocation happens inside step /
+ *    rollout calls.
+ *  - Every function returns a be_status.  On failure be_last_error() returns
+ *    a thread-local message.  Device-side failures (FIFO ring overflow,
+ *    non-finite router input) are latched in the handle and reported by
+ *    be_env_check() after a stream sync; they are never silently ignored.
+ *  - Per-env arrays are env-major: element (e, i) lives at [e * ld + i].
+ */
+#ifndef BE200_H
+#define BE200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BE_MAX_TIERS 8
+#define BE_MAX_TASKS 16
+#define BE_MAX_LANES 32 /* sum of replicas over tiers: one warp lane per replica */
+
+typedef enum {
+    BE_OK = 0,
+    BE_EINVAL = 1,    /* bad argument -> reference ValueError / InvalidParameterError */
+    BE_ECAPACITY = 2, /* a replica FIFO ring overflowed (simcore.py never drops) */
+    BE_ECUDA = 3,     /* CUDA runtime error */
+    BE_ENONFINITE = 4 /* non-finite router input (policy.py:115-116) */
+} be_status;
+
+/* ModelTierSpec (simcore.py:21-37) */
+typedef struct {
+    int32_t replicas;
+    int32_t max_batch;
+    int32_t tokens_per_request;
+    int32_t _pad;
+    double alpha_ms;
+    double beta_ms;
+} be_tier;
+
+/* Everything a ClusterSim + RewardSpec + StateEncoding + RateEstimator need. */
+typedef struct {
+    int32_t n_tiers;                 /* M */
+    int32_t n_tasks;                 /* T */
+    be_tier tiers[BE_MAX_TIERS];
+    double deadline[BE_MAX_TASKS];   /* TaskSpec.deadline_ms_per_token (reward.py:32-42) */
+    int32_t soft[BE_MAX_TASKS];      /* 1 = soft deadline kind */
+    double matrix[BE_MAX_TASKS * BE_MAX_TIERS]; /* RewardSpec.matrix, [T][M] */
+    double decay_per_ms;             /* RewardSpec.decay_per_ms */
+    double cutoff_fraction;          /* RewardSpec.cutoff_fraction */
+    double batch_scales[BE_MAX_TIERS]; /* StateEncoding.batch_scales (policy.py:23-42) */
+    double rate_scale;               /* StateEncoding.rate_scale */
+    int32_t estimator_true_rate;     /* RateEstimator mode: 0 estimated, 1 true-rate */
+    int32_t reset_between_segments;  /* run_eval(reset_between_segments=...) */
+    double prior_rate;               /* RateEstimator.prior_rate */
+    int32_t ring_capacity;           /* per-replica FIFO slots (power of two) */
+    int32_t skip_ahead;              /* 1 = exact closed-form iteration skipping (default) */
+} be_cfg;
+
+/* Trace batch: WorkloadTrace (workload.py:39-91) for E envs, SoA, env-major. */
+typedef struct {
+    int32_t n_envs;
+    int32_t _pad;
+    int64_t ld;                  /* row stride (elements) of arrival/task/outputs */
+    const double* arrival_ms;    /* [E][ld] nondecreasing per env */
+    const uint8_t* task;         /* [E][ld] */
+    const int64_t* n_events;     /* [E] or NULL (= ld for every env) */
+    const int64_t* seg_offsets;  /* [E+1] CSR into seg_start/seg_rate */
+    const int64_t* seg_start;    /* SegmentMark.start_index */
+    const double* seg_rate;      /* SegmentMark.rate */
+    const int32_t* seg_bucket;   /* per segment reducer bucket id, or NULL */
+} be_trace_soa;
+
+/* QNetwork parameters (policy.py:68-118), fp64, BEQN1 order/layout. */
+typedef struct {
+    int32_t hidden;      /* multiple of 32, <= 1024 */
+    int32_t _pad;
+    const double* w1;    /* [D][H], D = T + M + 1 */
+    const double* b1;    /* [H] */
+    const double* w2;    /* [H][M] */
+    const double* b2;    /* [M] */
+} be_qweights;
+
+/* Per-request records (RequestRecord, evalkit.py:37-45), env-major [E][ld].
+ * flags = tier_id | (deadline_miss << 7).  Optional per-step router inputs. */
+typedef struct {
+    uint8_t* flags;      /* required */
+    double* reward;      /* required */
+    double* realized;    /* nullable: realized ms/token */
+    int32_t* obs;        /* nullable: [E][ld][M] observed per-tier batch */
+    double* rate;        /* nullable: [E][ld] rate signal */
+    double* q;           /* nullable: [E][ld][M] Q-values (policy mode) */
+} be_records;
+
+typedef struct be_env be_env;
+
+const char* be_last_error(void);
+int32_t be_abi_version(void);
+
+/* Environment handle: E envs, device state (replica headers, FIFO rings). */
+int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env** out);
+int32_t be_env_destroy(be_env* env);
+size_t be_env_device_bytes(const be_env* env);
+/* Re-initialise envs whose mask byte is nonzero (all if mask == NULL). */
+int32_t be_env_reset(be_env* env, const uint8_t* mask, void* stream);
+/* Sync `stream` and report latched device errors (ring overflow, ...). */
+int32_t be_env_check(be_env* env, void* stream);
+
+/* One env step for all E envs (evalkit.py:193-205 / trainer.py:375-395):
+ * advance every replica to arrival_ms[e], score completions into `rec`
+ * (indexed by each env's request id), update the rate estimator, observe,
+ * route (forced_action[e] if non-NULL, else static_tier if >= 0, else greedy
+ * argmax of W; epsilon-greedy with Philox(seed, counter) when epsilon > 0),
+ * submit.  Outputs obs [E][M], rate [E], action [E], q [E][M] (nullable). */
+int32_t be_env_step(be_env* env, const double* arrival_ms, const uint8_t* task,
+                    const double* true_rate, const uint8_t* forced_action,
+                    const be_qweights* W, int32_t static_tier, double epsilon,
+                    uint64_t philox_seed, uint64_t philox_counter, int64_t rec_ld,
+                    be_records* rec, int32_t* obs_out, double* rate_out,
+                    uint8_t* action_out, double* q_out, double* x_out, void* stream);
+/* Run every replica to completion (simcore.py:151-153). */
+int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream);
+
+/* Whole greedy rollout (run_eval) of E envs over a trace batch, fused in one
+ * persistent kernel: one warp per env, one lane per replica.  Routing:
+ * forced_action [E][ld] if non-NULL, else static_tier if >= 0, else W. */
+int32_t be_rollout_greedy(be_env* env, const be_trace_soa* trace, const be_qweights* W,
+                          int32_t static_tier, const uint8_t* forced_action, be_records* rec,
+                          void* stream);
+
+/* Batched router: q = relu(x W1 + b1) W2 + b2; action = argmax (first max),
+ * or uniform random with probability epsilon (Philox4x32-10). x: [B][D]. */
+int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers,
+                          const double* x, int32_t batch, double epsilon, uint64_t philox_seed,
+                          uint64_t philox_counter, double* q_out, uint8_t* action_out,
+                          void* stream);
+
+/* Evaluation reducer (evalkit.py:212-241, :61-74): per env a sequential fp64
+ * prefix sum of rewards in request order, trailing `window` means, counts of
+ * windows >= theta (== 1.0 for theta == 1.0); per (env, bucket) miss and
+ * request counts and reward sums.  Outputs:
+ *   win_counts [E][n_theta] int64, n_windows [E] int64,
+ *   bucket_miss / bucket_req [E][n_buckets] int64, bucket_reward [E][n_buckets] f64
+ * Buckets come from trace->seg_bucket (NULL -> everything in bucket 0).
+ * `thetas` is a HOST array (the thresholds are turned into exact difference
+ * cut-offs on the host, see reduce.cu). */
+int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const double* reward,
+                       int32_t window, const double* thetas, int32_t n_theta,
+                       int32_t n_buckets, int64_t* win_counts, int64_t* n_windows,
+                       int64_t* bucket_miss, int64_t* bucket_req, double* bucket_reward,
+                       void* stream);
+
+/* On-device gen_stable (workload.py:120-141) with Philox4x32-10 keyed by
+ * (seed, env): per env one Poisson segment at rate[e] req/s, exponential gaps
+ * of mean 1000/rate ms accumulated sequentially in fp64, uniform task ids;
+ * the first n events of the segment (truncated).  Writes arrival/task [E][ld]. */
+int32_t be_trace_gen_stable(int32_t n_envs, int64_t n, int64_t ld, const double* rate,
+                            int32_t n_tasks, uint64_t seed, double* arrival_ms, uint8_t* task,
+                            void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BE200_H */

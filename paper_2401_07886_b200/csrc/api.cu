@@ -1,0 +1,259 @@
+// api.cu — the extern "C" boundary (include/be200.h): argument validation,
+// handle lifetime, error reporting.  All compute is in the other .cu files.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "be200.h"
+#include "be_internal.h"
+
+namespace be {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* msg) {
+    snprintf(g_err, sizeof(g_err), "%s", msg);
+    return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* where) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
+    return BE_ECUDA;
+}
+
+static int validate_cfg(const be_cfg* c, int* lanes) {
+    if (!c) return set_error(BE_EINVAL, "cfg is NULL");
+    if (c->n_tiers < 1 || c->n_tiers > BE_MAX_TIERS)
+        return set_error(BE_EINVAL, "n_tiers must be in [1, 8]");
+    if (c->n_tasks < 1 || c->n_tasks > BE_MAX_TASKS)
+        return set_error(BE_EINVAL, "n_tasks must be in [1, 16]");
+    int R = 0;
+    for (int m = 0; m < c->n_tiers; ++m) {
+        const be_tier& t = c->tiers[m];
+        // ModelTierSpec.__post_init__ (simcore.py:31-37)
+        if (t.replicas < 1) return set_error(BE_EINVAL, "replicas must be >= 1");
+        if (!(t.alpha_ms > 0) || !(t.beta_ms >= 0) || !isfinite(t.alpha_ms) || !isfinite(t.beta_ms))
+            return set_error(BE_EINVAL, "alpha_ms must be > 0 and beta_ms >= 0");
+        if (t.max_batch < 1 || t.tokens_per_request < 1)
+            return set_error(BE_EINVAL, "max_batch and tokens_per_request must be >= 1");
+        R += t.replicas;
+    }
+    if (R > BE_MAX_LANES) return set_error(BE_EINVAL, "total replicas per env must be <= 32 (one warp)");
+    for (int k = 0; k < c->n_tasks; ++k) {
+        if (!(c->deadline[k] > 0)) return set_error(BE_EINVAL, "deadline must be positive");
+        for (int m = 0; m < c->n_tiers; ++m) {
+            double v = c->matrix[k * c->n_tiers + m];
+            if (!(v >= 0 && v <= 1)) return set_error(BE_EINVAL, "matrix entries must lie in [0, 1]");
+        }
+    }
+    if (!(c->decay_per_ms > 0 && c->decay_per_ms <= 1) || !(c->cutoff_fraction > 0 && c->cutoff_fraction <= 1))
+        return set_error(BE_EINVAL, "decay_per_ms and cutoff_fraction must lie in (0, 1]");
+    if (!(c->rate_scale > 0)) return set_error(BE_EINVAL, "rate_scale must be positive");
+    for (int m = 0; m < c->n_tiers; ++m)
+        if (!(c->batch_scales[m] > 0)) return set_error(BE_EINVAL, "batch_scales must be positive");
+    if (!(c->prior_rate > 0)) return set_error(BE_EINVAL, "prior_rate must be positive");
+    int cap = c->ring_capacity;
+    if (cap < 2 || (cap & (cap - 1)) != 0 || cap > (1 << 24))
+        return set_error(BE_EINVAL, "ring_capacity must be a power of two in [2, 2^24]");
+    *lanes = R;
+    return BE_OK;
+}
+
+static int validate_weights(const be_qweights* W, const be_cfg& c) {
+    if (!W || !W->w1 || !W->b1 || !W->w2 || !W->b2) return set_error(BE_EINVAL, "policy weights missing");
+    if (W->hidden < 32 || W->hidden % 32 != 0 || W->hidden > 1024)
+        return set_error(BE_EINVAL, "hidden must be a multiple of 32 in [32, 1024]");
+    size_t smem = rollout_smem_bytes(c.n_tasks, c.n_tiers, W->hidden, true);
+    if (smem > 200 * 1024) return set_error(BE_EINVAL, "Q-network too large for shared memory");
+    return BE_OK;
+}
+
+}  // namespace be
+
+using namespace be;
+
+extern "C" {
+
+const char* be_last_error(void) { return g_err; }
+
+int32_t be_abi_version(void) { return 1; }
+
+int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env** out) {
+    if (!out) return set_error(BE_EINVAL, "out is NULL");
+    *out = nullptr;
+    int R = 0;
+    int rc = validate_cfg(cfg, &R);
+    if (rc) return rc;
+    if (n_envs < 1) return set_error(BE_EINVAL, "n_envs must be >= 1");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return set_cuda_error(e, "cudaSetDevice");
+    be_env* env = new be_env();
+    memset(env, 0, sizeof(*env));
+    env->cfg = *cfg;
+    env->E = n_envs;
+    env->R = R;
+    env->device = device;
+    int cap_log2 = 0;
+    while ((1 << cap_log2) < cfg->ring_capacity) ++cap_log2;
+    env->cap_log2 = cap_log2;
+    cudaDeviceGetAttribute(&env->sms, cudaDevAttrMultiProcessorCount, device);
+    env->ring_bytes = (size_t)n_envs * R * ((size_t)1 << cap_log2) * 16;
+    size_t state = env_state_bytes_per_env(R) * (size_t)n_envs;
+    if ((e = cudaMalloc(&env->rings, env->ring_bytes)) != cudaSuccess ||
+        (e = cudaMalloc(&env->reps, state)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&env->d_counter, 64)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&env->d_status, 64)) != cudaSuccess) {
+        be_env_destroy(env);
+        return set_cuda_error(e, "be_env_create: cudaMalloc");
+    }
+    cudaMemset(env->d_status, 0, 64);
+    env->envs = nullptr;
+    rc = launch_env_reset(env, nullptr, 0);
+    if (rc) {
+        be_env_destroy(env);
+        return rc;
+    }
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        be_env_destroy(env);
+        return set_cuda_error(e, "be_env_create: reset");
+    }
+    *out = env;
+    return BE_OK;
+}
+
+int32_t be_env_destroy(be_env* env) {
+    if (!env) return BE_OK;
+    cudaFree(env->rings);
+    cudaFree(env->reps);
+    cudaFree(env->d_counter);
+    cudaFree(env->d_status);
+    delete env;
+    return BE_OK;
+}
+
+size_t be_env_device_bytes(const be_env* env) {
+    if (!env) return 0;
+    return env->ring_bytes + env_state_bytes_per_env(env->R) * (size_t)env->E + 128;
+}
+
+int32_t be_env_reset(be_env* env, const uint8_t* mask, void* stream) {
+    if (!env) return set_error(BE_EINVAL, "env is NULL");
+    return launch_env_reset(env, mask, (cudaStream_t)stream);
+}
+
+int32_t be_env_check(be_env* env, void* stream) {
+    if (!env) return set_error(BE_EINVAL, "env is NULL");
+    cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return set_cuda_error(e, "be_env_check: sync");
+    int32_t st[2];
+    e = cudaMemcpy(st, env->d_status, sizeof(st), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return set_cuda_error(e, "be_env_check: copy");
+    if (st[0] == 0) return BE_OK;
+    cudaMemset(env->d_status, 0, 64);
+    char msg[256];
+    if (st[0] == BE_ECAPACITY)
+        snprintf(msg, sizeof(msg),
+                 "env %d: replica FIFO ring overflow (capacity %d) or iteration counter "
+                 "overflow; recreate the env with a larger ring_capacity",
+                 st[1], 1 << env->cap_log2);
+    else if (st[0] == BE_EINVAL)
+        snprintf(msg, sizeof(msg), "env %d: action / tier out of range", st[1]);
+    else if (st[0] == BE_ENONFINITE)
+        snprintf(msg, sizeof(msg), "env %d: non-finite network input", st[1]);
+    else
+        snprintf(msg, sizeof(msg), "env %d: device error %d", st[1], st[0]);
+    return set_error(st[0], msg);
+}
+
+int32_t be_rollout_greedy(be_env* env, const be_trace_soa* trace, const be_qweights* W,
+                          int32_t static_tier, const uint8_t* forced_action, be_records* rec,
+                          void* stream) {
+    if (!env || !trace || !rec) return set_error(BE_EINVAL, "NULL argument");
+    if (trace->n_envs < 1 || trace->n_envs > env->E)
+        return set_error(BE_EINVAL, "trace has more envs than the env handle");
+    if (!trace->arrival_ms || !trace->task || !trace->seg_offsets)
+        return set_error(BE_EINVAL, "trace arrays missing");
+    if (trace->ld < 0 || trace->ld > (1 << 24)) return set_error(BE_EINVAL, "trace length must be <= 2^24");
+    if (!rec->flags || !rec->reward) return set_error(BE_EINVAL, "records.flags/reward required");
+    if (static_tier >= env->cfg.n_tiers) return set_error(BE_EINVAL, "static tier out of range");
+    if (!forced_action && static_tier < 0) {
+        int rc = validate_weights(W, env->cfg);
+        if (rc) return rc;
+    }
+    if (rec->q && (forced_action || static_tier >= 0)) rec->q = nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != env->device) cudaSetDevice(env->device);
+    return launch_rollout(env, trace, W, static_tier, forced_action, rec, (cudaStream_t)stream);
+}
+
+int32_t be_env_step(be_env* env, const double* arrival_ms, const uint8_t* task,
+                    const double* true_rate, const uint8_t* forced_action, const be_qweights* W,
+                    int32_t static_tier, double epsilon, uint64_t philox_seed,
+                    uint64_t philox_counter, int64_t rec_ld, be_records* rec, int32_t* obs_out,
+                    double* rate_out, uint8_t* action_out, double* q_out, double* x_out,
+                    void* stream) {
+    if (!env || !arrival_ms || !task || !rec || !rec->flags || !rec->reward)
+        return set_error(BE_EINVAL, "NULL argument");
+    if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");
+    if (!(epsilon >= 0.0 && epsilon <= 1.0)) return set_error(BE_EINVAL, "epsilon must lie in [0, 1]");
+    if (static_tier >= env->cfg.n_tiers) return set_error(BE_EINVAL, "static tier out of range");
+    if (env->cfg.estimator_true_rate && !true_rate) return set_error(BE_EINVAL, "true-rate mode needs true_rate");
+    if (!forced_action && static_tier < 0) {
+        int rc = validate_weights(W, env->cfg);
+        if (rc) return rc;
+    }
+    return launch_env_step(env, arrival_ms, task, true_rate, forced_action, W, static_tier, epsilon,
+                           philox_seed, philox_counter, rec_ld, rec, obs_out, rate_out, action_out,
+                           q_out, x_out, (cudaStream_t)stream);
+}
+
+int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream) {
+    if (!env || !rec || !rec->flags || !rec->reward) return set_error(BE_EINVAL, "NULL argument");
+    if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");
+    return launch_env_drain(env, rec_ld, rec, (cudaStream_t)stream);
+}
+
+int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers, const double* x,
+                          int32_t batch, double epsilon, uint64_t philox_seed,
+                          uint64_t philox_counter, double* q_out, uint8_t* action_out,
+                          void* stream) {
+    if (!W || !W->w1 || !W->b1 || !W->w2 || !W->b2 || !x || !action_out)
+        return set_error(BE_EINVAL, "NULL argument");
+    if (n_tasks < 1 || n_tasks > BE_MAX_TASKS || n_tiers < 1 || n_tiers > BE_MAX_TIERS)
+        return set_error(BE_EINVAL, "dimensions out of range");
+    if (W->hidden < 1 || W->hidden > 4096) return set_error(BE_EINVAL, "hidden out of range");
+    if (!(epsilon >= 0.0 && epsilon <= 1.0)) return set_error(BE_EINVAL, "epsilon must lie in [0, 1]");
+    if (batch < 0) return set_error(BE_EINVAL, "batch must be >= 0");
+    if (batch == 0) return BE_OK;
+    return launch_route(W, n_tasks, n_tiers, x, batch, epsilon, philox_seed, philox_counter, q_out,
+                        action_out, (cudaStream_t)stream);
+}
+
+int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const double* reward,
+                       int32_t window, const double* thetas, int32_t n_theta, int32_t n_buckets,
+                       int64_t* win_counts, int64_t* n_windows, int64_t* bucket_miss,
+                       int64_t* bucket_req, double* bucket_reward, void* stream) {
+    if (!trace || !flags || !reward || !win_counts || !n_windows || !bucket_miss || !bucket_req ||
+        !bucket_reward || (n_theta > 0 && !thetas))
+        return set_error(BE_EINVAL, "NULL argument");
+    if (window < 1) return set_error(BE_EINVAL, "window must be >= 1");
+    if (n_theta < 0 || n_theta > 16) return set_error(BE_EINVAL, "n_theta must be in [0, 16]");
+    if (n_buckets < 1) return set_error(BE_EINVAL, "n_buckets must be >= 1");
+    if (!trace->seg_offsets) return set_error(BE_EINVAL, "trace segments missing");
+    return launch_reduce(trace, flags, reward, window, thetas, n_theta, n_buckets, win_counts,
+                         n_windows, bucket_miss, bucket_req, bucket_reward, (cudaStream_t)stream);
+}
+
+int32_t be_trace_gen_stable(int32_t n_envs, int64_t n, int64_t ld, const double* rate,
+                            int32_t n_tasks, uint64_t seed, double* arrival_ms, uint8_t* task,
+                            void* stream) {
+    if (!rate || !arrival_ms || !task) return set_error(BE_EINVAL, "NULL argument");
+    if (n_envs < 1 || n < 0 || ld < n || n_tasks < 1 || n_tasks > 255)
+        return set_error(BE_EINVAL, "bad sizes");
+    return launch_tracegen(n_envs, n, ld, rate, n_tasks, seed, arrival_ms, task, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,404 @@
+// be_env.cuh — device-side building blocks of the batched serving environment.
+//
+// Layout (B200-first):
+//   * one warp per environment, one lane per replica (sum of replicas <= 32);
+//     lane state (pending event, iteration counter, FIFO cursor, cached FIFO
+//     head) lives in registers for the whole rollout;
+//   * each replica owns a FIFO ring of 16-byte slots in HBM: the reference's
+//     `active` dict and `queue` deque (simcore.py:53-60) are one FIFO whose
+//     first min(count, max_batch) entries are the active batch;
+//   * per-env scalars (rate-estimator window, segment cursor) are warp-uniform
+//     registers; per-tier reductions use REDUX (__reduce_*_sync).
+//
+// Exactness: every event-time operation uses explicit round-to-nearest
+// intrinsics in the reference's evaluation order (simcore.py:146 evaluates
+// `time + alpha + beta * n` as (time + alpha) + (beta * n)), so the
+// translation unit's FMA contraction setting cannot change results.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "be200.h"
+
+namespace be {
+
+constexpr int K_NONE = 0;
+constexpr int K_START = 1;
+constexpr int K_END = 2;
+constexpr unsigned FULL = 0xffffffffu;
+
+// One FIFO entry: a submitted Request (simcore.py:40-50) reduced to what the
+// event loop needs.  join = iteration counter at the START that first put the
+// request in a running batch (tokens_done = iters - join), -1 before that.
+struct __align__(16) Slot {
+    double arrival;
+    uint32_t idtask;  // request id (low 24 bits) | task id << 24
+    int32_t join;
+};
+
+// Per-lane (= per-replica) state; the FIFO head is cached in registers.
+struct Rep {
+    double t;        // time of the pending event (kind != K_NONE)
+    double h_arr;    // arrival of the FIFO head
+    int kind;
+    int iters;       // END events processed on this replica
+    uint32_t head;   // monotone FIFO cursor (slot = head & mask)
+    int count;       // len(active) + len(queue)
+    int n_running;   // FIFO prefix that has joined an iteration
+    int h_join;
+    uint32_t h_idtask;
+};
+
+struct TierC {
+    double alpha;
+    double beta;
+    int max_batch;
+    int tokens;
+    int tier;
+};
+
+// Reward constants (reward.py:45-126) staged in shared memory.
+struct Score {
+    double deadline[BE_MAX_TASKS];
+    double cut[BE_MAX_TASKS];  // cutoff_fraction * deadline (reward.py:108)
+    double matrix[BE_MAX_TASKS * BE_MAX_TIERS];
+    int soft[BE_MAX_TASKS];
+    double decay;
+    int M;
+};
+
+struct RecOut {
+    uint8_t* flags;
+    double* reward;
+    double* realized;
+    int64_t base;  // e * ld
+};
+
+__device__ __forceinline__ void load_score(Score& s, const be_cfg& c) {
+    // called by a single warp; caller syncs
+    int lane = threadIdx.x & 31;
+    for (int k = lane; k < BE_MAX_TASKS; k += 32) {
+        s.deadline[k] = c.deadline[k];
+        s.cut[k] = __dmul_rn(c.cutoff_fraction, c.deadline[k]);
+        s.soft[k] = c.soft[k];
+    }
+    for (int k = lane; k < BE_MAX_TASKS * BE_MAX_TIERS; k += 32) {
+        int t = k / BE_MAX_TIERS, m = k % BE_MAX_TIERS;
+        s.matrix[k] = (t < c.n_tasks && m < c.n_tiers) ? c.matrix[t * c.n_tiers + m] : 0.0;
+    }
+    if (lane == 0) {
+        s.decay = c.decay_per_ms;
+        s.M = c.n_tiers;
+    }
+}
+
+// lane -> (tier, constants); lanes beyond the replica count get tier = -1.
+__device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane) {
+    TierC tc;
+    tc.alpha = 1.0;
+    tc.beta = 0.0;
+    tc.max_batch = 1;
+    tc.tokens = 1;
+    tc.tier = -1;
+    int acc = 0;
+#pragma unroll
+    for (int m = 0; m < BE_MAX_TIERS; ++m) {
+        if (m < c.n_tiers) {
+            int r = c.tiers[m].replicas;
+            if (lane >= acc && lane < acc + r) {
+                tc.alpha = c.tiers[m].alpha_ms;
+                tc.beta = c.tiers[m].beta_ms;
+                tc.max_batch = c.tiers[m].max_batch;
+                tc.tokens = c.tiers[m].tokens_per_request;
+                tc.tier = m;
+            }
+            acc += r;
+        }
+    }
+    return tc;
+}
+
+// ---------------------------------------------------------------------------
+// Request completion: realized latency (simcore.py:135), deadline weight and
+// reward (reward.py:94-126), deadline miss (evalkit.py:65-67).
+__device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Score& sc,
+                                         const RecOut& o, double t_end) {
+    double realized = __ddiv_rn(__dsub_rn(t_end, r.h_arr), (double)tc.tokens);
+    int task = (int)(r.h_idtask >> 24);
+    int64_t id = (int64_t)(r.h_idtask & 0xffffffu);
+    double dl = sc.deadline[task];
+    double w;
+    if (!sc.soft[task]) {
+        w = realized <= dl ? 1.0 : 0.0;
+    } else {
+        double excess = __dsub_rn(realized, dl);
+        if (excess <= 0.0) {
+            w = 1.0;
+        } else if (excess <= sc.cut[task]) {
+            double v = __dsub_rn(1.0, __dmul_rn(sc.decay, excess));
+            w = v > 0.0 ? v : 0.0;  // max(0.0, v)
+        } else {
+            w = 0.0;
+        }
+    }
+    double reward = __dmul_rn(w, sc.matrix[task * BE_MAX_TIERS + tc.tier]);
+    uint8_t flag = (uint8_t)(tc.tier | ((realized > dl) ? 0x80 : 0));
+    o.reward[o.base + id] = reward;
+    o.flags[o.base + id] = flag;
+    if (o.realized) o.realized[o.base + id] = realized;
+}
+
+// ---------------------------------------------------------------------------
+// Exact closed-form skipping of steady-state iterations.
+//
+// Between membership changes a replica repeats START(t) -> END at
+// t' = RN(RN(t + alpha) + c), c = RN(beta * n).  While t, RN(t + alpha) and t'
+// stay inside one binade [2^e, 2^(e+1)), every double there is an integer
+// multiple of u = 2^(e-52) and t is one, so RN(t + alpha) = t + RN_u(alpha)
+// and RN(. + c) = . + RN_u(c), where RN_u rounds to the nearest multiple of u
+// (ties excluded below, as they would depend on the parity of t / u).  Hence
+// k cycles advance t by exactly k * (a + b) * u, a = RN_u(alpha) / u,
+// b = RN_u(c) / u — the same bits the iteration-by-iteration recurrence
+// produces.  Anything outside those conditions falls back to single steps.
+
+// round(x * 2^(52-e)) to an integer; false on a rounding tie or overflow.
+__device__ __forceinline__ bool scaled_round(double x, int e, long long& out) {
+    if (x == 0.0) {
+        out = 0;
+        return true;
+    }
+    long long bits = __double_as_longlong(x);
+    int ex = (int)((bits >> 52) & 0x7ff);
+    if (ex == 0 || ex == 0x7ff || bits < 0) return false;
+    long long mx = (bits & 0xfffffffffffffLL) | (1LL << 52);
+    int s = e - (ex - 1023);  // right shift
+    if (s <= 0) {
+        if (s < -9) return false;
+        out = mx << (-s);
+        return true;
+    }
+    if (s >= 60) {
+        out = 0;
+        return true;
+    }
+    long long q = mx >> s;
+    long long rem = mx & ((1LL << s) - 1);
+    long long half = 1LL << (s - 1);
+    if (rem == half) return false;
+    out = q + (rem > half ? 1 : 0);
+    return true;
+}
+
+// Number k <= kmax of whole START->END cycles that can be jumped from a START
+// at time t (t < until) with constant increment; writes the time after k cycles.
+__device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int kmax,
+                                           double until, double& t_out) {
+    long long bits = __double_as_longlong(t);
+    int ext = (int)((bits >> 52) & 0x7ff);
+    if (kmax <= 0 || ext == 0 || ext == 0x7ff || bits < 0) return 0;
+    int e = ext - 1023;
+    long long T0 = (bits & 0xfffffffffffffLL) | (1LL << 52);
+    long long a, b;
+    if (!scaled_round(alpha, e, a) || !scaled_round(c, e, b)) return 0;
+    long long d = a + b;
+    if (d <= 0) return 0;
+    const long long TOP = 1LL << 53;
+    long long lim = TOP - 2 - T0;  // T0 + k d <= 2^53 - 2 keeps every operand in the binade
+    if (lim < d) return 0;
+    long long k = lim / d;
+    // horizon: the k-th END must satisfy t_k <= until
+    long long ub = __double_as_longlong(until);
+    int exu = (int)((ub >> 52) & 0x7ff);
+    if (exu != 0x7ff) {  // finite
+        int sh = (exu - 1023) - e;  // until >= t  =>  sh >= 0
+        if (sh < 0) return 0;
+        if (sh < 10) {
+            long long mu = (ub & 0xfffffffffffffLL) | (1LL << 52);
+            long long ui = mu << sh;  // floor(until / u): exact integer
+            long long ku = (ui - T0) / d;
+            if (ku < k) k = ku;
+        }
+    }
+    if (k > kmax) k = kmax;
+    if (k <= 0) return 0;
+    long long Tk = T0 + k * d;
+    t_out = __longlong_as_double(((long long)(e + 1023) << 52) | (Tk - (1LL << 52)));
+    return (int)k;
+}
+
+// ---------------------------------------------------------------------------
+// One replica's share of ClusterSim.advance(until) (simcore.py:113-149):
+// process events while (t, kind) < (until, START); END at the horizon is
+// processed, START at the horizon stays pending (simcore.py:120).
+// Returns false if the iteration counter would overflow.
+__device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double until, Slot* ring,
+                                             uint32_t mask, const Score& sc, const RecOut& o,
+                                             bool skip) {
+    while (r.kind != K_NONE) {
+        if (r.kind == K_START) {
+            if (!(r.t < until)) break;
+            int n_active = min(r.count, tc.max_batch);
+            if (r.n_running < n_active) {  // newly admitted requests join (simcore.py:143-145)
+                if (r.n_running == 0) r.h_join = r.iters;
+                for (int k = max(r.n_running, 1); k < n_active; ++k)
+                    ring[(r.head + (uint32_t)k) & mask].join = r.iters;
+                r.n_running = n_active;
+            }
+            double c = __dmul_rn(tc.beta, (double)n_active);
+            if (skip) {
+                int K = r.h_join + tc.tokens - r.iters;  // ENDs until the head completes
+                double tn;
+                int k = skip_cycles(r.t, tc.alpha, c, min(K - 1, (1 << 30) - r.iters), until, tn);
+                if (k > 0) {
+                    r.t = tn;
+                    r.iters += k;
+                    if (!(r.t < until)) break;
+                }
+            }
+            r.t = __dadd_rn(__dadd_rn(r.t, tc.alpha), c);
+            r.kind = K_END;
+        } else {
+            if (!(r.t <= until)) break;
+            if (r.iters >= (1 << 30)) return false;
+            r.iters++;
+            // FIFO completions (simcore.py:127-137): every running request got a token
+            while (r.n_running > 0 && r.iters - r.h_join >= tc.tokens) {
+                complete(r, tc, sc, o, r.t);
+                r.head++;
+                r.count--;
+                r.n_running--;
+                if (r.count > 0) {
+                    Slot s = ring[r.head & mask];
+                    r.h_arr = s.arrival;
+                    r.h_idtask = s.idtask;
+                    r.h_join = s.join;
+                }
+            }
+            // queue admission (simcore.py:138-140) is implicit: active = FIFO prefix
+            r.kind = r.count > 0 ? K_START : K_NONE;  // START at the same time (simcore.py:141-142)
+        }
+    }
+    return true;
+}
+
+// ClusterSim.submit on the chosen lane (simcore.py:94-111).  `clock` is the
+// env clock (== the arrival being routed).  Returns false on ring overflow.
+__device__ __forceinline__ bool submit_lane(Rep& r, const TierC& tc, double clock, uint32_t idtask,
+                                            Slot* ring, uint32_t mask) {
+    if ((uint32_t)r.count > mask) return false;
+    if (r.count == 0) {
+        r.h_arr = clock;
+        r.h_idtask = idtask;
+        r.h_join = -1;
+    } else {
+        Slot s;
+        s.arrival = clock;
+        s.idtask = idtask;
+        s.join = -1;
+        ring[(r.head + (uint32_t)r.count) & mask] = s;
+    }
+    r.count++;
+    if (r.kind == K_NONE) {  // idle replica: START at the current clock
+        r.kind = K_START;
+        r.t = clock;
+    }
+    return true;
+}
+
+__device__ __forceinline__ void rep_reset(Rep& r) {
+    r.t = 0.0;
+    r.h_arr = 0.0;
+    r.kind = K_NONE;
+    r.iters = 0;
+    r.count = 0;
+    r.n_running = 0;
+    r.h_join = -1;
+    r.h_idtask = 0;
+}
+
+// Rate estimator (workload.py:212-255), warp-uniform.
+struct Estimator {
+    double w[5];
+    int n;
+};
+
+__device__ __forceinline__ double estimator_observe(Estimator& est, double t, bool true_rate,
+                                                    double cur_rate, double prior) {
+    if (est.n == 5) {
+        est.w[0] = est.w[1];
+        est.w[1] = est.w[2];
+        est.w[2] = est.w[3];
+        est.w[3] = est.w[4];
+        est.n = 4;
+    }
+    // est.w[est.n] = t without dynamic register indexing
+    if (est.n == 0) est.w[0] = t;
+    else if (est.n == 1) est.w[1] = t;
+    else if (est.n == 2) est.w[2] = t;
+    else if (est.n == 3) est.w[3] = t;
+    else est.w[4] = t;
+    est.n++;
+    if (true_rate) return cur_rate;
+    if (est.n < 2) return prior;
+    double last = t;
+    double gap = __ddiv_rn(__ddiv_rn(__dsub_rn(last, est.w[0]), (double)(est.n - 1)), 1000.0);
+    return __ddiv_rn(1.0, gap > 1e-6 ? gap : 1e-6);
+}
+
+// ---------------------------------------------------------------------------
+// Q-network forward for one state, spread over the warp (policy.py:111-118):
+// lane l owns hidden units j = l + 32k.  Weights in shared memory:
+// sW1 [D][H] (as BEQN1), sb1 [H], sW2t [M][H] (transposed), sb2 [M].
+// Result q[] is bit-identical on every lane (xor-butterfly sums commute).
+template <int M>
+__device__ __forceinline__ void qnet_warp(const double* __restrict__ sW1,
+                                          const double* __restrict__ sb1,
+                                          const double* __restrict__ sW2t,
+                                          const double* __restrict__ sb2, int T, int H, int task,
+                                          const double (&xt)[M], double xr, double (&q)[M]) {
+    int lane = threadIdx.x & 31;
+    double acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = 0.0;
+    const double* wtask = sW1 + task * H;
+    const double* wtier = sW1 + T * H;
+    const double* wrate = sW1 + (T + M) * H;
+#pragma unroll 4
+    for (int j = lane; j < H; j += 32) {
+        double pre = wtask[j];
+#pragma unroll
+        for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], wtier[m * H + j], pre);
+        pre = __fma_rn(xr, wrate[j], pre);
+        pre = __dadd_rn(pre, sb1[j]);
+        double h = pre > 0.0 ? pre : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = __dadd_rn(acc[m], __shfl_xor_sync(FULL, acc[m], off));
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) q[m] = __dadd_rn(acc[m], sb2[m]);
+}
+
+// np.argmax semantics: first NaN if any, else first maximum.
+template <int M>
+__device__ __forceinline__ int argmax_first(const double (&q)[M]) {
+    int best = 0;
+    bool nan_seen = q[0] != q[0];
+#pragma unroll
+    for (int m = 1; m < M; ++m) {
+        if (nan_seen) break;
+        if (q[m] != q[m]) {
+            best = m;
+            nan_seen = true;
+        } else if (q[m] > q[best]) {
+            best = m;
+        }
+    }
+    return best;
+}
+
+}  // namespace be

@@ -1,0 +1,46 @@
+// be_internal.h — host-side internals shared by the translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "be200.h"
+
+struct be_env {
+    be_cfg cfg;
+    int32_t E;        // environments
+    int32_t R;        // replicas per env (lanes used per warp)
+    int32_t device;
+    int32_t sms;      // multiprocessor count
+    int32_t cap_log2; // per-replica FIFO ring capacity = 1 << cap_log2
+    void* rings;      // [E][R][cap] Slot (16 B)
+    size_t ring_bytes;
+    void* reps;       // step API: [E][R] Rep
+    void* envs;       // step API: [E] EnvState
+    int32_t* d_counter;
+    int32_t* d_status;  // [0] code, [1] env
+};
+
+namespace be {
+int set_error(int code, const char* msg);
+int set_cuda_error(cudaError_t e, const char* where);
+int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
+                   const uint8_t* forced, const be_records* rec, cudaStream_t st);
+size_t rollout_smem_bytes(int T, int M, int H, bool policy);
+int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st);
+int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
+                    const double* true_rate, const uint8_t* forced, const be_qweights* W,
+                    int static_tier, double epsilon, uint64_t seed, uint64_t counter,
+                    int64_t rec_ld, const be_records* rec, int32_t* obs_out, double* rate_out,
+                    uint8_t* action_out, double* q_out, double* x_out, cudaStream_t st);
+int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st);
+size_t env_state_bytes_per_env(int R);
+int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* reward, int window,
+                  const double* thetas, int n_theta, int n_buckets, int64_t* win_counts,
+                  int64_t* n_windows, int64_t* bucket_miss, int64_t* bucket_req,
+                  double* bucket_reward, cudaStream_t st);
+int launch_route(const be_qweights* W, int T, int M, const double* x, int B, double eps,
+                 uint64_t seed, uint64_t counter, double* q_out, uint8_t* a_out, cudaStream_t st);
+int launch_tracegen(int E, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
+                    double* arrival, uint8_t* task, cudaStream_t st);
+}  // namespace be

@@ -1,0 +1,284 @@
+// step.cu — step-synchronous environment API: be_env_reset / be_env_step /
+// be_env_drain.  Same device building blocks as the fused rollout
+// (be_env.cuh); the per-replica registers are loaded from and stored back to
+// HBM around every step, so the host can interleave its own logic (the
+// training loop, a custom router) between steps.  One warp per env.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "be_env.cuh"
+#include "be_internal.h"
+#include "be_philox.cuh"
+
+namespace be {
+
+struct EnvState {
+    double w[5];
+    int32_t n;
+    int32_t _pad;
+    int64_t next_id;  // request id of the next submitted request
+};
+
+size_t env_state_bytes_per_env(int R) { return (size_t)R * sizeof(Rep) + sizeof(EnvState); }
+
+static __device__ __forceinline__ Rep* reps_of(void* base, int e, int R) {
+    return reinterpret_cast<Rep*>(base) + (size_t)e * R;
+}
+static __device__ __forceinline__ EnvState* state_of(void* base, int e, int E, int R) {
+    return reinterpret_cast<EnvState*>(reinterpret_cast<Rep*>(base) + (size_t)E * R) + e;
+}
+
+__global__ void env_reset_kernel(void* base, int E, int R, const uint8_t* mask) {
+    int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (gw >= E) return;
+    if (mask && !mask[gw]) return;
+    if (lane < R) {
+        Rep r;
+        rep_reset(r);
+        r.head = 0;
+        reps_of(base, gw, R)[lane] = r;
+    }
+    if (lane == 0) {
+        EnvState s;
+        for (int k = 0; k < 5; ++k) s.w[k] = 0.0;
+        s.n = 0;
+        s._pad = 0;
+        s.next_id = 0;
+        *state_of(base, gw, E, R) = s;
+    }
+}
+
+struct StepParams {
+    be_cfg cfg;
+    int32_t E, R, cap_log2;
+    void* state;
+    Slot* rings;
+    const double* arrival;
+    const uint8_t* task;
+    const double* true_rate;
+    const uint8_t* forced;
+    int32_t static_tier;
+    int32_t H;
+    const double *w1, *b1, *w2, *b2;
+    double epsilon;
+    uint64_t seed, counter;
+    int64_t rec_ld;
+    be_records rec;
+    int32_t* obs_out;
+    double* rate_out;
+    uint8_t* action_out;
+    double* q_out;
+    double* x_out;
+    int32_t* status;
+    int32_t drain;
+};
+
+template <int M>
+__global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Score& sc = *reinterpret_cast<Score*>(smem_raw);
+    double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
+    const int T = p.cfg.n_tasks;
+    const int H = p.H, D = T + M + 1;
+    const bool policy = !p.drain && p.forced == nullptr && p.static_tier < 0;
+    if (threadIdx.x < 32) load_score(sc, p.cfg);
+    if (policy) {
+        for (int k = threadIdx.x; k < D * H; k += blockDim.x) sw[k] = p.w1[k];
+        for (int k = threadIdx.x; k < H; k += blockDim.x) sw[D * H + k] = p.b1[k];
+        for (int k = threadIdx.x; k < M * H; k += blockDim.x) sw[D * H + H + k] = p.w2[(k % H) * M + k / H];
+        for (int k = threadIdx.x; k < M; k += blockDim.x) sw[D * H + H + M * H + k] = p.b2[k];
+    }
+    __syncthreads();
+    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (e >= p.E) return;
+    const int lane = threadIdx.x & 31;
+    const TierC tc = lane_tier(p.cfg, lane);
+    const bool al = tc.tier >= 0;
+    const uint32_t mask = (1u << p.cap_log2) - 1u;
+    Slot* ring = p.rings + ((size_t)e * p.R + (al ? lane : 0)) * ((size_t)mask + 1);
+    Rep r;
+    if (al) r = reps_of(p.state, e, p.R)[lane];
+    else rep_reset(r);
+    EnvState* es = state_of(p.state, e, p.E, p.R);
+    // records are indexed by request id modulo rec_ld (a ring for long runs)
+    // complete() writes at base + id; id is the 24-bit slot id.
+    RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, (int64_t)e * p.rec_ld};
+    bool ok = true;
+    const bool skip = p.cfg.skip_ahead != 0;
+    if (p.drain) {
+        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip);
+        if (al) reps_of(p.state, e, p.R)[lane] = r;
+        const bool all_ok = __all_sync(FULL, ok);
+        if (!all_ok && lane == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
+        return;
+    }
+    const double U = p.arrival[e];
+    const int task = p.task[e];
+    if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out, skip);
+    Estimator est;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) est.w[k] = es->w[k];
+    est.n = es->n;
+    const int64_t id = es->next_id;
+    const double cur = p.true_rate ? p.true_rate[e] : 0.0;
+    const double rate = estimator_observe(est, U, p.cfg.estimator_true_rate != 0, cur, p.cfg.prior_rate);
+    int obs[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) obs[m] = (int)__reduce_add_sync(FULL, (tc.tier == m) ? (unsigned)r.count : 0u);
+    double xt[M], q[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        xt[m] = __ddiv_rn((double)obs[m], p.cfg.batch_scales[m]);
+        q[m] = 0.0;
+    }
+    const double xr = __ddiv_rn(rate, p.cfg.rate_scale);
+    int tier;
+    bool explore = false;
+    if (p.forced) {
+        tier = p.forced[e];
+    } else if (p.static_tier >= 0) {
+        tier = p.static_tier;
+    } else {
+        // select_action (policy.py:125-132): explore with probability epsilon
+        if (p.epsilon > 0.0) {
+            P4 rnd = philox4x32_10(p.counter, (uint64_t)e, p.seed);
+            if (u01(rnd.x[0], rnd.x[1]) < p.epsilon) {
+                explore = true;
+                tier = (int)below(rnd.x[2], (uint32_t)M);
+            }
+        }
+        qnet_warp<M>(sw, sw + D * H, sw + D * H + H, sw + D * H + H + M * H, T, H, task, xt, xr, q);
+        if (!explore) tier = argmax_first<M>(q);
+    }
+    if (lane < M) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            if (lane == m) {
+                if (p.obs_out) p.obs_out[(size_t)e * M + m] = obs[m];
+                if (p.q_out) p.q_out[(size_t)e * M + m] = q[m];
+            }
+        }
+    }
+    if (p.x_out && lane < D) {
+        // encode (policy.py:52-65): [onehot(task), obs/scale, rate/rate_scale]
+        double v = 0.0;
+        if (lane < T) v = lane == task ? 1.0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+            if (lane == T + m) v = xt[m];
+        if (lane == T + M) v = xr;
+        p.x_out[(size_t)e * D + lane] = v;
+    }
+    unsigned key = (tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)lane) : 0xffffffffu;
+    unsigned best = __reduce_min_sync(FULL, key);
+    bool bad = best == 0xffffffffu;
+    if (!bad && (int)(best & 31u) == lane) {
+        uint32_t rid = (uint32_t)(id % p.rec_ld);
+        ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
+    }
+    if (al) reps_of(p.state, e, p.R)[lane] = r;
+    if (lane == 0) {
+        if (p.rate_out) p.rate_out[e] = rate;
+        if (p.action_out) p.action_out[e] = (uint8_t)tier;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) es->w[k] = est.w[k];
+        es->n = est.n;
+        es->next_id = id + 1;
+    }
+    const bool all_ok = __all_sync(FULL, ok);
+    if (lane == 0 && (bad || !all_ok)) {
+        if (atomicCAS(&p.status[0], 0, bad ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
+    }
+}
+
+int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st) {
+    int threads = 256;
+    int blocks = (int)(((long long)env->E * 32 + threads - 1) / threads);
+    env_reset_kernel<<<blocks, threads, 0, st>>>(env->reps, env->E, env->R, mask);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env reset");
+}
+
+template <int M>
+static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
+    auto kern = env_step_kernel<M>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
+    }
+    int threads = 256;
+    int blocks = (int)(((long long)p.E * 32 + threads - 1) / threads);
+    kern<<<blocks, threads, smem, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step launch");
+}
+
+static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st) {
+    switch (p.cfg.n_tiers) {
+        case 1: return launch_step_m<1>(p, smem, st);
+        case 2: return launch_step_m<2>(p, smem, st);
+        case 3: return launch_step_m<3>(p, smem, st);
+        case 4: return launch_step_m<4>(p, smem, st);
+        case 5: return launch_step_m<5>(p, smem, st);
+        case 6: return launch_step_m<6>(p, smem, st);
+        case 7: return launch_step_m<7>(p, smem, st);
+        case 8: return launch_step_m<8>(p, smem, st);
+        default: return set_error(BE_EINVAL, "n_tiers out of range");
+    }
+}
+
+static StepParams base_params(be_env* env, int64_t rec_ld, const be_records* rec) {
+    StepParams p{};
+    p.cfg = env->cfg;
+    p.E = env->E;
+    p.R = env->R;
+    p.cap_log2 = env->cap_log2;
+    p.state = env->reps;
+    p.rings = reinterpret_cast<Slot*>(env->rings);
+    p.rec_ld = rec_ld;
+    p.rec = *rec;
+    p.status = env->d_status;
+    p.static_tier = -1;
+    return p;
+}
+
+int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
+                    const double* true_rate, const uint8_t* forced, const be_qweights* W,
+                    int static_tier, double epsilon, uint64_t seed, uint64_t counter,
+                    int64_t rec_ld, const be_records* rec, int32_t* obs_out, double* rate_out,
+                    uint8_t* action_out, double* q_out, double* x_out, cudaStream_t st) {
+    StepParams p = base_params(env, rec_ld, rec);
+    p.arrival = arrival;
+    p.task = task;
+    p.true_rate = true_rate;
+    p.forced = forced;
+    p.static_tier = static_tier;
+    p.epsilon = epsilon;
+    p.seed = seed;
+    p.counter = counter;
+    p.obs_out = obs_out;
+    p.rate_out = rate_out;
+    p.action_out = action_out;
+    p.q_out = q_out;
+    p.x_out = x_out;
+    bool policy = forced == nullptr && static_tier < 0;
+    if (policy) {
+        p.H = W->hidden;
+        p.w1 = W->w1;
+        p.b1 = W->b1;
+        p.w2 = W->w2;
+        p.b2 = W->b2;
+    }
+    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, policy ? p.H : 0, policy);
+    return dispatch_step(p, smem, st);
+}
+
+int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st) {
+    StepParams p = base_params(env, rec_ld, rec);
+    p.drain = 1;
+    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, 0, false);
+    return dispatch_step(p, smem, st);
+}
+
+}  // namespace be

@@ -1,0 +1,246 @@
+"""Greedy rollout + evaluation on the GPU (drop-ins for besteffort.evalkit).
+
+  run_eval            evalkit.py:154-209  (same signature, same EvalRun records)
+  run_eval_batch      the same loop for E envs in one persistent kernel
+  windowed / threshold_counts / miss fractions   evalkit.py:212-241, :61-74
+                      -> be_reduce_eval (sequential fp64 scan per env on device)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence, Union
+
+import numpy as np
+import torch
+
+from . import _lib
+from .env import EnvBatch, default_ring_capacity
+from .policy import DeviceQNet
+from .specs import StateEncoding, event_rates
+from .trace import TraceBatch
+
+WINDOW = 20
+THRESHOLDS = (1.00, 0.99, 0.98, 0.96, 0.94)
+PAPER_THRESHOLDS = (1.00, 0.98, 0.96, 0.94, 0.90)  # north-star: >= 90/94/96/98% of peak
+STABLE_SWEEP_RATES = (0.25, 0.5, 1.0, 2.0, 3.0, 4.0, 6.0, 8.0, 12.0, 16.0, 24.0, 32.0, 40.0, 48.0)
+
+
+@dataclass
+class RequestRecord:
+    index: int
+    arrival_ms: float
+    task_id: int
+    tier_id: int
+    reward: float
+    realized_ms_per_token: float
+    segment_rate: float
+
+
+@dataclass
+class EvalRun:
+    records: list
+    policy_id: str
+    gpu_count: int
+    seed: int
+
+    def rewards(self) -> np.ndarray:
+        return np.array([r.reward for r in self.records])
+
+    def rates(self) -> np.ndarray:
+        return np.array([r.segment_rate for r in self.records])
+
+    def miss_fractions_by_rate(self, spec) -> dict:
+        missed: dict = {}
+        for r in self.records:
+            deadline = spec.tasks[r.task_id].deadline_ms_per_token
+            missed.setdefault(r.segment_rate, []).append(
+                1 if r.realized_ms_per_token > deadline else 0)
+        return {rate: float(np.mean(v)) for rate, v in missed.items()}
+
+    def mean_reward_by_rate(self) -> dict:
+        by_rate: dict = {}
+        for r in self.records:
+            by_rate.setdefault(r.segment_rate, []).append(r.reward)
+        return {rate: float(np.mean(v)) for rate, v in by_rate.items()}
+
+
+@dataclass
+class RolloutOutputs:
+    flags: torch.Tensor            # u8 [E, ld]: tier | miss << 7
+    reward: torch.Tensor           # f64 [E, ld]
+    realized: Optional[torch.Tensor] = None
+    obs: Optional[torch.Tensor] = None    # i32 [E, ld, M]
+    rate: Optional[torch.Tensor] = None   # f64 [E, ld]
+    q: Optional[torch.Tensor] = None      # f64 [E, ld, M]
+
+    @property
+    def tier(self) -> torch.Tensor:
+        return self.flags & 0x7F
+
+    @property
+    def miss(self) -> torch.Tensor:
+        return (self.flags >> 7).to(torch.bool)
+
+
+class GreedyRollout:
+    """Reusable fused rollout for trace batches of a fixed shape.
+
+    Owns the env handle (replica rings) and the output buffers, so repeated
+    runs allocate nothing.  Every run re-initialises the envs in-kernel."""
+
+    def __init__(self, tiers, reward_spec, n_envs: int, ld: int, encoding=None, *,
+                 estimator_mode: str = "estimated", prior_rate: float = 1.0,
+                 reset_between_segments: bool = False, ring_capacity: Optional[int] = None,
+                 skip_ahead: bool = True, want_realized: bool = True, want_steps: bool = False,
+                 device=None):
+        self.device = _lib.require_cuda(device)
+        R = sum(int(t.replicas) for t in tiers)
+        if ring_capacity is None:
+            free, _ = torch.cuda.mem_get_info(self.device)
+            ring_capacity = default_ring_capacity(ld, n_envs, R, budget_bytes=int(free * 0.35))
+        self.env = EnvBatch(tiers, reward_spec, n_envs, encoding, estimator_mode=estimator_mode,
+                            prior_rate=prior_rate, reset_between_segments=reset_between_segments,
+                            ring_capacity=ring_capacity, skip_ahead=skip_ahead, device=self.device)
+        self.n_envs, self.ld, self.M = int(n_envs), int(ld), len(tiers)
+        dev = self.device
+        self.out = RolloutOutputs(
+            flags=torch.zeros((n_envs, ld), dtype=torch.uint8, device=dev),
+            reward=torch.zeros((n_envs, ld), dtype=torch.float64, device=dev),
+            realized=torch.zeros((n_envs, ld), dtype=torch.float64, device=dev) if want_realized else None,
+            obs=torch.zeros((n_envs, ld, self.M), dtype=torch.int32, device=dev) if want_steps else None,
+            rate=torch.zeros((n_envs, ld), dtype=torch.float64, device=dev) if want_steps else None,
+            q=torch.zeros((n_envs, ld, self.M), dtype=torch.float64, device=dev) if want_steps else None)
+
+    def launch(self, trace: TraceBatch, policy=None, static_tier: int = -1,
+               forced: Optional[torch.Tensor] = None, stream=None) -> RolloutOutputs:
+        """Asynchronous: enqueue the fused rollout on `stream` (no sync)."""
+        if trace.n_envs > self.n_envs or trace.ld != self.ld:
+            raise ValueError("trace batch does not match the rollout shape")
+        o = self.out
+        rec = _lib.BeRecords()
+        rec.flags, rec.reward = o.flags.data_ptr(), o.reward.data_ptr()
+        rec.realized = _lib.ptr(o.realized)
+        rec.obs, rec.rate = _lib.ptr(o.obs), _lib.ptr(o.rate)
+        rec.q = _lib.ptr(o.q) if (policy is not None and static_tier < 0 and forced is None) else None
+        w = None
+        if forced is None and static_tier < 0:
+            if policy is None:
+                raise ValueError("need a policy, a static tier or forced actions")
+            self._dn = DeviceQNet.of(policy, self.device)
+            w = self._dn.weights()
+        soa = trace.soa()
+        _lib.check(self.env._L.be_rollout_greedy(self.env.handle, soa, w, int(static_tier),
+                                                 _lib.ptr(forced), rec, _lib.stream_ptr(stream)))
+        return o
+
+    def run(self, trace: TraceBatch, policy=None, static_tier: int = -1,
+            forced: Optional[torch.Tensor] = None, stream=None) -> RolloutOutputs:
+        o = self.launch(trace, policy, static_tier, forced, stream)
+        self.env.check(stream)  # sync + raise on ring overflow / bad action
+        return o
+
+
+def _policy_args(policy, n_tiers):
+    if isinstance(policy, (int, np.integer)) and not isinstance(policy, bool):
+        st = int(policy)
+        if not 0 <= st < n_tiers:
+            raise ValueError(f"static tier {st} out of range")
+        return None, st
+    return policy, -1
+
+
+def run_eval(policy, trace, tiers, reward_spec, encoding=None, seed: int = 0, *,
+             gpu_count: int = 4, estimator_mode: str = "estimated", prior_rate: float = 1.0,
+             reset_between_segments: bool = False, policy_id: Optional[str] = None,
+             device=None) -> EvalRun:
+    """Drop-in for besteffort.evalkit.run_eval (evalkit.py:154-209), on the GPU."""
+    net, static_tier = _policy_args(policy, len(tiers))
+    if static_tier < 0 and encoding is None:
+        encoding = StateEncoding(n_tasks=len(reward_spec.tasks),
+                                 batch_scales=tuple(float(t.max_batch) for t in tiers))
+    if policy_id is None:
+        policy_id = f"static:{static_tier}" if static_tier >= 0 else "policy"
+    tb = TraceBatch.from_traces([trace], device=device)
+    ro = GreedyRollout(tiers, reward_spec, 1, tb.ld, encoding, estimator_mode=estimator_mode,
+                       prior_rate=prior_rate, reset_between_segments=reset_between_segments,
+                       device=device)
+    o = ro.run(tb, net, static_tier)
+    n = len(trace.events)
+    tier = o.tier[0, :n].cpu().numpy()
+    rw = o.reward[0, :n].cpu().numpy()
+    rl = o.realized[0, :n].cpu().numpy()
+    rates = event_rates(trace)
+    records = [RequestRecord(i, ev.time_ms, ev.task_id, int(tier[i]), float(rw[i]), float(rl[i]),
+                             float(rates[i])) for i, ev in enumerate(trace.events)]
+    return EvalRun(records=records, policy_id=policy_id, gpu_count=gpu_count, seed=seed)
+
+
+# --------------------------------------------------------------- reducer
+@dataclass
+class ReduceResult:
+    thresholds: tuple
+    win_counts: torch.Tensor     # i64 [E, n_theta]
+    n_windows: torch.Tensor      # i64 [E]
+    bucket_miss: torch.Tensor    # i64 [E, K]
+    bucket_req: torch.Tensor     # i64 [E, K]
+    bucket_reward: torch.Tensor  # f64 [E, K] (sequential per env)
+
+    def totals(self) -> dict:
+        """Whole-batch stats (int64 sums are exact; reward sums in env order)."""
+        wc = self.win_counts.sum(0).cpu().numpy()
+        nw = int(self.n_windows.sum())
+        miss = self.bucket_miss.sum(0).cpu().numpy()
+        req = self.bucket_req.sum(0).cpu().numpy()
+        rws = self.bucket_reward.cpu().numpy().sum(0)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            return dict(
+                thresholds=list(self.thresholds), win_counts=wc.tolist(), n_windows=nw,
+                window_fraction=(wc / max(nw, 1)).tolist(),
+                requests=req.tolist(), misses=miss.tolist(),
+                availability=(1.0 - miss / np.maximum(req, 1)).tolist(),
+                mean_reward=(rws / np.maximum(req, 1)).tolist())
+
+
+def reduce_eval(trace: TraceBatch, flags: torch.Tensor, reward: torch.Tensor,
+                thresholds: Sequence[float] = THRESHOLDS, n_buckets: int = 1,
+                window: int = WINDOW, stream=None) -> ReduceResult:
+    """On-device windowed + threshold_counts + per-bucket miss/request/reward."""
+    E, dev = trace.n_envs, trace.device
+    th = torch.tensor(list(thresholds), dtype=torch.float64)  # host array: taus computed on host
+    K = int(n_buckets)
+    out = ReduceResult(tuple(thresholds),
+                       torch.empty((E, len(thresholds)), dtype=torch.int64, device=dev),
+                       torch.empty(E, dtype=torch.int64, device=dev),
+                       torch.empty((E, K), dtype=torch.int64, device=dev),
+                       torch.empty((E, K), dtype=torch.int64, device=dev),
+                       torch.empty((E, K), dtype=torch.float64, device=dev))
+    L = _lib.load()
+    _lib.check(L.be_reduce_eval(trace.soa(), flags.data_ptr(), reward.data_ptr(), int(window),
+                                th.data_ptr(), len(thresholds), K, out.win_counts.data_ptr(),
+                                out.n_windows.data_ptr(), out.bucket_miss.data_ptr(),
+                                out.bucket_req.data_ptr(), out.bucket_reward.data_ptr(),
+                                _lib.stream_ptr(stream)))
+    return out
+
+
+def run_eval_batch(policy, traces: Union[TraceBatch, Sequence], tiers, reward_spec, encoding=None,
+                   *, estimator_mode: str = "estimated", prior_rate: float = 1.0,
+                   reset_between_segments: bool = False, thresholds=THRESHOLDS,
+                   buckets: Optional[Sequence[float]] = None, ring_capacity: Optional[int] = None,
+                   device=None):
+    """run_eval over many envs at once + the on-device reducer.
+    Returns (RolloutOutputs, ReduceResult)."""
+    net, static_tier = _policy_args(policy, len(tiers))
+    if static_tier < 0 and encoding is None:
+        encoding = StateEncoding(n_tasks=len(reward_spec.tasks),
+                                 batch_scales=tuple(float(t.max_batch) for t in tiers))
+    tb = traces if isinstance(traces, TraceBatch) else TraceBatch.from_traces(
+        list(traces), device=device, buckets=buckets)
+    ro = GreedyRollout(tiers, reward_spec, tb.n_envs, tb.ld, encoding,
+                       estimator_mode=estimator_mode, prior_rate=prior_rate,
+                       reset_between_segments=reset_between_segments,
+                       ring_capacity=ring_capacity, device=device)
+    o = ro.run(tb, net, static_tier)
+    K = 1 if buckets is None else len(buckets)
+    red = reduce_eval(tb, o.flags, o.reward, thresholds, K)
+    return o, red

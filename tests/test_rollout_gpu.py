@@ -1,0 +1,121 @@
+"""Parity of the fused GPU rollout (be_rollout_greedy) with the reference
+(golden records) and the CPU oracle.  Bit-exact: routing decisions, queue
+lengths (obs), rate signal, rewards, realized latency, deadline misses.
+Q-values: |dQ| <= 1e-9 (fp64; OpenBLAS order not reproducible)."""
+import numpy as np
+import pytest
+import torch
+
+import goldens
+from helpers import enc_of, first_diff, oracle_run, reward_of, tiers_of
+from paper_2401_07886_b200 import (CapacityError, GreedyRollout, QNetwork, TraceBatch,
+                                   reduce_eval, run_eval)
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+NAMES = goldens.names()
+
+
+def gpu_run(g, skip=True, want_steps=True, n_copies=1, ring_capacity=None, forced=None):
+    m = g["meta"]
+    arr = np.tile(g["arrival"], (n_copies, 1))
+    tsk = np.tile(g["task"], (n_copies, 1))
+    ss = [list(g["seg_start"])] * n_copies
+    sr = [list(g["seg_rate"])] * n_copies
+    tb = TraceBatch.from_arrays(arr, tsk, ss, sr)
+    ro = GreedyRollout(tiers_of(m), reward_of(m), n_copies, tb.ld, enc_of(m),
+                       estimator_mode=m["estimator_mode"], reset_between_segments=m["reset"],
+                       skip_ahead=skip, want_steps=want_steps, ring_capacity=ring_capacity)
+    net = goldens.net_for(m)
+    f = None if forced is None else torch.as_tensor(np.tile(forced, (n_copies, 1)), device="cuda")
+    if f is not None:
+        return ro.run(tb, forced=f), tb
+    if net is None:
+        return ro.run(tb, static_tier=m["static_tier"]), tb
+    return ro.run(tb, QNetwork.from_any(net)), tb
+
+
+def assert_env_equal(o, e, g, check_q=True):
+    n = len(g["arrival"])
+    tier = o.tier[e, :n].cpu().numpy()
+    i = first_diff(tier, g["tier"])
+    if i >= 0:
+        pytest.fail(f"tier differs first at request {i} (fp64 ref margin {g['margin'][i]:.3g})")
+    assert np.array_equal(o.reward[e, :n].cpu().numpy(), g["reward"])
+    assert np.array_equal(o.realized[e, :n].cpu().numpy(), g["realized"])
+    dl = np.array([t["deadline"] for t in g["meta"]["reward"]["tasks"]])
+    miss = g["realized"] > dl[g["task"]]
+    assert np.array_equal(o.miss[e, :n].cpu().numpy(), miss)
+    if o.obs is not None:
+        assert np.array_equal(o.obs[e, :n].cpu().numpy(), g["obs"])
+        assert np.array_equal(o.rate[e, :n].cpu().numpy(), g["rate"])
+        if check_q and g["meta"]["static_tier"] < 0:
+            assert np.max(np.abs(o.q[e, :n].cpu().numpy() - g["q"])) < 1e-9
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_rollout_matches_reference(cuda, name):
+    g = goldens.load(name)
+    o, _ = gpu_run(g)
+    assert_env_equal(o, 0, g)
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if "static" in n or "quantized" in n])
+def test_rollout_without_skip_matches(cuda, name):
+    g = goldens.load(name)
+    o, _ = gpu_run(g, skip=False)
+    assert_env_equal(o, 0, g)
+
+
+@pytest.mark.parametrize("name", ["unpredictable-1_mixed2", "stable_static2", "unpredictable-2_static2"])
+def test_rollout_batch_of_copies(cuda, name):
+    g = goldens.load(name)
+    o, _ = gpu_run(g, n_copies=257, want_steps=False)
+    for e in (0, 1, 128, 256):
+        assert_env_equal(o, e, g)
+    t = o.tier[:, :len(g["arrival"])]
+    assert bool((t == t[0:1]).all())
+
+
+def test_forced_actions_match_oracle(cuda):
+    g = goldens.load("unpredictable-1_mixed1")
+    forced = np.random.default_rng(1).integers(0, 3, size=len(g["arrival"])).astype(np.uint8)
+    o, _ = gpu_run(g, forced=forced)
+    ref = oracle_run(g, forced_actions=forced, net=None)
+    assert np.array_equal(o.tier[0].cpu().numpy(), forced)
+    assert np.array_equal(o.reward[0].cpu().numpy(), ref["reward"])
+    assert np.array_equal(o.obs[0].cpu().numpy(), ref["obs"])
+
+
+def test_ring_overflow_raises(cuda):
+    g = goldens.load("unpredictable-2_static2")  # large tier floods: queues grow to ~hundreds
+    with pytest.raises(CapacityError):
+        gpu_run(g, ring_capacity=8, want_steps=False)
+
+
+def test_run_eval_dropin_records(cuda):
+    g = goldens.load("hellaswag-copa-soft_mixed0")
+    m = g["meta"]
+    from paper_2401_07886_b200.specs import ArrivalEvent, SegmentMark, WorkloadTrace
+    tr = WorkloadTrace([ArrivalEvent(float(t), int(k)) for t, k in zip(g["arrival"], g["task"])],
+                       [SegmentMark(int(a), float(b)) for a, b in zip(g["seg_start"], g["seg_rate"])], 0)
+    run = run_eval(QNetwork.from_any(goldens.net_for(m)), tr, tiers_of(m), reward_of(m), enc_of(m),
+                   estimator_mode=m["estimator_mode"], reset_between_segments=m["reset"])
+    assert [r.tier_id for r in run.records] == g["tier"].tolist()
+    assert [r.reward for r in run.records] == g["reward"].tolist()
+    assert [r.realized_ms_per_token for r in run.records] == g["realized"].tolist()
+    assert sorted(run.miss_fractions_by_rate(reward_of(m)).items()) == [tuple(x) for x in m["miss_by_rate"]]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_reducer_matches_reference(cuda, name):
+    g = goldens.load(name)
+    m = g["meta"]
+    o, tb = gpu_run(g, want_steps=False)
+    red = reduce_eval(tb, o.flags, o.reward, thresholds=m["thresholds"])
+    assert red.win_counts[0].cpu().tolist() == m["counts"]
+    assert int(red.n_windows[0]) == m["n_windows"]
+    dl = np.array([t["deadline"] for t in m["reward"]["tasks"]])
+    assert int(red.bucket_miss[0, 0]) == int(np.sum(g["realized"] > dl[g["task"]]))
+    assert int(red.bucket_req[0, 0]) == len(g["arrival"])
+    assert float(red.bucket_reward[0, 0]) == pytest.approx(float(np.sum(g["reward"])), rel=1e-12)
