@@ -1,0 +1,377 @@
+"""bench.py — simulated env-steps/s of the greedy-DQN rollout (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3]): per GPU 65,536
+independent serving environments (3 tiers x 4 replicas, 4 tasks, hard 40
+ms/token deadlines — the shipped config), each a stable Poisson trace of
+10,000 requests at load L x 3 req/s with L = 1 + (global env id mod 10)
+(3 req/s = the large tier's static collapse rate), true-rate estimator,
+greedy routing by the reference-trained DQN (tests/golden/trained_seed7.beqn,
+200k iterations of the reference trainer, seed 7).  One step = one full
+rollout of every env over its trace (fused kernel) + the evaluation reducer
+(windows >= 0.90/0.94/0.96/0.98 and == 1.00 of peak, availability per load).
+Traces are generated on device (Philox) and exceed L2 (5.9 GB per GPU).
+
+Arms:
+  default            our CUDA path; prints the contract JSON line
+  --impl reference   the reference's own CPU implementation (besteffort.run_eval
+                     from baseline/_ref, fallback: the C oracle port) on all host
+                     cores, bounded sample per step
+Multi-GPU: torchrun, one process per GPU, envs sharded by global id (no data-path
+collective), int64/f64 statistics all-reduced once at the end; weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LOAD_BASE = 3.0       # req/s: large-tier static collapse rate (criterion 5)
+N_LOADS = 10
+N_TASKS = 4
+POLICY = os.path.join(ROOT, "tests", "golden", "trained_seed7.beqn")
+THRESHOLDS = (1.00, 0.98, 0.96, 0.94, 0.90)
+ALG_BYTES_STEP = 18   # arrival f64 + task u8 + action/flags u8 + reward f64
+ALG_BYTES_REDUCE = 9  # reward f64 + flags u8 per request
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--envs", type=int, default=65536, help="environments per GPU")
+    ap.add_argument("--requests", type=int, default=10000)
+    ap.add_argument("--seed", type=int, default=2401)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def load_rates(gids):
+    return [LOAD_BASE * (1 + (g % N_LOADS)) for g in gids]
+
+
+# ----------------------------------------------------------------- CPU side
+def _ref_worker(args):
+    """One host process: the reference run_eval over a slice of env traces."""
+    (arrs, tasks, rates, deadline_s, ref_path) = args
+    import numpy as np  # noqa: F401
+    sys.path.insert(0, ref_path)
+    from besteffort.config import parse_config
+    from besteffort.evalkit import run_eval
+    from besteffort.policy import load_checkpoint
+    from besteffort.workload import ArrivalEvent, SegmentMark, WorkloadTrace
+    cfg = parse_config()
+    net = load_checkpoint(POLICY)
+    steps = 0
+    t0 = time.perf_counter()
+    for a, k, r in zip(arrs, tasks, rates):
+        tr = WorkloadTrace([ArrivalEvent(float(x), int(y)) for x, y in zip(a, k)],
+                           [SegmentMark(0, float(r))], seed=0)
+        run_eval(net, tr, cfg.tiers(), cfg.reward_spec(), cfg.encoding(),
+                 estimator_mode="true-rate")
+        steps += len(a)
+        if time.perf_counter() - t0 > deadline_s:
+            break
+    return steps, time.perf_counter() - t0
+
+
+def _oracle_worker(args):
+    (arrs, tasks, rates, deadline_s, _) = args
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    from oracle import oracle
+    from paper_2401_07886_b200.specs import DEFAULT_TIERS, load_checkpoint, RewardSpec
+    net = load_checkpoint(POLICY)
+    rw = RewardSpec.default()
+    steps = 0
+    t0 = time.perf_counter()
+    for a, k, r in zip(arrs, tasks, rates):
+        oracle.run_eval_oracle(tiers=DEFAULT_TIERS, reward=rw, arrival=a, task=k, seg_start=[0],
+                               seg_rate=[r], net=net, estimator_mode="true-rate", want_steps=False)
+        steps += len(a)
+        if time.perf_counter() - t0 > deadline_s:
+            break
+    return steps, time.perf_counter() - t0
+
+
+def host_traces(n_envs, n, seed, gid0=0):
+    """Host-generated traces of the same workload (reference gen_stable, PCG64)."""
+    import numpy as np
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "besteffort")):
+        sys.path.insert(0, ref)
+        from besteffort.workload import gen_stable
+        out = []
+        for g in range(gid0, gid0 + n_envs):
+            rate = LOAD_BASE * (1 + g % N_LOADS)
+            tr = gen_stable([rate], math.ceil(n / rate * 1.1), N_TASKS, seed * 1000003 + g)
+            out.append((np.array([e.time_ms for e in tr.events[:n]]),
+                        np.array([e.task_id for e in tr.events[:n]], np.uint8), rate))
+        return out
+    rng = np.random.default_rng(seed)
+    out = []
+    for g in range(gid0, gid0 + n_envs):
+        rate = LOAD_BASE * (1 + g % N_LOADS)
+        out.append((np.cumsum(rng.exponential(1000.0 / rate, n)),
+                    rng.integers(0, N_TASKS, n).astype(np.uint8), rate))
+    return out
+
+
+def cpu_rollout(samples, seconds, procs=None):
+    """Time the reference CPU path on `procs` host processes (one per core)."""
+    import multiprocessing as mp
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    kind = "reference" if os.path.isdir(os.path.join(ref, "besteffort")) else "port"
+    worker = _ref_worker if kind == "reference" else _oracle_worker
+    procs = procs or len(os.sched_getaffinity(0))
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    os.environ["OMP_NUM_THREADS"] = "1"
+    chunks = [([], [], []) for _ in range(procs)]
+    for i, (a, k, r) in enumerate(samples):
+        c = chunks[i % procs]
+        c[0].append(a)
+        c[1].append(k)
+        c[2].append(r)
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        pool.map(abs, range(procs))  # warm the workers (imports happen per task below)
+        t0 = time.perf_counter()
+        res = pool.map(worker, [(c[0], c[1], c[2], seconds, ref) for c in chunks])
+        wall = time.perf_counter() - t0
+    steps = sum(s for s, _ in res)
+    return dict(value=steps / wall, unit="env-steps/s", cores=procs, kind=kind,
+                sample=f"{steps} env-steps ({len(samples)} envs max, 10k requests each, "
+                       f"load 1x-10x) on {procs} processes, {wall:.1f}s wall, "
+                       f"{'besteffort.run_eval (baseline/_ref)' if kind == 'reference' else 'oracle C port'}")
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = len(os.sched_getaffinity(0))
+    per_step = []
+    samples = host_traces(procs * 3, a.requests, a.seed)
+    seconds = max(2.0, min(8.0, 150.0 / max(1, a.steps + a.warmup)))
+    for i in range(a.warmup + a.steps):
+        r = cpu_rollout(samples, seconds, procs)
+        if i >= a.warmup:
+            per_step.append(r)
+    v = statistics.median(r["value"] for r in per_step)
+    line = dict(metric="simulated env-steps/sec (greedy DQN rollout, 65536 envs)", value=v,
+                unit="env-steps/s", impl="reference", n_gpus=a.gpus, steps=a.steps,
+                warmup=a.warmup, higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="f64", data="synthetic",
+                config=dict(workload="config4: 65536 envs/GPU x 10k requests, stable Poisson at "
+                                     "1x-10x of 3 req/s, 3 tiers x 4 replicas, 4 tasks, trained DQN",
+                            sample_per_step=per_step[-1]["sample"]),
+                cpu_baseline=dict(value=v, unit="env-steps/s", cores=per_step[-1]["cores"],
+                                  kind=per_step[-1]["kind"], sample=per_step[-1]["sample"]),
+                e2e=dict(value=v, unit="env-steps/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU side
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=mx,
+                    reasons=sorted(reasons), samples=len(sm))
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2401_07886_b200 import (GreedyRollout, RewardSpec, StateEncoding, TraceBatch,
+                                       default_tiers, load_checkpoint, reduce_eval)
+    from paper_2401_07886_b200.evalkit import StreamingEvaluator, pin_trace
+    from paper_2401_07886_b200 import sharding
+
+    E, N = a.envs, a.requests
+    gid0 = rank * E
+    gids = list(range(gid0, gid0 + E))
+    tiers, rw = default_tiers(), RewardSpec.default()
+    enc = StateEncoding(N_TASKS, tuple(float(t.max_batch) for t in tiers))
+    net = load_checkpoint(POLICY)
+    tb = TraceBatch.generate_stable(load_rates(gids), N, N_TASKS, a.seed, device=dev,
+                                    buckets=[g % N_LOADS for g in gids], env_offset=gid0)
+    ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False,
+                       device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        o = ro.launch(tb, net)
+        return o, reduce_eval(tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
+
+    for _ in range(a.warmup):
+        step()
+    ro.env.check()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(a.steps):
+            ev[k][0].record(stream)
+            o = ro.launch(tb, net)
+            ev[k][1].record(stream)
+            red = reduce_eval(tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
+            ev[k][2].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ro.env.check()
+    ms = t_start.elapsed_time(t_end)
+    rollout_ms = [e[0].elapsed_time(e[1]) for e in ev]
+    reduce_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms = sharding.max_over_ranks(ms, dev) if world > 1 else ms
+    ms_step = ms / a.steps
+    value = world * E * N / (ms_step / 1e3)
+    stats = sharding.reduce_stats(red, dev) if world > 1 else red.totals()
+
+    # ------------------------------------------------ end to end (host buffers)
+    host = pin_trace(tb)
+    se = StreamingEvaluator(net, tiers, rw, E, N, enc, estimator_mode="true-rate",
+                            thresholds=THRESHOLDS, n_buckets=N_LOADS, device=dev)
+    se.result(se.submit(host))  # warm
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hs = [se.submit(host) for _ in range(a.steps)]
+    for h in hs:
+        se.result(h)
+    e2e_s = time.perf_counter() - t0
+    e2e_s = sharding.max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
+    e2e = dict(value=world * E * N * a.steps / e2e_s, unit="env-steps/s",
+               h2d_bytes_per_step=se.h2d_bytes, d2h_bytes_per_step=se.d2h_bytes,
+               note="pinned host traces -> H2D (copy stream, double-buffered) -> fused rollout "
+                    "-> reducer -> D2H of the statistics, host wall clock incl. syncs")
+    del se, host
+
+    # ------------------------------------------------ roofline (rollout = dominant kernel)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    r_ms = statistics.mean(rollout_ms)
+    achieved = ALG_BYTES_STEP * E * N / (r_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        pj = json.load(open(prof))
+        k = pj.get("kernels", {}).get("rollout", {})
+        if k.get("envs") == E and k.get("requests") == N:
+            traffic = k.get("dram_bytes")
+    red_ms = statistics.mean(reduce_ms)
+    red_gbs = ALG_BYTES_REDUCE * E * N / (red_ms / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        procs = len(os.sched_getaffinity(0))
+        # the same workload bits: device-generated traces of the first envs
+        arr = tb.arrival[: procs * 3].cpu().numpy()
+        tsk = tb.task[: procs * 3].cpu().numpy()
+        samples = [(arr[i], tsk[i], load_rates([i])[0]) for i in range(arr.shape[0])]
+        cpu = cpu_rollout(samples, a.cpu_seconds, procs)
+
+    if rank == 0:
+        line = dict(
+            metric="simulated env-steps/sec (greedy DQN rollout, 65536 envs)", value=value,
+            unit="env-steps/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
+            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None,
+            dtype="f64", data="synthetic (on-device Philox gen_stable traces; reference-trained DQN)",
+            config=dict(workload=f"config4: {E} envs/GPU x {N} requests, stable Poisson at "
+                                 f"1x-10x of {LOAD_BASE:g} req/s, 3 tiers x 4 replicas, 4 tasks, "
+                                 "hard 40 ms/token, true-rate estimator, greedy trained DQN (fp64)",
+                        envs_per_gpu=E, requests_per_env=N, total_envs=world * E,
+                        parallelism=f"env-sharded dp{world}", l2="inputs larger than L2 (5.9 GB traces/GPU)",
+                        step="fused rollout kernel + evaluation reducer"),
+            gpu_launches=2 * a.steps,
+            roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
+                          frac=achieved / hbm_peak, traffic=traffic, peak_source=peak_src,
+                          kernel="rollout_kernel<3>", algorithmic_bytes_per_env_step=ALG_BYTES_STEP,
+                          note="env step is issue/latency-bound (serial fp64 event recurrence), "
+                               "not HBM-bound; see DESIGN.md §5"),
+            reducer_roofline=dict(bound="hbm", achieved=red_gbs, peak=hbm_peak, unit="GB/s",
+                                  frac=red_gbs / hbm_peak, ms=red_ms,
+                                  algorithmic_bytes_per_request=ALG_BYTES_REDUCE),
+            kernel_ms=dict(rollout=r_ms, reduce=red_ms),
+            e2e=e2e, cpu_baseline=cpu, clocks=clk.summary(),
+            results=dict(load_multipliers=list(range(1, N_LOADS + 1)), **stats))
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

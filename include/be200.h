@@ -178,12 +178,12 @@ int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const do
                        void* stream);
 
 /* On-device gen_stable (workload.py:120-141) with Philox4x32-10 keyed by
- * (seed, env): per env one Poisson segment at rate[e] req/s, exponential gaps
+ * (seed, env_offset + e): per env one Poisson segment at rate[e] req/s, exponential gaps
  * of mean 1000/rate ms accumulated sequentially in fp64, uniform task ids;
  * the first n events of the segment (truncated).  Writes arrival/task [E][ld]. */
-int32_t be_trace_gen_stable(int32_t n_envs, int64_t n, int64_t ld, const double* rate,
-                            int32_t n_tasks, uint64_t seed, double* arrival_ms, uint8_t* task,
-                            void* stream);
+int32_t be_trace_gen_stable(int32_t n_envs, int64_t env_offset, int64_t n, int64_t ld,
+                            const double* rate, int32_t n_tasks, uint64_t seed,
+                            double* arrival_ms, uint8_t* task, void* stream);
 
 #ifdef __cplusplus
 }

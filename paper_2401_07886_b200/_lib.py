@@ -90,7 +90,7 @@ SIGNATURES = {
                                  _P, _P, _P]),
     "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
                               _P, _P, _P]),
-    "be_trace_gen_stable": (_I32, [_I32, _I64, _I64, _P, _I32, _U64, _P, _P, _P]),
+    "be_trace_gen_stable": (_I32, [_I32, _I64, _I64, _I64, _P, _I32, _U64, _P, _P, _P]),
 }
 
 _lib = None

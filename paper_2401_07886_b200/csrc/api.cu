@@ -22,6 +22,13 @@ int set_cuda_error(cudaError_t e, const char* where) {
     return BE_ECUDA;
 }
 
+void make_score_aux(const be_cfg& c, ScoreAux* aux) {
+    for (int k = 0; k < BE_MAX_TASKS * BE_MAX_TIERS; ++k) aux->hit_tau[k] = -INFINITY;
+    for (int t = 0; t < c.n_tasks; ++t)
+        for (int m = 0; m < c.n_tiers; ++m)
+            aux->hit_tau[t * BE_MAX_TIERS + m] = tau_le(c.deadline[t], (double)c.tiers[m].tokens_per_request);
+}
+
 static int validate_cfg(const be_cfg* c, int* lanes) {
     if (!c) return set_error(BE_EINVAL, "cfg is NULL");
     if (c->n_tiers < 1 || c->n_tiers > BE_MAX_TIERS)
@@ -247,13 +254,14 @@ int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const do
                          n_windows, bucket_miss, bucket_req, bucket_reward, (cudaStream_t)stream);
 }
 
-int32_t be_trace_gen_stable(int32_t n_envs, int64_t n, int64_t ld, const double* rate,
-                            int32_t n_tasks, uint64_t seed, double* arrival_ms, uint8_t* task,
-                            void* stream) {
+int32_t be_trace_gen_stable(int32_t n_envs, int64_t env_offset, int64_t n, int64_t ld,
+                            const double* rate, int32_t n_tasks, uint64_t seed,
+                            double* arrival_ms, uint8_t* task, void* stream) {
     if (!rate || !arrival_ms || !task) return set_error(BE_EINVAL, "NULL argument");
-    if (n_envs < 1 || n < 0 || ld < n || n_tasks < 1 || n_tasks > 255)
+    if (n_envs < 1 || n < 0 || ld < n || n_tasks < 1 || n_tasks > 255 || env_offset < 0)
         return set_error(BE_EINVAL, "bad sizes");
-    return launch_tracegen(n_envs, n, ld, rate, n_tasks, seed, arrival_ms, task, (cudaStream_t)stream);
+    return launch_tracegen(n_envs, env_offset, n, ld, rate, n_tasks, seed, arrival_ms, task,
+                           (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "be200.h"
+#include "be_internal.h"
 
 namespace be {
 
@@ -62,10 +63,16 @@ struct Score {
     double deadline[BE_MAX_TASKS];
     double cut[BE_MAX_TASKS];  // cutoff_fraction * deadline (reward.py:108)
     double matrix[BE_MAX_TASKS * BE_MAX_TIERS];
+    // hit_tau[t][m]: largest x with RN(x / tokens_m) <= deadline_t, so that for a
+    // hard deadline "realized <= deadline" is exactly "(t_end - arrival) <= hit_tau"
+    // (RN(x / c) is monotone in x) and no division is needed (host-computed).
+    double hit_tau[BE_MAX_TASKS * BE_MAX_TIERS];
     int soft[BE_MAX_TASKS];
     double decay;
     int M;
 };
+
+
 
 struct RecOut {
     uint8_t* flags;
@@ -74,9 +81,10 @@ struct RecOut {
     int64_t base;  // e * ld
 };
 
-__device__ __forceinline__ void load_score(Score& s, const be_cfg& c) {
+__device__ __forceinline__ void load_score(Score& s, const be_cfg& c, const ScoreAux& aux) {
     // called by a single warp; caller syncs
     int lane = threadIdx.x & 31;
+    for (int k = lane; k < BE_MAX_TASKS * BE_MAX_TIERS; k += 32) s.hit_tau[k] = aux.hit_tau[k];
     for (int k = lane; k < BE_MAX_TASKS; k += 32) {
         s.deadline[k] = c.deadline[k];
         s.cut[k] = __dmul_rn(c.cutoff_fraction, c.deadline[k]);
@@ -123,9 +131,18 @@ __device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane) {
 // reward (reward.py:94-126), deadline miss (evalkit.py:65-67).
 __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Score& sc,
                                          const RecOut& o, double t_end) {
-    double realized = __ddiv_rn(__dsub_rn(t_end, r.h_arr), (double)tc.tokens);
     int task = (int)(r.h_idtask >> 24);
     int64_t id = (int64_t)(r.h_idtask & 0xffffffu);
+    const double span = __dsub_rn(t_end, r.h_arr);
+    if (!sc.soft[task] && !o.realized) {
+        // hard deadline, realized not requested: weight_hard (reward.py:94-96) via the
+        // exact division-free threshold
+        const bool hit = span <= sc.hit_tau[task * BE_MAX_TIERS + tc.tier];
+        o.reward[o.base + id] = hit ? sc.matrix[task * BE_MAX_TIERS + tc.tier] : 0.0;
+        o.flags[o.base + id] = (uint8_t)(tc.tier | (hit ? 0 : 0x80));
+        return;
+    }
+    double realized = __ddiv_rn(span, (double)tc.tokens);
     double dl = sc.deadline[task];
     double w;
     if (!sc.soft[task]) {
@@ -189,24 +206,59 @@ __device__ __forceinline__ bool scaled_round(double x, int e, long long& out) {
     return true;
 }
 
+// floor(x / d) for 0 <= x < 2^53, 1 <= d: reciprocal estimate + exact integer fix-up
+// (a 64-bit integer division is a ~70-instruction software sequence on the GPU).
+__device__ __forceinline__ long long div_floor(long long x, long long d, double inv_d) {
+    long long q = (long long)((double)x * inv_d);
+    long long rem = x - q * d;
+    while (rem < 0) {
+        --q;
+        rem += d;
+    }
+    while (rem >= d) {
+        ++q;
+        rem -= d;
+    }
+    return q;
+}
+
 // Number k <= kmax of whole START->END cycles that can be jumped from a START
 // at time t (t < until) with constant increment; writes the time after k cycles.
-__device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int kmax,
-                                           double until, double& t_out) {
+// Per-lane cache of the binade increment d = a + b (and 1/d), valid for one
+// (binade exponent, batch size) pair: recomputed only when either changes.
+struct SkipCache {
+    int e;       // biased exponent of the binade, -1 = empty
+    int n;       // n_active the increment was computed for
+    long long d; // increment in units of u; <= 0 = skipping impossible here
+    double inv_d;
+};
+
+__device__ __forceinline__ void skip_cache_reset(SkipCache& s) {
+    s.e = -1;
+    s.n = -1;
+    s.d = 0;
+    s.inv_d = 0.0;
+}
+
+__device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int n, int kmax,
+                                           double until, double& t_out, SkipCache& sc) {
     long long bits = __double_as_longlong(t);
     int ext = (int)((bits >> 52) & 0x7ff);
     if (kmax <= 0 || ext == 0 || ext == 0x7ff || bits < 0) return 0;
     int e = ext - 1023;
     long long T0 = (bits & 0xfffffffffffffLL) | (1LL << 52);
-    long long a, b;
-    if (!scaled_round(alpha, e, a) || !scaled_round(c, e, b)) return 0;
-    long long d = a + b;
+    if (ext != sc.e || n != sc.n) {
+        long long a, b;
+        sc.e = ext;
+        sc.n = n;
+        sc.d = (scaled_round(alpha, e, a) && scaled_round(c, e, b)) ? a + b : 0;
+        sc.inv_d = sc.d > 0 ? __drcp_rn((double)sc.d) : 0.0;
+    }
+    const long long d = sc.d;
     if (d <= 0) return 0;
     const long long TOP = 1LL << 53;
-    long long lim = TOP - 2 - T0;  // T0 + k d <= 2^53 - 2 keeps every operand in the binade
-    if (lim < d) return 0;
-    long long k = lim / d;
-    // horizon: the k-th END must satisfy t_k <= until
+    long long x = TOP - 2 - T0;  // T0 + k d <= 2^53 - 2 keeps every operand in the binade
+    // horizon: the k-th END must satisfy t_k <= until, i.e. k d <= floor(until/u) - T0
     long long ub = __double_as_longlong(until);
     int exu = (int)((ub >> 52) & 0x7ff);
     if (exu != 0x7ff) {  // finite
@@ -214,11 +266,17 @@ __device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int
         if (sh < 0) return 0;
         if (sh < 10) {
             long long mu = (ub & 0xfffffffffffffLL) | (1LL << 52);
-            long long ui = mu << sh;  // floor(until / u): exact integer
-            long long ku = (ui - T0) / d;
-            if (ku < k) k = ku;
+            long long xu = (mu << sh) - T0;  // floor(until / u) - T0: exact
+            if (xu < x) x = xu;
         }
     }
+    if (x < d) return 0;
+    long long k;
+    unsigned long long lo = (unsigned long long)kmax * (unsigned long long)d;
+    if (__umul64hi((unsigned long long)kmax, (unsigned long long)d) == 0 && lo <= (unsigned long long)x)
+        k = kmax;  // common case: the next completion comes first (no division)
+    else
+        k = div_floor(x, d, sc.inv_d);
     if (k > kmax) k = kmax;
     if (k <= 0) return 0;
     long long Tk = T0 + k * d;
@@ -233,7 +291,7 @@ __device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int
 // Returns false if the iteration counter would overflow.
 __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double until, Slot* ring,
                                              uint32_t mask, const Score& sc, const RecOut& o,
-                                             bool skip) {
+                                             bool skip, SkipCache& skc) {
     while (r.kind != K_NONE) {
         if (r.kind == K_START) {
             if (!(r.t < until)) break;
@@ -248,7 +306,8 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
             if (skip) {
                 int K = r.h_join + tc.tokens - r.iters;  // ENDs until the head completes
                 double tn;
-                int k = skip_cycles(r.t, tc.alpha, c, min(K - 1, (1 << 30) - r.iters), until, tn);
+                int k = skip_cycles(r.t, tc.alpha, c, n_active, min(K - 1, (1 << 30) - r.iters), until,
+                                    tn, skc);
                 if (k > 0) {
                     r.t = tn;
                     r.iters += k;
@@ -350,6 +409,40 @@ __device__ __forceinline__ double estimator_observe(Estimator& est, double t, bo
 // lane l owns hidden units j = l + 32k.  Weights in shared memory:
 // sW1 [D][H] (as BEQN1), sb1 [H], sW2t [M][H] (transposed), sb2 [M].
 // Result q[] is bit-identical on every lane (xor-butterfly sums commute).
+// Same forward over a group of LPE lanes (LPE = 16: two environments per
+// warp); lane g of the group owns hidden units j = g + LPE k.
+template <int M, int LPE>
+__device__ __forceinline__ void qnet_group(const double* __restrict__ sW1,
+                                           const double* __restrict__ sW2t,
+                                           const double* __restrict__ sb2, int T, int H, int task,
+                                           const double (&xt)[M], double xr, double (&q)[M]) {
+    const int g = threadIdx.x & (LPE - 1);
+    double acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = 0.0;
+    const double* wtask = sW1 + task * H;
+    const double* wtier = sW1 + T * H;
+    const double* wrate = sW1 + (T + M) * H;
+#pragma unroll 4
+    for (int j = g; j < H; j += LPE) {
+        double pre = wtask[j];  // W1[task][j] + b1[j] (folded at staging)
+#pragma unroll
+        for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], wtier[m * H + j], pre);
+        pre = __fma_rn(xr, wrate[j], pre);
+        const long long pb = __double_as_longlong(pre);
+        const double h = __longlong_as_double(pb & ~(pb >> 63));  // relu
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
+    }
+#pragma unroll
+    for (int off = LPE / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = __dadd_rn(acc[m], __shfl_xor_sync(FULL, acc[m], off));
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) q[m] = __dadd_rn(acc[m], sb2[m]);
+}
+
 template <int M>
 __device__ __forceinline__ void qnet_warp(const double* __restrict__ sW1,
                                           const double* __restrict__ sb1,
@@ -368,9 +461,11 @@ __device__ __forceinline__ void qnet_warp(const double* __restrict__ sW1,
         double pre = wtask[j];
 #pragma unroll
         for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], wtier[m * H + j], pre);
-        pre = __fma_rn(xr, wrate[j], pre);
-        pre = __dadd_rn(pre, sb1[j]);
-        double h = pre > 0.0 ? pre : 0.0;
+        pre = __fma_rn(xr, wrate[j], pre);  // b1 is folded into the task rows
+        // relu by sign-mask (3 integer ops instead of a compare/select chain);
+        // equals max(pre, 0) for every non-NaN input
+        const long long pb = __double_as_longlong(pre);
+        const double h = __longlong_as_double(pb & ~(pb >> 63));
 #pragma unroll
         for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
     }
@@ -387,16 +482,14 @@ __device__ __forceinline__ void qnet_warp(const double* __restrict__ sW1,
 template <int M>
 __device__ __forceinline__ int argmax_first(const double (&q)[M]) {
     int best = 0;
-    bool nan_seen = q[0] != q[0];
+    double bv = q[0];
+    bool nan_seen = bv != bv;
 #pragma unroll
     for (int m = 1; m < M; ++m) {
-        if (nan_seen) break;
-        if (q[m] != q[m]) {
-            best = m;
-            nan_seen = true;
-        } else if (q[m] > q[best]) {
-            best = m;
-        }
+        const bool take = !nan_seen && (q[m] != q[m] || q[m] > bv);
+        nan_seen = nan_seen || q[m] != q[m];
+        best = take ? m : best;
+        bv = take ? q[m] : bv;
     }
     return best;
 }

@@ -22,6 +22,13 @@ struct be_env {
 };
 
 namespace be {
+// Host-side derived reward constants shipped in kernel parameters (see Score).
+struct ScoreAux {
+    double hit_tau[BE_MAX_TASKS * BE_MAX_TIERS];
+};
+void make_score_aux(const be_cfg& c, ScoreAux* aux);
+double tau_le(double theta, double w);
+double tau_ge(double theta, double w);
 int set_error(int code, const char* msg);
 int set_cuda_error(cudaError_t e, const char* where);
 int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
@@ -41,6 +48,6 @@ int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* re
                   double* bucket_reward, cudaStream_t st);
 int launch_route(const be_qweights* W, int T, int M, const double* x, int B, double eps,
                  uint64_t seed, uint64_t counter, double* q_out, uint8_t* a_out, cudaStream_t st);
-int launch_tracegen(int E, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
+int launch_tracegen(int E, int64_t env_offset, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
                     double* arrival, uint8_t* task, cudaStream_t st);
 }  // namespace be

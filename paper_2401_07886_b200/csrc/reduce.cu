@@ -7,13 +7,13 @@
 // One thread per environment owns the strictly sequential fp64 prefix sum
 // c_{k+1} = c_k + r_k (np.cumsum order — any parallel scan would change the
 // rounding and therefore the threshold counts).  Rewards
-// are env-major in HBM, so each warp stages a 32-env x 32-request tile with
-// fully coalesced row loads (each row = 256 contiguous bytes) into padded
-// shared memory, and every lane then scans its own row from there.  The
-// trailing-window quotient (c[k+w] - c[k]) / w is never formed: because
-// RN(x / w) is monotone in x, `RN(x/w) >= theta` is exactly `x >= tau(theta)`
-// for a host-precomputed double tau (and `== 1.0` an interval), so the
-// kernel compares differences directly — bit-identical counts, no DDIV.
+// are env-major in HBM, so each warp streams a 32-env x 16-request tile per
+// stage with cp.async (16-byte LDGSTS, every env row a fully used 128-byte
+// segment) into padded shared memory, NST stages deep, while the lanes scan
+// an earlier stage row by row.  The trailing-window quotient
+// (c[k+w] - c[k]) / w is never formed: RN(x / w) is monotone in x, so
+// `RN(x/w) >= theta` is exactly `x >= tau(theta)` for a host-precomputed
+// double tau (and `== 1.0` an interval) — bit-identical counts, no DDIV.
 // HBM-bound: 9 algorithmic bytes per request (8 B reward + 1 B flags).
 #include <cuda_runtime.h>
 #include <math.h>
@@ -26,7 +26,11 @@
 namespace be {
 
 constexpr int RED_WARPS = 4;
-constexpr int MAX_THETA = 16;
+constexpr int MAX_THETA = 8;
+constexpr int CH = 16;       // requests per stage
+constexpr int NST = 3;       // pipeline stages
+constexpr int W = 20;        // evalkit.WINDOW
+constexpr int TSTRIDE = 18;  // padded tile row (doubles): 16-byte aligned rows
 
 struct ReduceParams {
     int32_t E;
@@ -38,9 +42,9 @@ struct ReduceParams {
     const int64_t* seg_start;
     const int32_t* seg_bucket;
     int32_t n_buckets;
-    int32_t n_theta;
+    int32_t exact_k;  // index of the theta == 1.0 threshold (interval test), -1 if none
     double lo[MAX_THETA];
-    double hi[MAX_THETA];
+    double hi;        // upper end of the theta == 1.0 interval
     int64_t* win_counts;
     int64_t* n_windows;
     int64_t* bucket_miss;
@@ -48,23 +52,153 @@ struct ReduceParams {
     double* bucket_reward;
 };
 
-// W = window (template so the 32-slot prefix ring stays in registers).
-template <int W>
-__global__ void __launch_bounds__(RED_WARPS * 32) reduce_kernel(const ReduceParams p) {
-    __shared__ double tile[RED_WARPS][32][33];
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes, bool valid) {
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int src_size = valid ? bytes : 0;  // 0 -> zero-fill
+    if (bytes == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(src_size));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct Acc {
+    double c;         // running prefix sum
+    double ring[32];  // ring[j] = prefix sum after request (32 m + j)
+    double c_bucket;  // prefix sum when the current bucket started
+    int miss, req;    // current bucket
+};
+
+template <int NT>
+__device__ __forceinline__ void count_window(const ReduceParams& p, int (&cnt)[NT], double d) {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+        bool in = d >= p.lo[k];
+        if (k == p.exact_k) in = in && d <= p.hi;
+        cnt[k] += in ? 1 : 0;
+    }
+}
+
+__device__ __forceinline__ void flush_bucket(const ReduceParams& p, Acc& a, int64_t env, int bucket) {
+    if (a.req) {
+        const int64_t o = env * p.n_buckets + bucket;
+        p.bucket_miss[o] += a.miss;
+        p.bucket_req[o] += a.req;
+        p.bucket_reward[o] = __dadd_rn(p.bucket_reward[o], __dsub_rn(a.c, a.c_bucket));
+    }
+    a.miss = a.req = 0;
+    a.c_bucket = a.c;
+}
+
+// General path: ragged tails, the first windows, segment boundaries.
+template <int NT, int OFF>
+__device__ __forceinline__ void scan_chunk_slow(const ReduceParams& p, Acc& a, int (&cnt)[NT],
+                                                const double* row, uint4 fl, int64_t i0, int64_t n,
+                                                int64_t& next_seg, int64_t& seg, int64_t seg_end,
+                                                int& bucket, int64_t env) {
+    const uint32_t fw[4] = {fl.x, fl.y, fl.z, fl.w};
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+        const int64_t i = i0 + s;
+        if (i < n) {
+            while (i >= next_seg) {  // segment boundary
+                flush_bucket(p, a, env, bucket);
+                bucket = p.seg_bucket ? p.seg_bucket[seg] : 0;
+                ++seg;
+                next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
+            }
+            a.c = __dadd_rn(a.c, row[s]);
+            const double prev = a.ring[(OFF + s - W + 64) & 31];  // prefix sum W requests back
+            a.ring[OFF + s] = a.c;
+            if (i >= W - 1) count_window<NT>(p, cnt, __dsub_rn(a.c, prev));
+            a.miss += (fw[s >> 2] >> (8 * (s & 3) + 7)) & 1u;
+            a.req += 1;
+        }
+    }
+}
+
+// Steady state: whole chunk valid, windows complete, no boundary inside.
+template <int NT, int OFF>
+__device__ __forceinline__ void scan_chunk_fast(const ReduceParams& p, Acc& a, int (&cnt)[NT],
+                                                const double* row, uint4 fl) {
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+        a.c = __dadd_rn(a.c, row[s]);
+        const double prev = a.ring[(OFF + s - W + 64) & 31];
+        a.ring[OFF + s] = a.c;
+        count_window<NT>(p, cnt, __dsub_rn(a.c, prev));
+    }
+    a.miss += __popc(fl.x & 0x80808080u) + __popc(fl.y & 0x80808080u) +
+              __popc(fl.z & 0x80808080u) + __popc(fl.w & 0x80808080u);
+    a.req += CH;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(RED_WARPS * 32, 4) reduce_kernel(const ReduceParams p) {
+    extern __shared__ __align__(16) double red_smem[];
+    typedef double TileT[NST][32][TSTRIDE];
+    TileT* tile = reinterpret_cast<TileT*>(red_smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t e0 = ((int64_t)blockIdx.x * RED_WARPS + warp) * 32;
-    if (e0 >= p.E) return;
+    int64_t* n_row = reinterpret_cast<int64_t*>(red_smem + RED_WARPS * NST * 32 * TSTRIDE) + warp * 32;
+    typedef uint4 FlT[NST][32];
+    FlT* fl_tile = reinterpret_cast<FlT*>(reinterpret_cast<int64_t*>(red_smem + RED_WARPS * NST * 32 * TSTRIDE) +
+                                          RED_WARPS * 32);
+    const int64_t n_groups = (p.E + 31) / 32;
+    const int64_t g = (int64_t)blockIdx.x * RED_WARPS + warp;
+    if (g >= n_groups) return;
+    const int64_t e0 = g * 32;
     const int64_t env = e0 + lane;
     const bool live = env < p.E;
     const int64_t n = live ? (p.n_events ? p.n_events[env] : p.ld) : 0;
-    int64_t nmax = n;
+    int64_t nmax = n, nmin = live ? n : INT64_MAX;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         int64_t o = __shfl_xor_sync(0xffffffffu, nmax, off);
         nmax = o > nmax ? o : nmax;
+        o = __shfl_xor_sync(0xffffffffu, nmin, off);
+        nmin = o < nmin ? o : nmin;
     }
-    // segment cursor -> bucket
+    const bool full_group = e0 + 32 <= p.E;
+    const int64_t nchunks = (nmax + CH - 1) / CH;
+    n_row[lane] = live ? n : -1;
+    __syncwarp();
+    // staging, 16-byte copies: lanes 8q..8q+7 copy row 4k+q (128 contiguous bytes)
+    const bool vec16 = ((reinterpret_cast<uintptr_t>(p.reward) | (uintptr_t)(p.ld * 8)) & 15) == 0;
+    const int q4 = lane >> 3, c4 = (lane & 7) * 2;
+    const double* src16 = p.reward + (e0 + q4) * p.ld + c4;  // + k * 4 * ld + i0
+    const int64_t step16 = 4 * p.ld;
+    const int half = lane >> 4, col = lane & 15;
+    const bool fl_vec = ((reinterpret_cast<uintptr_t>(p.flags) | (uintptr_t)p.ld) & 15) == 0;
+    const uint8_t* fsrc = p.flags + (live ? env * p.ld : 0);
+    auto issue = [&](int64_t ch) {
+        if (ch < nchunks) {
+            const int st = (int)(ch % NST);
+            const int64_t i0 = ch * CH;
+            // own row of flags (16 bytes) rides in the same cp.async group
+            if (fl_vec) cp_async(&fl_tile[warp][st][lane], fsrc + i0, 16, live && i0 + CH <= n);
+            if (vec16 && full_group && i0 + CH <= nmin) {  // every row complete
+                const double* s = src16 + i0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    cp_async(&tile[warp][st][4 * k + q4][c4], s, 16, true);
+                    s += step16;
+                }
+            } else {
+                const int64_t i = i0 + col;
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int r = 2 * k + half;
+                    const bool v = i < n_row[r];
+                    const double* s = p.reward + (v ? (e0 + r) * p.ld + i : 0);
+                    cp_async(&tile[warp][st][r][col], s, 8, v);
+                }
+            }
+        }
+        cp_commit();  // uniform group accounting (possibly empty)
+    };
+
     int64_t seg = live ? p.seg_off[env] : 0;
     const int64_t seg_end = live ? p.seg_off[env + 1] : 0;
     int bucket = 0;
@@ -75,92 +209,64 @@ __global__ void __launch_bounds__(RED_WARPS * 32) reduce_kernel(const ReducePara
             p.bucket_req[env * p.n_buckets + b] = 0;
             p.bucket_reward[env * p.n_buckets + b] = 0.0;
         }
-    int64_t acc_miss = 0, acc_req = 0;
-    double acc_rw = 0.0;
-    int64_t cnt[MAX_THETA];
+    Acc a;
+    a.c = 0.0;
+    a.c_bucket = 0.0;
+    a.miss = a.req = 0;
 #pragma unroll
-    for (int k = 0; k < MAX_THETA; ++k) cnt[k] = 0;
-    double lo[MAX_THETA], hi[MAX_THETA];
+    for (int j = 0; j < 32; ++j) a.ring[j] = 0.0;
+    int cnt[NT];
 #pragma unroll
-    for (int k = 0; k < MAX_THETA; ++k) {
-        lo[k] = p.lo[k];
-        hi[k] = p.hi[k];
-    }
-    double ring[32];  // ring[s] = prefix sum after request (chunk*32 + s)
-#pragma unroll
-    for (int s = 0; s < 32; ++s) ring[s] = 0.0;
-    double c = 0.0;
-    const double* rrow = p.reward;
-    for (int64_t i0 = 0; i0 < nmax; i0 += 32) {
-        // coalesced staging: row r of the tile = env e0 + r, requests i0..i0+31
-        for (int r = 0; r < 32; ++r) {
-            int64_t nr = __shfl_sync(0xffffffffu, n, r);
-            double v = 0.0;
-            if (e0 + r < p.E && i0 + lane < nr) v = rrow[(e0 + r) * p.ld + i0 + lane];
-            tile[warp][r][lane] = v;
-        }
-        __syncwarp();
-        // own row of flags: 32 bytes
-        uint32_t fw[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) fw[k] = 0;
+    for (int k = 0; k < NT; ++k) cnt[k] = 0;
+
+    const uint8_t* frow = p.flags + (live ? env * p.ld : 0);
+    auto load_flags = [&](int64_t ch) {
+        uint4 f = make_uint4(0, 0, 0, 0);
+        const int64_t i0 = ch * CH;
         if (live && i0 < n) {
-            const uint8_t* fr = p.flags + env * p.ld + i0;
-            if (((reinterpret_cast<uintptr_t>(fr) & 15) == 0) && i0 + 32 <= n) {
-                uint4 a = *reinterpret_cast<const uint4*>(fr);
-                uint4 b = *reinterpret_cast<const uint4*>(fr + 16);
-                fw[0] = a.x; fw[1] = a.y; fw[2] = a.z; fw[3] = a.w;
-                fw[4] = b.x; fw[5] = b.y; fw[6] = b.z; fw[7] = b.w;
+            if (fl_vec && i0 + CH <= n) {
+                f = fl_tile[warp][ch % NST][lane];  // staged by issue() with the rewards
             } else {
-                for (int k = 0; k < 32 && i0 + k < n; ++k) fw[k >> 2] |= (uint32_t)fr[k] << (8 * (k & 3));
+                uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+                for (int k = 0; k < CH && i0 + k < n; ++k) {
+                    const uint32_t b = (uint32_t)frow[i0 + k] << (8 * (k & 3));
+                    if (k < 4) w0 |= b; else if (k < 8) w1 |= b; else if (k < 12) w2 |= b; else w3 |= b;
+                }
+                f = make_uint4(w0, w1, w2, w3);
             }
         }
+        return f;
+    };
+
 #pragma unroll
-        for (int s = 0; s < 32; ++s) {
-            const int64_t i = i0 + s;
-            if (i < n) {
-                while (i >= next_seg) {  // segment boundary: flush the bucket partials
-                    if (acc_req) {
-                        p.bucket_miss[env * p.n_buckets + bucket] += acc_miss;
-                        p.bucket_req[env * p.n_buckets + bucket] += acc_req;
-                        p.bucket_reward[env * p.n_buckets + bucket] = __dadd_rn(p.bucket_reward[env * p.n_buckets + bucket], acc_rw);
-                    }
-                    acc_miss = acc_req = 0;
-                    acc_rw = 0.0;
-                    bucket = p.seg_bucket ? p.seg_bucket[seg] : 0;
-                    ++seg;
-                    next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
-                }
-                const double r = tile[warp][lane][s];
-                c = __dadd_rn(c, r);
-                const double prev = ring[(s - W + 64) & 31];  // prefix sum W requests back
-                ring[s] = c;
-                if (i >= W - 1) {
-                    const double d = __dsub_rn(c, prev);
-#pragma unroll
-                    for (int k = 0; k < MAX_THETA; ++k)
-                        if (k < p.n_theta) cnt[k] += (d >= lo[k] && d <= hi[k]) ? 1 : 0;
-                }
-                const uint32_t f = (fw[s >> 2] >> (8 * (s & 3))) & 0xffu;
-                acc_miss += (f >> 7) & 1u;
-                acc_req += 1;
-                acc_rw = __dadd_rn(acc_rw, r);
-            }
-        }
+    for (int s = 0; s < NST - 1; ++s) issue(s);
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+        issue(ch + NST - 1);
+        cp_wait<NST - 1>();
         __syncwarp();
+        const uint4 fl = load_flags(ch);
+        const double* row = &tile[warp][ch % NST][lane][0];
+        const int64_t i0 = ch * CH;
+        const bool fast = i0 >= 32 && i0 + CH <= n && next_seg >= i0 + CH;
+        if (ch & 1) {
+            if (fast) scan_chunk_fast<NT, 16>(p, a, cnt, row, fl);
+            else scan_chunk_slow<NT, 16>(p, a, cnt, row, fl, i0, n, next_seg, seg, seg_end, bucket, env);
+        } else {
+            if (fast) scan_chunk_fast<NT, 0>(p, a, cnt, row, fl);
+            else scan_chunk_slow<NT, 0>(p, a, cnt, row, fl, i0, n, next_seg, seg, seg_end, bucket, env);
+        }
+        __syncwarp();  // stage ch % NST is refilled by the next iteration's issue
     }
+    cp_wait<0>();
     if (!live) return;
-    if (acc_req) {
-        p.bucket_miss[env * p.n_buckets + bucket] += acc_miss;
-        p.bucket_req[env * p.n_buckets + bucket] += acc_req;
-        p.bucket_reward[env * p.n_buckets + bucket] = __dadd_rn(p.bucket_reward[env * p.n_buckets + bucket], acc_rw);
-    }
-    for (int k = 0; k < p.n_theta; ++k) p.win_counts[env * p.n_theta + k] = cnt[k];
+    flush_bucket(p, a, env, bucket);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) p.win_counts[env * NT + k] = cnt[k];
     p.n_windows[env] = n >= W ? n - W + 1 : 0;
 }
 
 // smallest double x with RN(x / w) >= theta (x >= 0 domain; -inf if all qualify)
-static double tau_ge(double theta, double w) {
+double tau_ge(double theta, double w) {
     if (0.0 / w >= theta) return -INFINITY;
     // binary search over the bit patterns of non-negative doubles
     uint64_t lo = 0, hi = 0x7ff0000000000000ULL;  // +inf qualifies (inf/w = inf)
@@ -177,7 +283,7 @@ static double tau_ge(double theta, double w) {
 }
 
 // largest double x with RN(x / w) <= theta
-static double tau_le(double theta, double w) {
+double tau_le(double theta, double w) {
     uint64_t lo = 0, hi = 0x7ff0000000000000ULL;
     double x0 = 0.0;
     if (!(x0 / w <= theta)) return -INFINITY;
@@ -193,11 +299,28 @@ static double tau_le(double theta, double w) {
     return x;
 }
 
+template <int NT>
+static int launch_nt(const ReduceParams& p, cudaStream_t st) {
+    int64_t groups = (p.E + 31) / 32;
+    int blocks = (int)((groups + RED_WARPS - 1) / RED_WARPS);
+    const size_t smem = sizeof(double) * RED_WARPS * NST * 32 * TSTRIDE + sizeof(int64_t) * RED_WARPS * 32 +
+                        sizeof(uint4) * RED_WARPS * NST * 32;
+    static bool configured[MAX_THETA + 1] = {false};
+    if (!configured[NT]) {
+        cudaFuncSetAttribute(reduce_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        configured[NT] = true;
+    }
+    reduce_kernel<NT><<<blocks, RED_WARPS * 32, smem, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "reduce launch");
+}
+
 int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* reward, int window,
                   const double* thetas, int n_theta, int n_buckets, int64_t* win_counts,
                   int64_t* n_windows, int64_t* bucket_miss, int64_t* bucket_req,
                   double* bucket_reward, cudaStream_t st) {
-    if (window != 20) return set_error(BE_EINVAL, "reducer window must be 20 (evalkit.WINDOW)");
+    if (window != W) return set_error(BE_EINVAL, "reducer window must be 20 (evalkit.WINDOW)");
+    if (n_theta < 1 || n_theta > MAX_THETA) return set_error(BE_EINVAL, "n_theta must be in [1, 8]");
     ReduceParams p{};
     p.E = tr->n_envs;
     p.ld = tr->ld;
@@ -208,29 +331,36 @@ int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* re
     p.seg_start = tr->seg_start;
     p.seg_bucket = tr->seg_bucket;
     p.n_buckets = n_buckets;
-    p.n_theta = n_theta;
+    p.exact_k = -1;
+    p.hi = INFINITY;
     const double w = (double)window;
-    for (int k = 0; k < MAX_THETA; ++k) {
-        p.lo[k] = INFINITY;
-        p.hi[k] = -INFINITY;
-    }
+    for (int k = 0; k < MAX_THETA; ++k) p.lo[k] = INFINITY;
     for (int k = 0; k < n_theta; ++k) {
         double th = thetas[k];
         if (!(th >= 0.0 && th <= 1.0)) return set_error(BE_EINVAL, "thresholds must lie in [0, 1]");
         p.lo[k] = tau_ge(th, w);
-        // theta == 1.0 counts exact peak windows only (evalkit.py:237-238)
-        p.hi[k] = th == 1.0 ? tau_le(1.0, w) : INFINITY;
+        if (th == 1.0) {
+            // theta == 1.0 counts exact peak windows only (evalkit.py:237-238)
+            if (p.exact_k >= 0) return set_error(BE_EINVAL, "threshold 1.0 given twice");
+            p.exact_k = k;
+            p.hi = tau_le(1.0, w);
+        }
     }
     p.win_counts = win_counts;
     p.n_windows = n_windows;
     p.bucket_miss = bucket_miss;
     p.bucket_req = bucket_req;
     p.bucket_reward = bucket_reward;
-    int64_t warps = (p.E + 31) / 32;
-    int blocks = (int)((warps + RED_WARPS - 1) / RED_WARPS);
-    reduce_kernel<20><<<blocks, RED_WARPS * 32, 0, st>>>(p);
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "reduce launch");
+    switch (n_theta) {
+        case 1: return launch_nt<1>(p, st);
+        case 2: return launch_nt<2>(p, st);
+        case 3: return launch_nt<3>(p, st);
+        case 4: return launch_nt<4>(p, st);
+        case 5: return launch_nt<5>(p, st);
+        case 6: return launch_nt<6>(p, st);
+        case 7: return launch_nt<7>(p, st);
+        default: return launch_nt<8>(p, st);
+    }
 }
 
 }  // namespace be

@@ -1,13 +1,16 @@
-// rollout.cu — fused greedy rollout (run_eval, evalkit.py:154-209) and the
-// step-synchronous env API (ClusterSim reset/advance/observe/submit).
+// rollout.cu — fused greedy rollout (run_eval, evalkit.py:154-209).
 //
-// be_rollout_greedy runs ONE persistent kernel for the whole trace batch:
-// each warp pulls an environment id from a global counter, keeps the
-// replica state in registers (one lane per replica) and walks its trace
-// request by request — advance (with exact iteration skipping), score
-// completions, estimate the rate, observe, Q-network forward + argmax in fp64,
-// submit — then drains.  Trace reads are coalesced 32-request blocks
-// broadcast with shuffles; per-tier sums and the replica argmin are REDUX ops.
+// be_rollout_greedy runs ONE persistent kernel for the whole trace batch.
+// Each warp hosts 32 / LPE environments (LPE = lanes per env: 16 when the
+// cluster has <= 16 replicas — the shipped 3 x 4 — else 32); each group of
+// LPE lanes pulls an environment id from a global counter, keeps one replica
+// per lane in registers and walks that env's trace request by request:
+// advance (with exact iteration skipping), score completions, rate signal,
+// observe, Q-network forward + argmax in fp64, submit — then drains and
+// pulls the next env.  Two envs per warp halve the per-env cost of every
+// warp-wide instruction (the Q-network, reductions, bookkeeping).  Trace
+// reads are coalesced LPE-request blocks broadcast with shuffles; per-tier
+// sums and the replica argmin are REDUX ops.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -18,6 +21,7 @@ namespace be {
 
 struct RolloutParams {
     be_cfg cfg;
+    ScoreAux aux;
     int32_t E;
     int64_t ld;
     const double* arrival;
@@ -36,7 +40,7 @@ struct RolloutParams {
     be_records rec;
     Slot* rings;
     int32_t cap_log2;
-    int32_t R;  // replicas per env (= active lanes)
+    int32_t R;  // replicas per env (= active lanes per group)
     int32_t* env_counter;
     int32_t* status;  // [0] = error code, [1] = first failing env
 };
@@ -45,11 +49,14 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code, int env)
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
 }
 
-// Shared-memory staging: Score, then W1 [D][H], b1 [H], W2^T [M][H], b2 [M].
+// Shared-memory staging: Score, then W1 [D][H] (task rows + b1), b1 [H], W2^T [M][H], b2 [M].
 template <int M>
 __device__ void stage_weights(const RolloutParams& p, double* sw, int T) {
     const int H = p.H, D = T + M + 1;
-    for (int k = threadIdx.x; k < D * H; k += blockDim.x) sw[k] = p.w1[k];
+    // task rows carry the layer-1 bias: base[t][j] = W1[t][j] + b1[j] (the one-hot
+    // input selects exactly one of them); the forward then skips the bias add
+    for (int k = threadIdx.x; k < D * H; k += blockDim.x)
+        sw[k] = k < T * H ? __dadd_rn(p.w1[k], p.b1[k % H]) : p.w1[k];
     double* sb1 = sw + D * H;
     for (int k = threadIdx.x; k < H; k += blockDim.x) sb1[k] = p.b1[k];
     double* sw2t = sb1 + H;
@@ -61,72 +68,125 @@ __device__ void stage_weights(const RolloutParams& p, double* sw, int T) {
     for (int k = threadIdx.x; k < M; k += blockDim.x) sb2[k] = p.b2[k];
 }
 
-template <int M>
+// Sum / min over the lanes of this lane's group (REDUX over the warp with the
+// other group masked out; all 32 lanes must call).
+template <int LPE>
+__device__ __forceinline__ unsigned group_sum(unsigned v, int grp) {
+    if (LPE == 32) return __reduce_add_sync(FULL, v);
+    const unsigned s0 = __reduce_add_sync(FULL, grp == 0 ? v : 0u);
+    const unsigned s1 = __reduce_add_sync(FULL, grp == 1 ? v : 0u);
+    return grp ? s1 : s0;
+}
+template <int LPE>
+__device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
+    if (LPE == 32) return __reduce_min_sync(FULL, v);
+    const unsigned s0 = __reduce_min_sync(FULL, grp == 0 ? v : 0xffffffffu);
+    const unsigned s1 = __reduce_min_sync(FULL, grp == 1 ? v : 0xffffffffu);
+    return grp ? s1 : s0;
+}
+
+template <int M, int LPE>
 __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
     const int T = p.cfg.n_tasks;
     const bool policy = p.forced == nullptr && p.static_tier < 0;
-    if (threadIdx.x < 32) load_score(sc, p.cfg);
+    if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     if (policy) stage_weights<M>(p, sw, T);
     __syncthreads();
     const int H = p.H, D = T + M + 1;
     const double* sW1 = sw;
-    const double* sb1 = sw + D * H;
-    const double* sW2t = sb1 + H;
+    const double* sW2t = sw + D * H + H;
     const double* sb2 = sW2t + M * H;
 
     const int lane = threadIdx.x & 31;
-    const TierC tc = lane_tier(p.cfg, lane);
+    const int gl = lane & (LPE - 1);       // lane within the env group
+    const int grp = LPE == 32 ? 0 : lane / LPE;
+    const int g0 = grp * LPE;              // first lane of the group
+    const unsigned gmask = LPE == 32 ? FULL : (0xffffu << g0);
+    const TierC tc = lane_tier(p.cfg, gl);
     const bool active_lane = tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
     const bool skip = p.cfg.skip_ahead != 0;
     const bool true_rate = p.cfg.estimator_true_rate != 0;
     const bool reset_segs = p.cfg.reset_between_segments != 0;
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    // encode (policy.py:63-64) divides by the scales; multiplying by the
+    // reciprocal is bit-identical for power-of-two scales (the shipped
+    // 128/32/8) and within 1 ulp otherwise (Q tolerance)
+    double inv_scale[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) inv_scale[m] = __ddiv_rn(1.0, p.cfg.batch_scales[m]);
+    const double inv_rate_scale = __ddiv_rn(1.0, p.cfg.rate_scale);
+
+    // per-group ("group-uniform") env state
+    int env = -1;
+    bool need = true, dead = false;
+    int64_t base = 0, n = 0, i = 0, seg = 0, seg_end = 0, next_seg = INT64_MAX;
+    double cur_rate = 0.0;
+    Slot* ring = p.rings;
+    Rep r;
+    rep_reset(r);
+    SkipCache skc;
+    skip_cache_reset(skc);
+    Estimator est;
+    est.n = 0;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) est.w[k] = 0.0;
+    bool ok = true, bad = false;
+    double pf_arr = 0.0;
+    int pf_task = 0, pf_forced = 0;
 
     for (;;) {
-        int env = 0;
-        if (lane == 0) env = atomicAdd(p.env_counter, 1);
-        env = __shfl_sync(FULL, env, 0);
-        if (env >= p.E) break;
-
-        Slot* ring = p.rings + ((size_t)env * p.R + (active_lane ? lane : 0)) * ((size_t)mask + 1);
-        RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, (int64_t)env * p.ld};
-        const int64_t base = (int64_t)env * p.ld;
-        const int64_t n = p.n_events ? p.n_events[env] : p.ld;
-        int64_t seg = p.seg_off[env];
-        const int64_t seg_end = p.seg_off[env + 1];
-        int64_t next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
-        double cur_rate = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
-        Rep r;
-        rep_reset(r);
-        r.head = 0;
-        Estimator est;
-        est.n = 0;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) est.w[k] = 0.0;
-        bool ok = true;   // ring capacity / iteration counter
-        bool bad = false; // forced action out of range
-
-        double pf_arr = 0.0;
-        int pf_task = 0, pf_forced = 0;
-        for (int64_t i = 0; i < n; ++i) {
-            const int sub = (int)(i & 31);
-            if (sub == 0) {  // coalesced 32-request prefetch
-                int64_t ii = i + lane;
-                if (ii < n) {
-                    pf_arr = __ldg(p.arrival + base + ii);
-                    pf_task = __ldg(p.task + base + ii);
-                    if (p.forced) pf_forced = __ldg(p.forced + base + ii);
-                }
+        // ---- (re)fill groups that finished their env
+        int got = (need && gl == 0) ? atomicAdd(p.env_counter, 1) : 0;
+        got = __shfl_sync(FULL, got, g0);
+        if (need) {
+            need = false;
+            if (got >= p.E) {
+                dead = true;
+            } else {
+                env = got;
+                base = (int64_t)env * p.ld;
+                n = p.n_events ? p.n_events[env] : p.ld;
+                i = 0;
+                seg = p.seg_off[env];
+                seg_end = p.seg_off[env + 1];
+                next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
+                cur_rate = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
+                ring = p.rings + ((size_t)env * p.R + (active_lane ? gl : 0)) * ((size_t)mask + 1);
+                rep_reset(r);
+                r.head = 0;
+                skip_cache_reset(skc);
+                est.n = 0;
+                ok = true;
+                bad = false;
             }
-            const double U = __shfl_sync(FULL, pf_arr, sub);
-            const int task = __shfl_sync(FULL, pf_task, sub);
-            // segment boundaries (evalkit.py:186-192)
-            while (i >= next_seg) {
+        }
+        if (__all_sync(FULL, dead)) break;
+        const bool live = !dead && i < n;
+        RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, base};
+
+        // ---- one request for every live group (evalkit.py:185-205)
+        const int sub = (int)(i & (LPE - 1));
+        if (live && sub == 0) {  // coalesced LPE-request prefetch
+            const int64_t ii = i + gl;
+            if (ii < n) {
+                pf_arr = __ldg(p.arrival + base + ii);
+                pf_task = __ldg(p.task + base + ii);
+                if (p.forced) pf_forced = __ldg(p.forced + base + ii);
+            }
+        }
+        const double U = __shfl_sync(FULL, pf_arr, g0 + sub);
+        int task = __shfl_sync(FULL, pf_task, g0 + sub);
+        const int ftier = __shfl_sync(FULL, pf_forced, g0 + sub);
+        if (!live) task = 0;  // keep idle groups' shared-memory reads in range
+        double rate = 0.0;
+        if (live) {
+            while (i >= next_seg) {  // segment boundaries (evalkit.py:186-192)
                 if (reset_segs && i == next_seg && i > 0) {
-                    if (active_lane) ok &= advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip);
+                    if (active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out, skip, skc);
                     rep_reset(r);
                     est.n = 0;
                 }
@@ -134,49 +194,61 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
                 ++seg;
                 next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
             }
-            if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out, skip);
-            const double rate = estimator_observe(est, U, true_rate, cur_rate, p.cfg.prior_rate);
-            int obs[M];
+            if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out, skip, skc);
+            // true-rate mode never reads the arrival window (workload.py:241-242)
+            rate = true_rate ? cur_rate : estimator_observe(est, U, false, cur_rate, p.cfg.prior_rate);
+        }
+        int obs[M];
 #pragma unroll
-            for (int m = 0; m < M; ++m) obs[m] = (int)__reduce_add_sync(FULL, (tc.tier == m) ? (unsigned)r.count : 0u);
-            int tier;
-            if (p.forced) {
-                tier = __shfl_sync(FULL, pf_forced, sub);
-            } else if (p.static_tier >= 0) {
-                tier = p.static_tier;
-            } else {
-                double xt[M], q[M];
+        for (int m = 0; m < M; ++m)
+            obs[m] = (int)group_sum<LPE>((live && tc.tier == m) ? (unsigned)r.count : 0u, grp);
+        int tier;
+        if (p.forced) {
+            tier = ftier;
+        } else if (p.static_tier >= 0) {
+            tier = p.static_tier;
+        } else {
+            double xt[M], q[M];
 #pragma unroll
-                for (int m = 0; m < M; ++m) xt[m] = __ddiv_rn((double)obs[m], p.cfg.batch_scales[m]);
-                const double xr = __ddiv_rn(rate, p.cfg.rate_scale);
-                qnet_warp<M>(sW1, sb1, sW2t, sb2, T, H, task, xt, xr, q);
-                tier = argmax_first<M>(q);
-                if (p.rec.q && lane < M) {
-#pragma unroll
-                    for (int m = 0; m < M; ++m)
-                        if (lane == m) p.rec.q[(base + i) * M + m] = q[m];
-                }
-            }
-            if (p.rec.obs && lane < M) {
+            for (int m = 0; m < M; ++m) xt[m] = __dmul_rn((double)obs[m], inv_scale[m]);
+            const double xr = __dmul_rn(rate, inv_rate_scale);
+            qnet_group<M, LPE>(sW1, sW2t, sb2, T, H, task, xt, xr, q);
+            tier = argmax_first<M>(q);
+            if (live && p.rec.q && gl < M) {
 #pragma unroll
                 for (int m = 0; m < M; ++m)
-                    if (lane == m) p.rec.obs[(base + i) * M + m] = obs[m];
+                    if (gl == m) p.rec.q[(base + i) * M + m] = q[m];
             }
-            if (p.rec.rate && lane == 0) p.rec.rate[base + i] = rate;
-            // replica argmin of (len(active), len(queue), id) == argmin (count, lane)
-            unsigned key = (tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)lane) : 0xffffffffu;
-            unsigned best = __reduce_min_sync(FULL, key);
+        }
+        if (live && p.rec.obs && gl < M) {
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+                if (gl == m) p.rec.obs[(base + i) * M + m] = obs[m];
+        }
+        if (live && p.rec.rate && gl == 0) p.rec.rate[base + i] = rate;
+        // replica argmin of (len(active), len(queue), id) == argmin (count, replica)
+        const unsigned key = (live && tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)gl) : 0xffffffffu;
+        const unsigned best = group_min<LPE>(key, grp);
+        if (live) {
             if (best == 0xffffffffu) {  // tier out of range (forced action)
                 bad = true;
-            } else if ((int)(best & 31u) == lane) {
+            } else if ((int)(best & 31u) == gl) {
                 ok &= submit_lane(r, tc, U, (uint32_t)i | ((uint32_t)task << 24), ring, mask);
             }
-            if (!__all_sync(FULL, ok) || bad) break;
+            ++i;
         }
-        if (active_lane && ok && !bad)
-            ok &= advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip);
-        if (bad && lane == 0) raise_status(p.status, BE_EINVAL, env);
-        else if (!__all_sync(FULL, ok) && lane == 0) raise_status(p.status, BE_ECAPACITY, env);
+        // ---- group bookkeeping: failure or end of trace -> drain, next env
+        const bool gfail = (__ballot_sync(FULL, live && (!ok || bad)) & gmask) != 0;
+        const bool gbad = (__ballot_sync(FULL, live && bad) & gmask) != 0;
+        if (!dead && (gfail || i >= n)) {
+            if (!gfail && active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out, skip, skc);
+            const bool drain_fail = (__ballot_sync(gmask, !ok) & gmask) != 0;
+            if (gl == 0) {
+                if (gbad) raise_status(p.status, BE_EINVAL, env);
+                else if (gfail || drain_fail) raise_status(p.status, BE_ECAPACITY, env);
+            }
+            need = true;
+        }
     }
 }
 
@@ -186,9 +258,9 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy) {
     return s;
 }
 
-template <int M>
+template <int M, int LPE>
 static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
-    auto kern = rollout_kernel<M>;
+    auto kern = rollout_kernel<M, LPE>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
@@ -198,9 +270,9 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "occupancy");
     if (per_sm < 1) per_sm = 1;
-    long long warps_needed = p.E;
+    const long long groups_per_block = threads / LPE;
     long long blocks = (long long)sms * per_sm;
-    long long max_blocks = (warps_needed + threads / 32 - 1) / (threads / 32);
+    const long long max_blocks = (p.E + groups_per_block - 1) / groups_per_block;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
     kern<<<(unsigned)blocks, threads, smem, st>>>(p);
@@ -209,10 +281,17 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
     return BE_OK;
 }
 
+template <int M>
+static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
+    if (p.R <= 16 && (p.H == 0 || p.H % 16 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms);
+    return launch_rollout_m<M, 32>(p, smem, st, sms);
+}
+
 int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
                    const uint8_t* forced, const be_records* rec, cudaStream_t st) {
     RolloutParams p{};
     p.cfg = env->cfg;
+    make_score_aux(env->cfg, &p.aux);
     p.E = tr->n_envs;
     p.ld = tr->ld;
     p.arrival = tr->arrival_ms;
@@ -242,14 +321,14 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
     switch (M) {
-        case 1: return launch_rollout_m<1>(p, smem, st, env->sms);
-        case 2: return launch_rollout_m<2>(p, smem, st, env->sms);
-        case 3: return launch_rollout_m<3>(p, smem, st, env->sms);
-        case 4: return launch_rollout_m<4>(p, smem, st, env->sms);
-        case 5: return launch_rollout_m<5>(p, smem, st, env->sms);
-        case 6: return launch_rollout_m<6>(p, smem, st, env->sms);
-        case 7: return launch_rollout_m<7>(p, smem, st, env->sms);
-        case 8: return launch_rollout_m<8>(p, smem, st, env->sms);
+        case 1: return launch_rollout_lpe<1>(p, smem, st, env->sms);
+        case 2: return launch_rollout_lpe<2>(p, smem, st, env->sms);
+        case 3: return launch_rollout_lpe<3>(p, smem, st, env->sms);
+        case 4: return launch_rollout_lpe<4>(p, smem, st, env->sms);
+        case 5: return launch_rollout_lpe<5>(p, smem, st, env->sms);
+        case 6: return launch_rollout_lpe<6>(p, smem, st, env->sms);
+        case 7: return launch_rollout_lpe<7>(p, smem, st, env->sms);
+        case 8: return launch_rollout_lpe<8>(p, smem, st, env->sms);
         default: return set_error(BE_EINVAL, "n_tiers out of range");
     }
 }

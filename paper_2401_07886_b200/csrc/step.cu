@@ -51,6 +51,7 @@ __global__ void env_reset_kernel(void* base, int E, int R, const uint8_t* mask) 
 
 struct StepParams {
     be_cfg cfg;
+    ScoreAux aux;
     int32_t E, R, cap_log2;
     void* state;
     Slot* rings;
@@ -82,9 +83,10 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     const int T = p.cfg.n_tasks;
     const int H = p.H, D = T + M + 1;
     const bool policy = !p.drain && p.forced == nullptr && p.static_tier < 0;
-    if (threadIdx.x < 32) load_score(sc, p.cfg);
+    if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     if (policy) {
-        for (int k = threadIdx.x; k < D * H; k += blockDim.x) sw[k] = p.w1[k];
+        for (int k = threadIdx.x; k < D * H; k += blockDim.x)
+            sw[k] = k < T * H ? __dadd_rn(p.w1[k], p.b1[k % H]) : p.w1[k];  // b1 folded
         for (int k = threadIdx.x; k < H; k += blockDim.x) sw[D * H + k] = p.b1[k];
         for (int k = threadIdx.x; k < M * H; k += blockDim.x) sw[D * H + H + k] = p.w2[(k % H) * M + k / H];
         for (int k = threadIdx.x; k < M; k += blockDim.x) sw[D * H + H + M * H + k] = p.b2[k];
@@ -100,6 +102,8 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     Rep r;
     if (al) r = reps_of(p.state, e, p.R)[lane];
     else rep_reset(r);
+    SkipCache skc;
+    skip_cache_reset(skc);
     EnvState* es = state_of(p.state, e, p.E, p.R);
     // records are indexed by request id modulo rec_ld (a ring for long runs)
     // complete() writes at base + id; id is the 24-bit slot id.
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     bool ok = true;
     const bool skip = p.cfg.skip_ahead != 0;
     if (p.drain) {
-        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip);
+        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip, skc);
         if (al) reps_of(p.state, e, p.R)[lane] = r;
         const bool all_ok = __all_sync(FULL, ok);
         if (!all_ok && lane == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     }
     const double U = p.arrival[e];
     const int task = p.task[e];
-    if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out, skip);
+    if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out, skip, skc);
     Estimator est;
 #pragma unroll
     for (int k = 0; k < 5; ++k) est.w[k] = es->w[k];
@@ -231,6 +235,7 @@ static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st) {
 static StepParams base_params(be_env* env, int64_t rec_ld, const be_records* rec) {
     StepParams p{};
     p.cfg = env->cfg;
+    make_score_aux(env->cfg, &p.aux);
     p.E = env->E;
     p.R = env->R;
     p.cap_log2 = env->cap_log2;

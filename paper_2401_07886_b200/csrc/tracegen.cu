@@ -17,7 +17,8 @@
 
 namespace be {
 
-__global__ void tracegen_stable_kernel(int E, int64_t n, int64_t ld, const double* rate, int T,
+__global__ void tracegen_stable_kernel(int E, int64_t env_offset, int64_t n, int64_t ld,
+                                       const double* rate, int T,
                                        uint64_t seed, double* arrival, uint8_t* task) {
     // one warp per env: lanes draw 32 gaps in parallel, the prefix sum is
     // done sequentially (lane order) so times equal the left-to-right cumsum
@@ -28,7 +29,7 @@ __global__ void tracegen_stable_kernel(int E, int64_t n, int64_t ld, const doubl
     double t = 0.0;
     for (int64_t i0 = 0; i0 < n; i0 += 32) {
         const int64_t i = i0 + lane;
-        P4 r = philox4x32_10((uint64_t)i, (uint64_t)env, seed);
+        P4 r = philox4x32_10((uint64_t)i, (uint64_t)(env_offset + env), seed);
         // Exp(mean) by inversion: -log(1 - u) * mean, u in [0, 1)
         const double u = u01(r.x[0], r.x[1]);
         const double gap = __dmul_rn(-log1p(-u), mean_gap);
@@ -47,11 +48,11 @@ __global__ void tracegen_stable_kernel(int E, int64_t n, int64_t ld, const doubl
     }
 }
 
-int launch_tracegen(int E, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
+int launch_tracegen(int E, int64_t env_offset, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
                     double* arrival, uint8_t* task, cudaStream_t st) {
     const int threads = 256;
     const int blocks = (int)(((int64_t)E * 32 + threads - 1) / threads);
-    tracegen_stable_kernel<<<blocks, threads, 0, st>>>(E, n, ld, rate, n_tasks, seed, arrival, task);
+    tracegen_stable_kernel<<<blocks, threads, 0, st>>>(E, env_offset, n, ld, rate, n_tasks, seed, arrival, task);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "tracegen launch");
 }

@@ -223,6 +223,98 @@ def reduce_eval(trace: TraceBatch, flags: torch.Tensor, reward: torch.Tensor,
     return out
 
 
+class StreamingEvaluator:
+    """End-to-end evaluation of host-resident trace batches.
+
+    Each `submit` copies one pinned-host trace batch to the device on a copy
+    stream (double-buffered, so batch k+1 uploads while batch k rolls out),
+    runs the fused rollout + reducer on the compute stream and copies the
+    int64 / f64 statistics back.  `result(k)` waits for batch k."""
+
+    def __init__(self, policy, tiers, reward_spec, n_envs: int, ld: int, encoding=None, *,
+                 estimator_mode: str = "estimated", thresholds=THRESHOLDS, n_buckets: int = 1,
+                 ring_capacity: Optional[int] = None, device=None):
+        self.device = _lib.require_cuda(device)
+        self.net, self.static_tier = _policy_args(policy, len(tiers))
+        if self.static_tier < 0 and encoding is None:
+            encoding = StateEncoding(n_tasks=len(reward_spec.tasks),
+                                     batch_scales=tuple(float(t.max_batch) for t in tiers))
+        self.ro = GreedyRollout(tiers, reward_spec, n_envs, ld, encoding,
+                                estimator_mode=estimator_mode, ring_capacity=ring_capacity,
+                                want_realized=False, device=self.device)
+        if self.net is not None:
+            self.net = DeviceQNet.of(self.net, self.device)
+        self.thresholds, self.n_buckets = tuple(thresholds), int(n_buckets)
+        self.copy_stream = torch.cuda.Stream(self.device)
+        self.compute_stream = torch.cuda.Stream(self.device)
+        self._bufs = [None, None]
+        self._copied = [torch.cuda.Event(), torch.cuda.Event()]
+        self._freed = [torch.cuda.Event(), torch.cuda.Event()]
+        self._k = 0
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def _device_buf(self, slot: int, host: TraceBatch) -> TraceBatch:
+        b = self._bufs[slot]
+        if b is None:
+            def like(t):
+                return None if t is None else torch.empty_like(t, device=self.device)
+            b = TraceBatch(like(host.arrival), like(host.task), like(host.n_events),
+                           like(host.seg_offsets), like(host.seg_start), like(host.seg_rate),
+                           like(host.seg_bucket), host.n_tasks)
+            self._bufs[slot] = b
+        return b
+
+    def submit(self, host: TraceBatch):
+        """host: a TraceBatch whose tensors live in pinned host memory."""
+        slot = self._k & 1
+        dev = self._device_buf(slot, host)
+        cs, ks = self.copy_stream, self.compute_stream
+        with torch.cuda.stream(cs):
+            cs.wait_event(self._freed[slot])  # previous use of this buffer finished
+            nbytes = 0
+            for name in ("arrival", "task", "n_events", "seg_offsets", "seg_start", "seg_rate",
+                         "seg_bucket"):
+                src, dst = getattr(host, name), getattr(dev, name)
+                if src is not None:
+                    dst.copy_(src, non_blocking=True)
+                    nbytes += src.numel() * src.element_size()
+            self._copied[slot].record(cs)
+        self.h2d_bytes = nbytes
+        with torch.cuda.stream(ks):
+            ks.wait_event(self._copied[slot])
+            o = self.ro.launch(dev, self.net, self.static_tier, stream=ks)
+            red = reduce_eval(dev, o.flags, o.reward, self.thresholds, self.n_buckets, stream=ks)
+            self._freed[slot].record(ks)
+            host_stats = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                          for k, v in (("win_counts", red.win_counts), ("n_windows", red.n_windows),
+                                       ("bucket_miss", red.bucket_miss),
+                                       ("bucket_req", red.bucket_req),
+                                       ("bucket_reward", red.bucket_reward))}
+            for k, t in host_stats.items():
+                t.copy_(getattr(red, k), non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(ks)
+        self.d2h_bytes = sum(t.numel() * t.element_size() for t in host_stats.values())
+        self._k += 1
+        return done, host_stats
+
+    def result(self, handle) -> ReduceResult:
+        done, hs = handle
+        done.synchronize()
+        self.ro.env.check(self.compute_stream)
+        return ReduceResult(self.thresholds, hs["win_counts"], hs["n_windows"], hs["bucket_miss"],
+                            hs["bucket_req"], hs["bucket_reward"])
+
+
+def pin_trace(tb: TraceBatch) -> TraceBatch:
+    """Copy a device TraceBatch into pinned host memory (for end-to-end runs)."""
+    def h(t):
+        return None if t is None else t.cpu().pin_memory()
+    return TraceBatch(h(tb.arrival), h(tb.task), h(tb.n_events), h(tb.seg_offsets),
+                      h(tb.seg_start), h(tb.seg_rate), h(tb.seg_bucket), tb.n_tasks)
+
+
 def run_eval_batch(policy, traces: Union[TraceBatch, Sequence], tiers, reward_spec, encoding=None,
                    *, estimator_mode: str = "estimated", prior_rate: float = 1.0,
                    reset_between_segments: bool = False, thresholds=THRESHOLDS,

@@ -125,16 +125,19 @@ class TraceBatch:
 
     @classmethod
     def generate_stable(cls, rates: Sequence[float], n: int, n_tasks: int, seed: int,
-                        device=None, buckets: Optional[Sequence[int]] = None) -> "TraceBatch":
+                        device=None, buckets: Optional[Sequence[int]] = None,
+                        env_offset: int = 0) -> "TraceBatch":
         """On-device gen_stable (workload.py:120-141): env e is one Poisson
-        segment at rates[e] req/s truncated to n requests (Philox4x32-10)."""
+        segment at rates[e] req/s truncated to n requests (Philox4x32-10 keyed
+        by (seed, env_offset + e), so a global env id gets the same trace on
+        any number of GPUs)."""
         dev = _lib.require_cuda(device)
         E = len(rates)
         rate = torch.as_tensor(np.asarray(rates, np.float64), device=dev)
         arrival = torch.empty((E, n), dtype=torch.float64, device=dev)
         task = torch.empty((E, n), dtype=torch.uint8, device=dev)
         L = _lib.load()
-        _lib.check(L.be_trace_gen_stable(E, n, n, rate.data_ptr(), n_tasks, seed,
+        _lib.check(L.be_trace_gen_stable(E, int(env_offset), n, n, rate.data_ptr(), n_tasks, seed,
                                          arrival.data_ptr(), task.data_ptr(), _lib.stream_ptr()))
         offs = torch.arange(E + 1, dtype=torch.int64, device=dev)
         seg_start = torch.zeros(E, dtype=torch.int64, device=dev)

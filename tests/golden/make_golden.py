@@ -36,7 +36,7 @@ from besteffort.policy import (QNetwork, RouterState, StateEncoding, encode,  # 
 from besteffort.reward import RewardSpec, request_reward  # noqa: E402
 from besteffort.simcore import ClusterSim, Request  # noqa: E402
 from besteffort.workload import (RateEstimator, WorkloadTrace, ArrivalEvent,  # noqa: E402
-                                 SegmentMark, estimate_rate)
+                                 SegmentMark, estimate_rate, gen_stable)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -190,6 +190,26 @@ def main():
                 trace = truncate(trace, 4000)
             run_case(f"{scen_name}_trained", nets["trained"], "trained", trace,
                      scen.adjust_tiers(cfg.tiers()), reward, enc, scen)
+    # config 1 (BASELINE.json configs[0]): one env, 3 tiers x 1 task
+    # (hellaswag, hard 40 ms/token), Poisson arrivals, true-rate estimator,
+    # greedy DQN over 10k requests; T=1 trained policy + init_random(rng 0)
+    ckpt1 = os.path.join(HERE, "trained_seed7_t1.beqn")
+    reward1 = RewardSpec(tasks=cfg.reward_spec().tasks[:1], matrix=cfg.reward_spec().matrix[:1])
+    enc1 = StateEncoding(n_tasks=1, batch_scales=enc.batch_scales, rate_scale=enc.rate_scale)
+    nets1 = {"random_t1": QNetwork.init_random(1, 3, 256, np.random.default_rng(0))}
+    if os.path.exists(ckpt1):
+        nets1["trained_t1"] = load_checkpoint(ckpt1)
+    np.savez_compressed(os.path.join(HERE, "nets_t1.npz"),
+                        **{f"{k}_{p}": getattr(v, p) for k, v in nets1.items()
+                           for p in ("w1", "b1", "w2", "b2")})
+    from dataclasses import replace as _replace
+    scen1 = _replace(cfg.scenario("stable"), name="cfg1")
+    for lam in (0.25, 4.0, 32.0, 48.0):
+        tr = gen_stable([lam], math.ceil(10000 / lam * 1.1), 1,
+                        component_seed(0, f"gen:cfg1:{lam}"))
+        tr = truncate(tr, 10000)
+        for pname, net in nets1.items():
+            run_case(f"cfg1_{lam:g}_{pname}", net, pname, tr, cfg.tiers(), reward1, enc1, scen1)
     # tie-forcing: 5 ms quantised arrivals make END == arrival coincidences common
     scen = cfg.scenario("unpredictable-2")
     reward = cfg.reward_spec()

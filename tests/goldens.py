@@ -20,11 +20,12 @@ def load(name):
 
 
 def nets():
-    z = np.load(os.path.join(GOLDEN, "nets.npz"))
     out = {}
-    for k in z.files:
-        net, p = k.rsplit("_", 1)
-        out.setdefault(net, {})[p] = z[k]
+    for f in ("nets.npz", "nets_t1.npz"):
+        z = np.load(os.path.join(GOLDEN, f))
+        for k in z.files:
+            net, p = k.rsplit("_", 1)
+            out.setdefault(net, {})[p] = z[k]
     return out
 
 

@@ -77,6 +77,46 @@ def test_rollout_batch_of_copies(cuda, name):
     assert bool((t == t[0:1]).all())
 
 
+@pytest.mark.parametrize("scenario", ["unpredictable-1", "stable", "hellaswag-copa-soft"])
+def test_ragged_batch_matches_oracle(cuda, scenario):
+    """Many envs of different lengths in one launch (exercises the persistent
+    env scheduler, two envs per warp and mid-warp env refills)."""
+    names = [n for n in NAMES if n.startswith(scenario + "_")]
+    gs = [goldens.load(n) for n in names]
+    m = gs[0]["meta"]
+    net = goldens.nets()["mixed1"]
+    rng = np.random.default_rng(7)
+    traces = []
+    for k in range(61):
+        g = gs[k % len(gs)]
+        n = int(rng.integers(0, len(g["arrival"]) + 1))
+        ss = [s for s in g["seg_start"] if s < max(n, 1)] or [0]
+        traces.append((g["arrival"][:n], g["task"][:n], ss, list(g["seg_rate"][:len(ss)])))
+    ld = max(len(t[0]) for t in traces)
+    arr = np.zeros((len(traces), ld))
+    tsk = np.zeros((len(traces), ld), np.uint8)
+    for e, t in enumerate(traces):
+        arr[e, :len(t[0])] = t[0]
+        if len(t[0]):
+            arr[e, len(t[0]):] = t[0][-1]
+        tsk[e, :len(t[1])] = t[1]
+    tb = TraceBatch.from_arrays(arr, tsk, [t[2] for t in traces], [t[3] for t in traces],
+                                n_events=[len(t[0]) for t in traces])
+    ro = GreedyRollout(tiers_of(m), reward_of(m), len(traces), ld, enc_of(m),
+                       estimator_mode=m["estimator_mode"], reset_between_segments=m["reset"],
+                       want_steps=True)
+    o = ro.run(tb, QNetwork.from_any(net))
+    for e, t in enumerate(traces):
+        n = len(t[0])
+        ref = oracle.run_eval_oracle(tiers=m["tiers"], reward=m["reward"], arrival=t[0], task=t[1],
+                                     seg_start=t[2], seg_rate=t[3], net=net,
+                                     batch_scales=m["enc"]["batch_scales"],
+                                     estimator_mode=m["estimator_mode"], reset=m["reset"])
+        assert np.array_equal(o.tier[e, :n].cpu().numpy(), ref["tier"]), f"env {e}"
+        assert np.array_equal(o.reward[e, :n].cpu().numpy(), ref["reward"]), f"env {e}"
+        assert np.array_equal(o.obs[e, :n].cpu().numpy(), ref["obs"]), f"env {e}"
+
+
 def test_forced_actions_match_oracle(cuda):
     g = goldens.load("unpredictable-1_mixed1")
     forced = np.random.default_rng(1).integers(0, 3, size=len(g["arrival"])).astype(np.uint8)
