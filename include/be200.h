@@ -185,6 +185,75 @@ int32_t be_trace_gen_stable(int32_t n_envs, int64_t env_offset, int64_t n, int64
                             const double* rate, int32_t n_tasks, uint64_t seed,
                             double* arrival_ms, uint8_t* task, void* stream);
 
+/* ---------------------------------------------------------------- training
+ * Replay + learner (trainer.py:101-290) and the training workload
+ * (trainer.py:293-316) for E envs stepping in lockstep (request id = step).
+ * All learner arithmetic is fp64; updates are deterministic for a batch. */
+typedef struct {
+    int32_t n_tasks, n_tiers, hidden, n_envs;
+    int64_t replay_capacity;    /* TrainConfig.buffer_capacity */
+    int32_t pending_capacity;   /* P: max decisions a request may stay unresolved */
+    int32_t batch;              /* TrainConfig.batch_size */
+    int64_t warmup;             /* TrainConfig.warmup */
+    int64_t target_sync_every;  /* TrainConfig.target_sync_every */
+    double discount, learning_rate;
+    int32_t adam;               /* 1 = Adam (beta 0.9/0.999, eps 1e-8), 0 = SGD */
+    int32_t huber;              /* 1 = huber (delta 1), 0 = squared */
+    double rate_low, rate_high; /* TrainingWorkload rate range (log-uniform) */
+    int32_t regime_equal_time;  /* 1 = "equal-time" cadence, 0 = "requests" */
+    int32_t _pad;
+    double regime_mean_seconds, regime_mean_requests;
+} be_learner_cfg;
+
+typedef struct be_learner be_learner;
+
+/* Device views into a learner (all device pointers). */
+typedef struct {
+    be_qweights online, target;  /* routing weights for be_env_step */
+    double* params;              /* online w1 | b1 | w2 | b2, contiguous (nparam) */
+    double* grad;                /* gradient of the last backward (nparam): all-reduce here */
+    int32_t nparam;
+    int32_t _pad;
+    double* loss;                /* [0] loss of the last backward, [1] loss of the last update */
+    int64_t* counters;           /* [0] Adam t, [1] gradient steps, [2] any update applied */
+    double* ring_states;         /* [C][D] */
+    double* ring_next_states;    /* [C][D] */
+    uint8_t* ring_actions;       /* [C] */
+    double* ring_rewards;        /* [C] */
+    double* ring_cont;           /* [C] */
+    int64_t* ring_state;         /* [0] cursor, [1] size, [2] total commits */
+    double* pending_x;           /* [P][E][D]: x_out of be_env_step for request id = step */
+    uint8_t* pending_action;     /* [P][E]:    action_out of be_env_step */
+    uint8_t* pending_flags;      /* [E][P]:    be_records.flags with rec_ld = P */
+    double* pending_reward;      /* [E][P]:    be_records.reward with rec_ld = P */
+    double* workload_state;      /* [E][3] time_ms, rate, requests left in the regime */
+} be_learner_views_t;
+
+int32_t be_learner_create(const be_learner_cfg* cfg, int32_t device, be_learner** out);
+int32_t be_learner_destroy(be_learner* learner);
+/* Online = target = the given parameters (host or device pointers); Adam state reset. */
+int32_t be_learner_set_params(be_learner* learner, const double* w1, const double* b1,
+                              const double* w2, const double* b2, void* stream);
+int32_t be_learner_views(be_learner* learner, be_learner_views_t* views);
+/* TrainingWorkload.next_arrival for every env (Philox keyed by seed, counter step). */
+int32_t be_learner_workload(be_learner* learner, uint64_t seed, int64_t step, double* arrival_ms,
+                            uint8_t* task, double* true_rate, void* stream);
+/* Commit every transition whose reward and next state are both known after the
+ * decision for request `step` (trainer.py:143-156); ring slots by env-order scan. */
+int32_t be_learner_commit(be_learner* learner, int64_t step, void* stream);
+/* Sample a batch (Philox(seed, counter)) and compute loss + gradients into views.grad
+ * (no-op while the ring holds fewer than max(batch, warmup) transitions). */
+int32_t be_learner_backward(be_learner* learner, uint64_t seed, uint64_t counter,
+                            int64_t* sample_idx /* nullable [batch] */, void* stream);
+/* Same on an explicit batch (states/next_states [B][D], actions u8, rewards, cont). */
+int32_t be_learner_backward_batch(be_learner* learner, const double* states,
+                                  const uint8_t* actions, const double* rewards,
+                                  const double* next_states, const double* cont,
+                                  int32_t batch, void* stream);
+/* Adam/SGD on views.grad, then the target sync every target_sync_every steps. */
+int32_t be_learner_apply(be_learner* learner, int32_t explicit_batch, void* stream);
+int32_t be_learner_check(be_learner* learner, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,6 +69,30 @@ class BeRecords(ctypes.Structure):
                 ("rate", ctypes.c_void_p), ("q", ctypes.c_void_p)]
 
 
+class BeLearnerCfg(ctypes.Structure):
+    _fields_ = [("n_tasks", ctypes.c_int32), ("n_tiers", ctypes.c_int32), ("hidden", ctypes.c_int32),
+                ("n_envs", ctypes.c_int32), ("replay_capacity", ctypes.c_int64),
+                ("pending_capacity", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("warmup", ctypes.c_int64), ("target_sync_every", ctypes.c_int64),
+                ("discount", ctypes.c_double), ("learning_rate", ctypes.c_double),
+                ("adam", ctypes.c_int32), ("huber", ctypes.c_int32),
+                ("rate_low", ctypes.c_double), ("rate_high", ctypes.c_double),
+                ("regime_equal_time", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("regime_mean_seconds", ctypes.c_double), ("regime_mean_requests", ctypes.c_double)]
+
+
+class BeLearnerViews(ctypes.Structure):
+    _fields_ = [("online", BeQWeights), ("target", BeQWeights), ("params", ctypes.c_void_p),
+                ("grad", ctypes.c_void_p), ("nparam", ctypes.c_int32), ("_pad", ctypes.c_int32),
+                ("loss", ctypes.c_void_p), ("counters", ctypes.c_void_p),
+                ("ring_states", ctypes.c_void_p), ("ring_next_states", ctypes.c_void_p),
+                ("ring_actions", ctypes.c_void_p), ("ring_rewards", ctypes.c_void_p),
+                ("ring_cont", ctypes.c_void_p), ("ring_state", ctypes.c_void_p),
+                ("pending_x", ctypes.c_void_p), ("pending_action", ctypes.c_void_p),
+                ("pending_flags", ctypes.c_void_p), ("pending_reward", ctypes.c_void_p),
+                ("workload_state", ctypes.c_void_p)]
+
+
 _P = ctypes.c_void_p
 _I32, _I64, _U64, _D, _SZ = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t
 
@@ -91,6 +115,16 @@ SIGNATURES = {
     "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
                               _P, _P, _P]),
     "be_trace_gen_stable": (_I32, [_I32, _I64, _I64, _I64, _P, _I32, _U64, _P, _P, _P]),
+    "be_learner_create": (_I32, [ctypes.POINTER(BeLearnerCfg), _I32, ctypes.POINTER(_P)]),
+    "be_learner_destroy": (_I32, [_P]),
+    "be_learner_set_params": (_I32, [_P, _P, _P, _P, _P, _P]),
+    "be_learner_views": (_I32, [_P, ctypes.POINTER(BeLearnerViews)]),
+    "be_learner_workload": (_I32, [_P, _U64, _I64, _P, _P, _P, _P]),
+    "be_learner_commit": (_I32, [_P, _I64, _P]),
+    "be_learner_backward": (_I32, [_P, _U64, _U64, _P, _P]),
+    "be_learner_backward_batch": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _P]),
+    "be_learner_apply": (_I32, [_P, _I32, _P]),
+    "be_learner_check": (_I32, [_P, _P]),
 }
 
 _lib = None

@@ -139,7 +139,7 @@ __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Sc
         // exact division-free threshold
         const bool hit = span <= sc.hit_tau[task * BE_MAX_TIERS + tc.tier];
         o.reward[o.base + id] = hit ? sc.matrix[task * BE_MAX_TIERS + tc.tier] : 0.0;
-        o.flags[o.base + id] = (uint8_t)(tc.tier | (hit ? 0 : 0x80));
+        o.flags[o.base + id] = (uint8_t)(tc.tier | 0x40 | (hit ? 0 : 0x80));
         return;
     }
     double realized = __ddiv_rn(span, (double)tc.tokens);
@@ -159,7 +159,8 @@ __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Sc
         }
     }
     double reward = __dmul_rn(w, sc.matrix[task * BE_MAX_TIERS + tc.tier]);
-    uint8_t flag = (uint8_t)(tc.tier | ((realized > dl) ? 0x80 : 0));
+    // flags: tier (bits 0-5) | completed (0x40) | deadline miss (0x80)
+    uint8_t flag = (uint8_t)(tc.tier | 0x40 | ((realized > dl) ? 0x80 : 0));
     o.reward[o.base + id] = reward;
     o.flags[o.base + id] = flag;
     if (o.realized) o.realized[o.base + id] = realized;

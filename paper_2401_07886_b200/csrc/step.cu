@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     bool bad = best == 0xffffffffu;
     if (!bad && (int)(best & 31u) == lane) {
         uint32_t rid = (uint32_t)(id % p.rec_ld);
+        p.rec.flags[(int64_t)e * p.rec_ld + rid] = 0;  // record slot now "in flight"
         ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
     }
     if (al) reps_of(p.state, e, p.R)[lane] = r;

@@ -75,7 +75,7 @@ class RolloutOutputs:
 
     @property
     def tier(self) -> torch.Tensor:
-        return self.flags & 0x7F
+        return self.flags & 0x3F  # bit 6 = completed, bit 7 = deadline miss
 
     @property
     def miss(self) -> torch.Tensor:

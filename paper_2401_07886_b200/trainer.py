@@ -1,0 +1,339 @@
+"""DQN training on the GPU (drop-in for besteffort.trainer).
+
+  TrainConfig                 trainer.py:39-90 (same fields, validation, epsilon_at)
+  run_training                trainer.py:333-406 — E environments step in lockstep; each
+                              vectorised iteration routes one request per env (epsilon-
+                              greedy), commits resolved transitions into the device
+                              replay ring and takes `updates_per_step` learner updates
+  DeviceLearner               ReplayBuffer + _StepKernel + Adam/SGD + target sync on the
+                              device (be_learner_*), fp64, deterministic per batch
+  train_step_batch            one update on an explicit batch (parity with the reference)
+
+Update-to-data ratio: the reference takes one update per routed request (one env). With
+E envs per iteration this module takes `updates_per_step` updates per E requests (UTD =
+updates_per_step / E); with n_envs=1 it is exactly the reference's schedule.
+Randomness (arrivals, epsilon, sampling, init) uses Philox, so runs are reproducible
+but not bit-identical to numpy PCG64 streams (statistical parity).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .env import EnvBatch, StepRecords
+from .specs import QNetwork, StateEncoding
+
+
+@dataclass
+class TrainConfig:
+    discount: float = 0.99
+    learning_rate: float = 1e-4
+    batch_size: int = 1024
+    target_sync_every: int = 500
+    total_iterations: int = 200_000
+    epsilon_start: float = 1.0
+    epsilon_end: float = 0.05
+    epsilon_decay_fraction: float = 0.25
+    buffer_capacity: int = 500_000
+    warmup: int = 10_000
+    optimizer: str = "adam"
+    loss: str = "huber"
+    hidden: int = 256
+    seed: int = 0
+    log_every: int = 10_000
+    rate_low: float = 0.25
+    rate_high: float = 48.0
+    regime_cadence: str = "equal-time"
+    regime_mean_seconds: float = 20.0
+    regime_mean_requests: float = 100.0
+    estimator_mode: str = "true-rate"
+    prior_rate: float = 1.0
+
+    def __post_init__(self):  # trainer.py:74-83
+        if not 0.0 < self.discount < 1.0:
+            raise ValueError("discount must lie in (0, 1)")
+        if self.batch_size > self.buffer_capacity:
+            raise ValueError("batch_size must not exceed buffer capacity")
+        if self.batch_size < 1 or self.total_iterations < 0:
+            raise ValueError("batch_size must be >= 1 and total_iterations >= 0")
+        if not 0.0 <= self.epsilon_end <= self.epsilon_start <= 1.0:
+            raise ValueError("need 0 <= epsilon_end <= epsilon_start <= 1")
+        if self.rate_low <= 0 or self.rate_high < self.rate_low:
+            raise ValueError("need 0 < rate_low <= rate_high")
+        if self.optimizer not in ("adam", "sgd"):
+            raise ValueError("optimizer must be 'adam' or 'sgd'")
+        if self.regime_cadence not in ("equal-time", "requests"):
+            raise ValueError("regime_cadence must be 'equal-time' or 'requests'")
+
+    def epsilon_at(self, iteration: int) -> float:  # trainer.py:85-90
+        decay_steps = int(self.epsilon_decay_fraction * self.total_iterations)
+        if decay_steps <= 0:
+            return self.epsilon_end
+        frac = min(1.0, iteration / decay_steps)
+        return self.epsilon_start + (self.epsilon_end - self.epsilon_start) * frac
+
+
+@dataclass
+class LogRow:
+    step: int
+    loss: float
+    mean_recent_reward: float
+    epsilon: float
+
+
+@dataclass
+class TrainResult:
+    net: QNetwork
+    log: list = field(default_factory=list)
+    updates: int = 0
+    transitions: int = 0
+
+
+class DeviceLearner:
+    """be_learner handle: online/target nets, Adam state, replay ring, pending store."""
+
+    def __init__(self, n_tasks: int, n_tiers: int, cfg: TrainConfig, n_envs: int = 1,
+                 pending_capacity: int = 4096, device=None):
+        self.device = _lib.require_cuda(device)
+        self.cfg = cfg
+        self.n_tasks, self.n_tiers, self.n_envs = n_tasks, n_tiers, int(n_envs)
+        self.D = n_tasks + n_tiers + 1
+        self.P = int(pending_capacity)
+        c = _lib.BeLearnerCfg()
+        c.n_tasks, c.n_tiers, c.hidden, c.n_envs = n_tasks, n_tiers, cfg.hidden, self.n_envs
+        c.replay_capacity = int(cfg.buffer_capacity)
+        c.pending_capacity = self.P
+        c.batch = int(cfg.batch_size)
+        c.warmup = int(cfg.warmup)
+        c.target_sync_every = int(cfg.target_sync_every)
+        c.discount, c.learning_rate = float(cfg.discount), float(cfg.learning_rate)
+        c.adam = 1 if cfg.optimizer == "adam" else 0
+        c.huber = 1 if cfg.loss == "huber" else 0
+        c.rate_low, c.rate_high = float(cfg.rate_low), float(cfg.rate_high)
+        c.regime_equal_time = 1 if cfg.regime_cadence == "equal-time" else 0
+        c.regime_mean_seconds = float(cfg.regime_mean_seconds)
+        c.regime_mean_requests = float(cfg.regime_mean_requests)
+        self._L = _lib.load()
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self._L.be_learner_create(ctypes.byref(c), self.device.index or 0,
+                                                 ctypes.byref(h)))
+        self._h = h
+        self.views = _lib.BeLearnerViews()
+        _lib.check(self._L.be_learner_views(self._h, ctypes.byref(self.views)))
+        v = self.views
+        self.nparam = v.nparam
+        self.params = _wrap(v.params, (self.nparam,), torch.float64, self.device)
+        self.grad = _wrap(v.grad, (self.nparam,), torch.float64, self.device)
+        self.loss = _wrap(v.loss, (2,), torch.float64, self.device)
+        self.counters = _wrap(v.counters, (8,), torch.int64, self.device)
+        self.ring_state = _wrap(v.ring_state, (8,), torch.int64, self.device)
+        C = int(cfg.buffer_capacity)
+        self.ring_rewards = _wrap(v.ring_rewards, (C,), torch.float64, self.device)
+        self.ring_states = _wrap(v.ring_states, (C, self.D), torch.float64, self.device)
+        self.ring_next_states = _wrap(v.ring_next_states, (C, self.D), torch.float64, self.device)
+        self.ring_actions = _wrap(v.ring_actions, (C,), torch.uint8, self.device)
+        self.pending_x = _wrap(v.pending_x, (self.P, self.n_envs, self.D), torch.float64, self.device)
+        self.pending_action = _wrap(v.pending_action, (self.P, self.n_envs), torch.uint8, self.device)
+        self.pending_flags = _wrap(v.pending_flags, (self.n_envs, self.P), torch.uint8, self.device)
+        self.pending_reward = _wrap(v.pending_reward, (self.n_envs, self.P), torch.float64, self.device)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._L.be_learner_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ parameters
+    def set_params(self, net) -> None:
+        net = QNetwork.from_any(net)
+        arrs = [np.ascontiguousarray(a, np.float64) for a in (net.w1, net.b1, net.w2, net.b2)]
+        ts = [torch.from_numpy(a).to(self.device) for a in arrs]
+        _lib.check(self._L.be_learner_set_params(self._h, *(t.data_ptr() for t in ts),
+                                                 _lib.stream_ptr()))
+        torch.cuda.current_stream().synchronize()
+
+    def online_weights(self) -> _lib.BeQWeights:
+        return self.views.online
+
+    def net(self) -> QNetwork:
+        p = self.params.cpu().numpy()
+        D, H, M = self.D, self.cfg.hidden, self.n_tiers
+        o = 0
+        w1 = p[o:o + D * H].reshape(D, H); o += D * H
+        b1 = p[o:o + H]; o += H
+        w2 = p[o:o + H * M].reshape(H, M); o += H * M
+        b2 = p[o:o + M]
+        return QNetwork(self.n_tasks, M, w1.copy(), b1.copy(), w2.copy(), b2.copy())
+
+    def target_net(self) -> QNetwork:
+        v = self.views.target
+        D, H, M = self.D, self.cfg.hidden, self.n_tiers
+        w = [_wrap(ptr, shape, torch.float64, self.device).cpu().numpy().copy()
+             for ptr, shape in ((v.w1, (D, H)), (v.b1, (H,)), (v.w2, (H, M)), (v.b2, (M,)))]
+        return QNetwork(self.n_tasks, M, *w)
+
+    # ------------------------------------------------------------ steps
+    def backward(self, seed: int, counter: int, sample_idx: Optional[torch.Tensor] = None):
+        _lib.check(self._L.be_learner_backward(self._h, seed & (2**64 - 1), counter & (2**64 - 1),
+                                               _lib.ptr(sample_idx), _lib.stream_ptr()))
+
+    def backward_batch(self, states, actions, rewards, next_states, cont):
+        dev = self.device
+        t = [torch.as_tensor(np.ascontiguousarray(x, dt), device=dev) for x, dt in
+             ((states, np.float64), (actions, np.uint8), (rewards, np.float64),
+              (next_states, np.float64), (cont, np.float64))]
+        _lib.check(self._L.be_learner_backward_batch(self._h, *(x.data_ptr() for x in t),
+                                                     int(t[0].shape[0]), _lib.stream_ptr()))
+        self._keep = t
+
+    def apply(self, explicit_batch: bool = False) -> None:
+        _lib.check(self._L.be_learner_apply(self._h, 1 if explicit_batch else 0, _lib.stream_ptr()))
+
+    def commit(self, step: int) -> None:
+        _lib.check(self._L.be_learner_commit(self._h, int(step), _lib.stream_ptr()))
+
+    def workload(self, seed: int, step: int, arrival, task, rate) -> None:
+        _lib.check(self._L.be_learner_workload(self._h, seed & (2**64 - 1), int(step),
+                                               arrival.data_ptr(), task.data_ptr(), rate.data_ptr(),
+                                               _lib.stream_ptr()))
+
+    def check(self) -> None:
+        _lib.check(self._L.be_learner_check(self._h, _lib.stream_ptr()))
+
+    @property
+    def size(self) -> int:
+        return int(self.ring_state[1])
+
+
+def _wrap(ptr: int, shape, dtype, device) -> torch.Tensor:
+    """Zero-copy torch view of device memory owned by the C library."""
+    n = int(np.prod(shape))
+    esz = torch.empty((), dtype=dtype).element_size()
+    t = torch.as_tensor(_DevPtr(ptr, n * esz, device), device=device)
+    return t.view(dtype).view(*shape)
+
+
+class _DevPtr:
+    """__cuda_array_interface__ exporter for a raw device allocation (bytes)."""
+
+    def __init__(self, ptr: int, nbytes: int, device):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=None,
+                 completion_log=None, *, n_envs: int = 1, updates_per_step: int = 1,
+                 pending_capacity: int = 4096, ring_capacity: int = 1024, device=None,
+                 world=None) -> TrainResult:
+    """trainer.py:333-406 on the GPU for `n_envs` lockstep environments.
+
+    `world`: optional torch.distributed group — gradients are all-reduced (mean)
+    between backward and the optimizer step (data-parallel learner)."""
+    n_tasks, n_tiers = len(reward_spec.tasks), len(reward_spec.matrix[0])
+    if len(tiers) != n_tiers:
+        raise ValueError("tier count must match reward matrix width")
+    if encoding is None:
+        encoding = StateEncoding(n_tasks=n_tasks, batch_scales=tuple(float(t.max_batch) for t in tiers))
+    dev = _lib.require_cuda(device)
+    E = int(n_envs)
+    learner = DeviceLearner(n_tasks, n_tiers, cfg, E, pending_capacity, dev)
+    if init_net is None:
+        rng = np.random.default_rng(np.random.SeedSequence(cfg.seed).spawn(4)[0])
+        init_net = QNetwork.init_random(n_tasks, n_tiers, cfg.hidden, rng)
+    else:
+        init_net = QNetwork.from_any(init_net)
+        if init_net.n_tasks != n_tasks or init_net.n_tiers != n_tiers:
+            raise ValueError("init_net dimensions do not match the environment")
+    learner.set_params(init_net)
+    if world is not None:
+        import torch.distributed as dist
+        dist.broadcast(learner.params, 0)
+    env = EnvBatch(tiers, reward_spec, E, encoding, estimator_mode=cfg.estimator_mode,
+                   prior_rate=cfg.prior_rate, ring_capacity=ring_capacity, device=dev)
+    P = learner.P
+    rec = _PendingRecords(learner)
+    arrival = torch.empty(E, dtype=torch.float64, device=dev)
+    task = torch.empty(E, dtype=torch.uint8, device=dev)
+    rate = torch.empty(E, dtype=torch.float64, device=dev)
+    seeds = [int(s.generate_state(1, np.uint64)[0]) for s in np.random.SeedSequence(cfg.seed).spawn(4)]
+    wl_seed, pol_seed, smp_seed = seeds[1], seeds[2], seeds[3]
+    log = []
+    W = learner.online_weights()
+    n_updates = 0
+    for it in range(cfg.total_iterations):
+        learner.workload(wl_seed, it, arrival, task, rate)
+        slot = it % P
+        x_out = learner.pending_x[slot]
+        a_out = learner.pending_action[slot]
+        _env_step(env, arrival, task, rate, W, cfg.epsilon_at(it), pol_seed, it, rec, x_out, a_out)
+        learner.commit(it)
+        for u in range(updates_per_step):
+            learner.backward(smp_seed, it * updates_per_step + u)
+            if world is not None:
+                import torch.distributed as dist
+                dist.all_reduce(learner.grad)
+                learner.grad.mul_(1.0 / dist.get_world_size())
+            learner.apply()
+            n_updates += 1
+        if (it + 1) % cfg.log_every == 0:
+            learner.check()
+            env.check()
+            size = learner.size
+            k = min(size, 1000)
+            cur = int(learner.ring_state[0])
+            idx = [(cur - 1 - j) % cfg.buffer_capacity for j in range(k)]
+            mean_recent = float(learner.ring_rewards[idx].mean()) if k else math.nan
+            gs = int(learner.counters[1])
+            loss = float(learner.loss[1]) if gs > 0 else math.nan
+            log.append(LogRow(it + 1, loss, mean_recent, cfg.epsilon_at(it)))
+    learner.check()
+    env.check()
+    res = TrainResult(net=learner.net(), log=log, updates=int(learner.counters[1]),
+                      transitions=int(learner.ring_state[2]))
+    learner.close()
+    env.close()
+    return res
+
+
+class _PendingRecords:
+    """StepRecords view onto the learner's pending reward/flag store (rec_ld = P)."""
+
+    def __init__(self, learner: DeviceLearner):
+        self.ld = learner.P
+        self.flags = learner.pending_flags
+        self.reward = learner.pending_reward
+        self.realized = None
+
+    def struct(self) -> _lib.BeRecords:
+        r = _lib.BeRecords()
+        r.flags = self.flags.data_ptr()
+        r.reward = self.reward.data_ptr()
+        return r
+
+
+def _env_step(env: EnvBatch, arrival, task, rate, W, epsilon, seed, counter, rec, x_out, a_out):
+    E, M = env.n_envs, env.n_tiers
+    r = rec.struct()
+    _lib.check(env._L.be_env_step(env.handle, arrival.data_ptr(), task.data_ptr(), rate.data_ptr(),
+                                  None, ctypes.byref(W), -1, float(epsilon), seed & (2**64 - 1),
+                                  counter & (2**64 - 1), rec.ld, ctypes.byref(r), None, None,
+                                  a_out.data_ptr(), None, x_out.data_ptr(), _lib.stream_ptr()))
+
+
+def fine_tune(net, reward_spec, cfg: TrainConfig, tiers, encoding=None, completion_log=None, **kw):
+    """trainer.py:409-414: continue training from an existing network."""
+    return run_training(tiers, reward_spec, cfg, encoding=encoding, init_net=net,
+                        completion_log=completion_log, **kw)

@@ -1,0 +1,16 @@
+"""Training throughput probe (config 3 shape): E envs, 1M replay, batch 512."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2401_07886_b200 import default_tiers, RewardSpec
+from paper_2401_07886_b200.trainer import TrainConfig, run_training
+E = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+its = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+cfg = TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=its,
+                  log_every=its, seed=3)
+t0 = time.time()
+res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=E)
+torch.cuda.synchronize()
+dt = time.time() - t0
+print(f"E={E} its={its}: {dt:.2f}s  {its/dt:.1f} it/s  {E*its/dt:.3e} env-steps/s  "
+      f"updates={res.updates} ({res.updates/dt:.1f}/s) transitions={res.transitions} log={res.log[-1]}")
