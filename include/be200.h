@@ -17,6 +17,7 @@
  *   be_reduce_eval                   windowed + threshold_counts,  evalkit.py:217-241,
  *                                    miss_fractions_by_rate        evalkit.py:61-68
  *   be_trace_gen_stable              gen_stable (Philox, on device) workload.py:120-141
+ *   be_trace_gen                     gen_stable / gen_unpredictable_* workload.py:94-209
  *   be_learner_*                     train_step / _StepKernel /    trainer.py:211-290
  *                                    Adam                          trainer.py:177-199
  *   be_replay_*                      ReplayBuffer                  trainer.py:101-163
@@ -184,6 +185,46 @@ int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const do
 int32_t be_trace_gen_stable(int32_t n_envs, int64_t env_offset, int64_t n, int64_t ld,
                             const double* rate, int32_t n_tasks, uint64_t seed,
                             double* arrival_ms, uint8_t* task, void* stream);
+
+/* On-device workload generators (workload.py:94-209) with Philox4x32-10 keyed
+ * by (seed, env_offset + e) — every global env id gets the same trace on any
+ * number of GPUs.  Kinds:
+ *   BE_GEN_STABLE        gen_stable (workload.py:120-141): segment k holds
+ *                        rates[e][k] for hold_ms on [k*hold, (k+1)*hold)
+ *                        (Poisson arrivals, workload.py:94-111); with
+ *                        truncate = 1 the trace stops at ld events (config 1),
+ *                        else more than ld events is BE_ECAPACITY;
+ *   BE_GEN_UNPRED_TIME   gen_unpredictable_time_based (workload.py:144-171):
+ *                        band 90/8/2 %, rate uniform in the band, shifted-
+ *                        geometric count of mean 20 * rate, n requests;
+ *   BE_GEN_UNPRED_REQ    gen_unpredictable_request_based (workload.py:174-198):
+ *                        rate uniform on [1, 48], geometric count of mean 500.
+ * Tasks are uniform over task_ids[0..n_task_ids) (all of [0, n_tasks) when
+ * n_task_ids == 0), workload.py:201-209.  Outputs (device, env-major):
+ * arrival/task [E][ld], n_events [E], seg_count [E], seg_start/seg_rate
+ * [E][seg_capacity].  More than seg_capacity segments -> BE_ECAPACITY (latched
+ * in *status, a device int32[2] = {code, first env}, checked by the caller). */
+#define BE_GEN_STABLE 0
+#define BE_GEN_UNPRED_TIME 1
+#define BE_GEN_UNPRED_REQ 2
+typedef struct {
+    int32_t kind;
+    int32_t n_tasks;
+    int32_t n_task_ids;
+    int32_t task_ids[BE_MAX_TASKS];
+    int32_t n_rates;          /* BE_GEN_STABLE: segments per env */
+    int32_t truncate;         /* BE_GEN_STABLE: stop at ld events instead of failing */
+    int64_t rate_ld;          /* row stride of rates (0 = one row shared by every env) */
+    const double* rates;      /* BE_GEN_STABLE: device [E or 1][rate_ld] req/s */
+    double hold_ms;           /* BE_GEN_STABLE: segment duration */
+    int64_t n;                /* BE_GEN_UNPRED_*: requests per env (<= ld) */
+    int64_t seg_capacity;     /* segments per env the outputs can hold */
+} be_gen_cfg;
+
+int32_t be_trace_gen(const be_gen_cfg* cfg, int32_t n_envs, int64_t env_offset, int64_t ld,
+                     uint64_t seed, double* arrival_ms, uint8_t* task, int64_t* n_events,
+                     int64_t* seg_count, int64_t* seg_start, double* seg_rate, int32_t* status,
+                     void* stream);
 
 /* ---------------------------------------------------------------- training
  * Replay + learner (trainer.py:101-290) and the training workload

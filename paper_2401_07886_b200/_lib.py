@@ -69,6 +69,16 @@ class BeRecords(ctypes.Structure):
                 ("rate", ctypes.c_void_p), ("q", ctypes.c_void_p)]
 
 
+class BeGenCfg(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n_tasks", ctypes.c_int32), ("n_task_ids", ctypes.c_int32),
+                ("task_ids", ctypes.c_int32 * MAX_TASKS), ("n_rates", ctypes.c_int32),
+                ("truncate", ctypes.c_int32), ("rate_ld", ctypes.c_int64), ("rates", ctypes.c_void_p),
+                ("hold_ms", ctypes.c_double), ("n", ctypes.c_int64), ("seg_capacity", ctypes.c_int64)]
+
+
+GEN_STABLE, GEN_UNPRED_TIME, GEN_UNPRED_REQ = 0, 1, 2
+
+
 class BeLearnerCfg(ctypes.Structure):
     _fields_ = [("n_tasks", ctypes.c_int32), ("n_tiers", ctypes.c_int32), ("hidden", ctypes.c_int32),
                 ("n_envs", ctypes.c_int32), ("replay_capacity", ctypes.c_int64),
@@ -115,6 +125,8 @@ SIGNATURES = {
     "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
                               _P, _P, _P]),
     "be_trace_gen_stable": (_I32, [_I32, _I64, _I64, _I64, _P, _I32, _U64, _P, _P, _P]),
+    "be_trace_gen": (_I32, [ctypes.POINTER(BeGenCfg), _I32, _I64, _I64, _U64, _P, _P, _P, _P, _P, _P,
+                            _P, _P]),
     "be_learner_create": (_I32, [ctypes.POINTER(BeLearnerCfg), _I32, ctypes.POINTER(_P)]),
     "be_learner_destroy": (_I32, [_P]),
     "be_learner_set_params": (_I32, [_P, _P, _P, _P, _P, _P]),

@@ -264,4 +264,33 @@ int32_t be_trace_gen_stable(int32_t n_envs, int64_t env_offset, int64_t n, int64
                            (cudaStream_t)stream);
 }
 
+int32_t be_trace_gen(const be_gen_cfg* cfg, int32_t n_envs, int64_t env_offset, int64_t ld,
+                     uint64_t seed, double* arrival_ms, uint8_t* task, int64_t* n_events,
+                     int64_t* seg_count, int64_t* seg_start, double* seg_rate, int32_t* status,
+                     void* stream) {
+    if (!cfg || !arrival_ms || !task || !n_events || !seg_count || !seg_start || !seg_rate || !status)
+        return set_error(BE_EINVAL, "NULL argument");
+    // InvalidParameterError cases of workload.py:131-134, :152-153, :181-182, :201-209
+    if (n_envs < 1 || ld < 1 || env_offset < 0 || cfg->seg_capacity < 1)
+        return set_error(BE_EINVAL, "bad sizes");
+    if (cfg->n_tasks < 1 || cfg->n_tasks > 255) return set_error(BE_EINVAL, "n_tasks must be >= 1");
+    if (cfg->n_task_ids < 0 || cfg->n_task_ids > BE_MAX_TASKS)
+        return set_error(BE_EINVAL, "too many task_ids");
+    for (int k = 0; k < cfg->n_task_ids; ++k)
+        if (cfg->task_ids[k] < 0 || cfg->task_ids[k] >= cfg->n_tasks)
+            return set_error(BE_EINVAL, "task_ids must be a nonempty subset of [0, n_tasks)");
+    if (cfg->kind == BE_GEN_STABLE) {
+        if (!cfg->rates || cfg->n_rates < 1) return set_error(BE_EINVAL, "rates must be nonempty and positive");
+        if (!(cfg->hold_ms > 0) || !isfinite(cfg->hold_ms)) return set_error(BE_EINVAL, "hold_seconds must be positive");
+        if (cfg->rate_ld != 0 && cfg->rate_ld < cfg->n_rates) return set_error(BE_EINVAL, "bad rate_ld");
+    } else if (cfg->kind == BE_GEN_UNPRED_TIME || cfg->kind == BE_GEN_UNPRED_REQ) {
+        if (cfg->n < 1) return set_error(BE_EINVAL, "n_requests must be >= 1");
+        if (cfg->n > ld) return set_error(BE_EINVAL, "n_requests exceeds ld");
+    } else {
+        return set_error(BE_EINVAL, "unknown generator kind");
+    }
+    return launch_tracegen_general(cfg, n_envs, env_offset, ld, seed, arrival_ms, task, n_events,
+                                   seg_count, seg_start, seg_rate, status, (cudaStream_t)stream);
+}
+
 }  // extern "C"

@@ -50,4 +50,8 @@ int launch_route(const be_qweights* W, int T, int M, const double* x, int B, dou
                  uint64_t seed, uint64_t counter, double* q_out, uint8_t* a_out, cudaStream_t st);
 int launch_tracegen(int E, int64_t env_offset, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
                     double* arrival, uint8_t* task, cudaStream_t st);
+int launch_tracegen_general(const be_gen_cfg* cfg, int E, int64_t env_offset, int64_t ld,
+                            uint64_t seed, double* arrival, uint8_t* task, int64_t* n_events,
+                            int64_t* seg_count, int64_t* seg_start, double* seg_rate,
+                            int32_t* status, cudaStream_t st);
 }  // namespace be

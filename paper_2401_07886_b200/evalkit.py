@@ -23,6 +23,68 @@ WINDOW = 20
 THRESHOLDS = (1.00, 0.99, 0.98, 0.96, 0.94)
 PAPER_THRESHOLDS = (1.00, 0.98, 0.96, 0.94, 0.90)  # north-star: >= 90/94/96/98% of peak
 STABLE_SWEEP_RATES = (0.25, 0.5, 1.0, 2.0, 3.0, 4.0, 6.0, 8.0, 12.0, 16.0, 24.0, 32.0, 40.0, 48.0)
+STABLE_HOLD_SECONDS = 40.0
+
+
+@dataclass(frozen=True)
+class ScenarioConfig:
+    """evalkit.py:77-102 (host-side configuration, same fields and semantics)."""
+    name: str
+    workload: str = "stable"  # stable | unpredictable-time | unpredictable-request
+    rates: tuple = STABLE_SWEEP_RATES
+    hold_seconds: float = STABLE_HOLD_SECONDS
+    n_requests: int = 10_000
+    task_ids: Optional[tuple] = None
+    estimator_mode: str = "estimated"
+    reset_between_segments: bool = False
+    reward_kind: Optional[str] = None
+    deadline_overrides: tuple = ()
+    replicas: Optional[int] = None
+    gpu_count: Optional[int] = None
+
+    def adjust_rewards(self, spec):
+        if self.reward_kind is not None:
+            spec = spec.with_kind(self.reward_kind)
+        if self.deadline_overrides:
+            spec = spec.with_deadlines(dict(self.deadline_overrides))
+        return spec
+
+    def adjust_tiers(self, tiers):
+        if self.replicas is None:
+            return list(tiers)
+        from dataclasses import replace
+        return [replace(t, replicas=self.replicas) for t in tiers]
+
+
+_SCENARIOS = {  # evalkit.py:105-131
+    "stable": ScenarioConfig(name="stable", workload="stable", estimator_mode="true-rate",
+                             reset_between_segments=True),
+    "unpredictable-1": ScenarioConfig(name="unpredictable-1", workload="unpredictable-time"),
+    "unpredictable-2": ScenarioConfig(name="unpredictable-2", workload="unpredictable-request"),
+    "hellaswag-copa-soft": ScenarioConfig(name="hellaswag-copa-soft", workload="unpredictable-time",
+                                          task_ids=(0, 1), reward_kind="soft"),
+    "different-deadlines": ScenarioConfig(name="different-deadlines", workload="stable",
+                                          estimator_mode="true-rate", reset_between_segments=True,
+                                          deadline_overrides=(("openbookqa", 80.0), ("copa", 32.0))),
+    "hw-utility-8gpu": ScenarioConfig(name="hw-utility-8gpu", workload="unpredictable-time",
+                                      replicas=8, gpu_count=8),
+}
+for _k in range(4):
+    _SCENARIOS[f"single-task-{_k}"] = ScenarioConfig(
+        name=f"single-task-{_k}", workload="stable", estimator_mode="true-rate",
+        reset_between_segments=True, task_ids=(_k,))
+
+
+def scenario_names() -> list:
+    return sorted(_SCENARIOS)
+
+
+def scenario_suite(name: str) -> ScenarioConfig:
+    """evalkit.py:134-138."""
+    try:
+        return _SCENARIOS[name]
+    except KeyError:
+        raise ValueError(f"unknown scenario {name!r}; known: {', '.join(scenario_names())}")
 
 
 @dataclass

@@ -7,6 +7,7 @@ Layout in HBM (env-major, row stride `ld`):
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -144,6 +145,128 @@ class TraceBatch:
         sb = None if buckets is None else torch.as_tensor(np.asarray(buckets, np.int32), device=dev)
         return cls(arrival=arrival, task=task, n_events=None, seg_offsets=offs,
                    seg_start=seg_start, seg_rate=rate.clone(), seg_bucket=sb, n_tasks=n_tasks)
+
+    @classmethod
+    def generate(cls, workload: str, n_envs: int, n_tasks: int, seed: int, *,
+                 n_requests: int = 10_000, rates: Optional[Sequence] = None,
+                 hold_seconds: Optional[float] = None, task_ids: Optional[Sequence[int]] = None,
+                 ld: Optional[int] = None, truncate: bool = False, seg_capacity: Optional[int] = None,
+                 env_offset: int = 0, buckets: Optional[Sequence[float]] = None,
+                 device=None) -> "TraceBatch":
+        """On-device `make_trace` (evalkit.py:141-151) for `n_envs` environments.
+
+        workload: "stable" (gen_stable, workload.py:120-141: `rates` — one list
+        for every env or one list per env — each held `hold_seconds`),
+        "unpredictable-time" (workload.py:144-171) or "unpredictable-request"
+        (workload.py:174-198, `n_requests` each).  Draws are Philox4x32-10
+        keyed by (seed, env_offset + e).  `truncate` keeps the first `ld`
+        events of a stable trace (config 1); otherwise a stable trace longer
+        than `ld` raises CapacityError.  `buckets`: optional rate values; each
+        segment maps to the nearest (selection_distribution, evalkit.py:255-258)."""
+        dev = _lib.require_cuda(device)
+        if n_envs < 1:
+            raise _lib.InvalidParameterError("n_envs must be >= 1")
+        if n_tasks < 1:
+            raise _lib.InvalidParameterError("n_tasks must be >= 1")
+        cfg = _lib.BeGenCfg()
+        cfg.n_tasks = n_tasks
+        if task_ids is not None:
+            ids = [int(t) for t in task_ids]
+            if not ids or min(ids) < 0 or max(ids) >= n_tasks or len(ids) > _lib.MAX_TASKS:
+                raise _lib.InvalidParameterError(f"task_ids must be a nonempty subset of [0, {n_tasks})")
+            cfg.n_task_ids = len(ids)
+            for k, t in enumerate(ids):
+                cfg.task_ids[k] = t
+        keep = None
+        if workload == "stable":
+            if rates is None or hold_seconds is None:
+                raise _lib.InvalidParameterError("stable traces need rates and hold_seconds")
+            r = np.asarray(rates, np.float64)
+            if r.ndim == 1:
+                r = r[None, :]
+            if r.size == 0 or np.any(~(r > 0)) or not np.all(np.isfinite(r)):
+                raise _lib.InvalidParameterError("rates must be nonempty and positive")
+            if not hold_seconds > 0:
+                raise _lib.InvalidParameterError("hold_seconds must be positive")
+            if r.shape[0] not in (1, n_envs):
+                raise ValueError("rates: one row for every env or one row per env")
+            keep = torch.as_tensor(np.ascontiguousarray(r), device=dev)
+            cfg.kind = _lib.GEN_STABLE
+            cfg.n_rates = r.shape[1]
+            cfg.rate_ld = 0 if r.shape[0] == 1 else r.shape[1]
+            cfg.rates = keep.data_ptr()
+            cfg.hold_ms = float(hold_seconds) * 1000.0
+            cfg.truncate = 1 if truncate else 0
+            if ld is None:  # expected count + 8 sigma + slack
+                lam = float(np.max(r.sum(axis=1))) * float(hold_seconds)
+                ld = int(lam + 8.0 * np.sqrt(lam) + 64)
+            seg_capacity = seg_capacity or r.shape[1]
+        elif workload in ("unpredictable-time", "unpredictable-request"):
+            if n_requests < 1:
+                raise _lib.InvalidParameterError("n_requests must be >= 1")
+            cfg.kind = _lib.GEN_UNPRED_TIME if workload == "unpredictable-time" else _lib.GEN_UNPRED_REQ
+            cfg.n = n_requests
+            ld = n_requests if ld is None else ld
+            # expected segments: ~1/70 (time-based) or 1/500 (request-based) of the requests
+            seg_capacity = seg_capacity or max(64, n_requests // 8 + 64)
+        else:
+            raise ValueError(f"unknown workload kind {workload!r}")
+        cfg.seg_capacity = seg_capacity
+        E = n_envs
+        arrival = torch.empty((E, ld), dtype=torch.float64, device=dev)
+        task = torch.zeros((E, ld), dtype=torch.uint8, device=dev)
+        n_events = torch.empty(E, dtype=torch.int64, device=dev)
+        seg_count = torch.empty(E, dtype=torch.int64, device=dev)
+        ss = torch.empty((E, seg_capacity), dtype=torch.int64, device=dev)
+        sr = torch.empty((E, seg_capacity), dtype=torch.float64, device=dev)
+        status = torch.zeros(2, dtype=torch.int32, device=dev)
+        L = _lib.load()
+        _lib.check(L.be_trace_gen(ctypes.byref(cfg), E, int(env_offset), ld, seed & (2**64 - 1),
+                                  arrival.data_ptr(), task.data_ptr(), n_events.data_ptr(),
+                                  seg_count.data_ptr(), ss.data_ptr(), sr.data_ptr(),
+                                  status.data_ptr(), _lib.stream_ptr()))
+        st = status.cpu().tolist()
+        if st[0] == _lib.BE_ECAPACITY:
+            raise _lib.CapacityError(f"env {st[1]}: trace exceeds ld={ld} events or "
+                                     f"seg_capacity={seg_capacity} segments")
+        if st[0] != 0:
+            raise _lib.InvalidParameterError(f"env {st[1]}: invalid generator parameters")
+        # pad ragged rows with their last arrival so every row stays sorted
+        col = torch.arange(ld, device=dev)
+        last = arrival.gather(1, (n_events - 1).clamp(min=0)[:, None])
+        arrival = torch.where(col[None, :] < n_events[:, None], arrival, last)
+        # segment marks -> CSR
+        sel = torch.arange(seg_capacity, device=dev)[None, :] < seg_count[:, None]
+        offs = torch.zeros(E + 1, dtype=torch.int64, device=dev)
+        offs[1:] = torch.cumsum(seg_count, 0)
+        seg_start, seg_rate = ss[sel], sr[sel]
+        sb = None
+        if buckets is not None:
+            b = torch.as_tensor(np.asarray(buckets, np.float64), device=dev)
+            sb = torch.argmin((seg_rate[:, None] - b[None, :]).abs(), dim=1).to(torch.int32)
+        ragged = bool((n_events != ld).any())
+        return cls(arrival=arrival, task=task, n_events=n_events if ragged else None,
+                   seg_offsets=offs, seg_start=seg_start if seg_start.numel() else
+                   torch.zeros(1, dtype=torch.int64, device=dev),
+                   seg_rate=seg_rate if seg_rate.numel() else torch.zeros(1, device=dev, dtype=torch.float64),
+                   seg_bucket=sb, n_tasks=n_tasks)
+
+    @classmethod
+    def from_scenario(cls, scenario, n_envs: int, n_tasks: int, seed: int, *, env_offset: int = 0,
+                      device=None, **kw) -> "TraceBatch":
+        """`make_trace(scenario, n_tasks, seed)` (evalkit.py:141-151) for n_envs envs
+        on the device.  `scenario`: a ScenarioConfig-like object (workload, rates,
+        hold_seconds, n_requests, task_ids) or a scenario name."""
+        if isinstance(scenario, str):
+            from .evalkit import scenario_suite
+            scenario = scenario_suite(scenario)
+        kind = {"stable": "stable", "unpredictable-time": "unpredictable-time",
+                "unpredictable-request": "unpredictable-request"}.get(scenario.workload)
+        if kind is None:
+            raise ValueError(f"unknown workload kind {scenario.workload!r}")
+        return cls.generate(kind, n_envs, n_tasks, seed, n_requests=scenario.n_requests,
+                            rates=scenario.rates, hold_seconds=scenario.hold_seconds,
+                            task_ids=scenario.task_ids, env_offset=env_offset, device=device, **kw)
 
     # ------------------------------------------------------------- export
     def to_workload_trace(self, e: int, seed: int = 0) -> WorkloadTrace:

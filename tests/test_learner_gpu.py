@@ -138,3 +138,32 @@ def test_run_training_smoke(cuda):
     assert len(res.log) == 3 and np.isfinite(res.log[-1].loss)
     for p in res.net.params():
         assert np.all(np.isfinite(p))
+
+
+@pytest.mark.parametrize("loss,opt", [("huber", "adam"), ("squared", "adam"), ("huber", "sgd")])
+def test_learner_matches_reference_golden(cuda, loss, opt):
+    """Device learner vs the reference train_step's recorded I/O
+    (tests/golden/make_learner_golden.py): same replay contents, same sampled
+    indices -> loss (rel 1e-12), gradients (normwise 1e-10), parameters and the
+    target network after every step, for six consecutive updates."""
+    gl = goldens.learner(loss, opt)
+    m = gl["meta"]
+    s, a, r, s2, c = goldens.replay_transitions()
+    cfg = TrainConfig(batch_size=m["batch"], buffer_capacity=4096, learning_rate=m["lr"], loss=loss,
+                      optimizer=opt, target_sync_every=m["target_sync_every"], warmup=0)
+    L = DeviceLearner(4, 3, cfg, n_envs=1, pending_capacity=16)
+    L.set_params(goldens.nets()["trained"])
+    for step in range(1, m["steps"] + 1):
+        idx = gl["idx"][step - 1]
+        L.backward_batch(s[idx], a[idx], r[idx], s2[idx], c[idx])
+        L.apply(explicit_batch=True)
+        torch.cuda.synchronize()
+        lv = gl["loss"][step - 1]
+        assert abs(float(L.loss[0]) - lv) <= 1e-12 * abs(lv)
+        g_ref = gl["grad"][step - 1]
+        assert np.linalg.norm(L.grad.cpu().numpy() - g_ref) <= 1e-10 * np.linalg.norm(g_ref)
+        p_ref = gl["params"][step - 1]
+        p_dev = L.params.cpu().numpy()
+        assert np.max(np.abs(p_dev - p_ref)) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))
+        t_dev = flat(params_of(L.target_net().__dict__))
+        assert np.max(np.abs(t_dev - gl["target"][step - 1])) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))

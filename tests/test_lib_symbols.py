@@ -29,3 +29,4 @@ def test_struct_sizes_match_c():
     assert ctypes.sizeof(_lib.BeTraceSoa) == 16 + 7 * 8
     assert ctypes.sizeof(_lib.BeQWeights) == 8 + 4 * 8
     assert ctypes.sizeof(_lib.BeRecords) == 6 * 8
+    assert ctypes.sizeof(_lib.BeGenCfg) == 128

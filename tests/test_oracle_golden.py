@@ -105,3 +105,45 @@ def test_windowed_known_values():
     v = np.random.default_rng(0).random(100)
     naive = np.array([v[k:k + 20].mean() for k in range(81)])
     assert np.allclose(oracle.windowed(v), naive)
+
+
+LEARNER_CASES = [("huber", "adam"), ("squared", "adam"), ("huber", "sgd")]
+
+
+def _split(flat, like):
+    out, k = {}, 0
+    for name in ("w1", "b1", "w2", "b2"):
+        n = like[name].size
+        out[name] = flat[k:k + n].reshape(like[name].shape)
+        k += n
+    return out
+
+
+@pytest.mark.parametrize("loss,opt", LEARNER_CASES)
+def test_oracle_learner_matches_reference_train_step(loss, opt):
+    """oracle.learner_step vs the reference train_step (trainer.py:276-290) on the
+    recorded batches: loss, gradients, parameters and target sync."""
+    gl = goldens.learner(loss, opt)
+    m = gl["meta"]
+    s, a, r, s2, c = goldens.replay_transitions()
+    net = goldens.nets()["trained"]
+    params = {k: np.array(net[k], dtype=np.float64) for k in ("w1", "b1", "w2", "b2")}
+    target = {k: v.copy() for k, v in params.items()}
+    adam = oracle.adam_init(params)
+    flat = lambda d: np.concatenate([d[k].ravel() for k in ("w1", "b1", "w2", "b2")])
+    for step in range(1, m["steps"] + 1):
+        idx = gl["idx"][step - 1]
+        batch = (s[idx], a[idx], r[idx], s2[idx], c[idx])
+        lv, grads, new = oracle.learner_step(params, target, batch, discount=m["discount"],
+                                             adam_state=adam, lr=m["lr"], loss=loss)
+        if opt == "sgd":
+            new = {k: params[k] - m["lr"] * grads[k] for k in params}
+        assert abs(lv - gl["loss"][step - 1]) <= 1e-12 * abs(gl["loss"][step - 1])
+        g_ref = gl["grad"][step - 1]
+        assert np.linalg.norm(flat(grads) - g_ref) <= 1e-12 * np.linalg.norm(g_ref)
+        p_ref = gl["params"][step - 1]
+        assert np.max(np.abs(flat(new) - p_ref)) <= 1e-14 + 1e-12 * np.max(np.abs(p_ref))
+        params = _split(p_ref, params)  # continue from the reference's own parameters
+        if step % m["target_sync_every"] == 0:
+            target = {k: v.copy() for k, v in params.items()}
+        assert np.array_equal(flat(target), gl["target"][step - 1])
