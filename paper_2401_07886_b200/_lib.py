@@ -12,7 +12,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbe200.so")
+# BE200_LIB: alternative build of the same library (A/B experiments on the GPU box)
+LIB_PATH = os.environ.get("BE200_LIB") or os.path.join(_HERE, "libbe200.so")
 
 BE_OK, BE_EINVAL, BE_ECAPACITY, BE_ECUDA, BE_ENONFINITE = range(5)
 MAX_TIERS, MAX_TASKS, MAX_LANES = 8, 16, 32

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "be200.h"
@@ -27,6 +28,60 @@ void make_score_aux(const be_cfg& c, ScoreAux* aux) {
     for (int t = 0; t < c.n_tasks; ++t)
         for (int m = 0; m < c.n_tiers; ++m)
             aux->hit_tau[t * BE_MAX_TIERS + m] = tau_le(c.deadline[t], (double)c.tiers[m].tokens_per_request);
+}
+
+// round(x * 2^(52 - e)) to an integer (x >= 0); false on a rounding tie or overflow
+static bool scaled_round(double x, int e, long long& out) {
+    if (x == 0.0) {
+        out = 0;
+        return true;
+    }
+    long long bits;
+    memcpy(&bits, &x, 8);
+    int ex = (int)((bits >> 52) & 0x7ff);
+    if (ex == 0 || ex == 0x7ff || bits < 0) return false;
+    long long mx = (bits & 0xfffffffffffffLL) | (1LL << 52);
+    int s = e - (ex - 1023);  // right shift
+    if (s <= 0) {
+        if (s < -9) return false;
+        out = mx << (-s);
+        return true;
+    }
+    if (s >= 60) {
+        out = 0;
+        return true;
+    }
+    long long q = mx >> s;
+    long long rem = mx & ((1LL << s) - 1);
+    long long half = 1LL << (s - 1);
+    if (rem == half) return false;
+    out = q + (rem > half ? 1 : 0);
+    return true;
+}
+
+// D(tier m, n, e) = (RN_u(alpha_m) + RN_u(RN(beta_m * n))) with u = 2^(e - 52): the
+// exact per-cycle advance of a replica with n running requests while its clock
+// stays in binade e (be_env.cuh, skip_cycles).  0 where a rounding tie makes the
+// advance parity-dependent (the kernel then steps one iteration at a time).
+int build_skip_table(const be_cfg& c, double* out) {
+    int rows = 0;
+    for (int m = 0; m < c.n_tiers; ++m) {
+        const be_tier& t = c.tiers[m];
+        for (int n = 0; n <= t.max_batch; ++n, ++rows) {
+            if (!out) continue;
+            const double cn = t.beta_ms * (double)n;  // simcore.py:146, beta * n
+            for (int k = 0; k < SKIP_NB; ++k) {
+                const int e = SKIP_ELO + k;
+                long long a, b;
+                double D = 0.0;
+                if (n > 0 && scaled_round(t.alpha_ms, e, a) && scaled_round(cn, e, b) && a + b > 0 &&
+                    a + b < (1LL << 53))
+                    D = ldexp((double)(a + b), e - 52);
+                out[(size_t)rows * SKIP_NB + k] = D;
+            }
+        }
+    }
+    return rows;
 }
 
 static int validate_cfg(const be_cfg* c, int* lanes) {
@@ -116,6 +171,19 @@ int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env*
     }
     cudaMemset(env->d_status, 0, 64);
     env->envs = nullptr;
+    if (cfg->skip_ahead) {
+        env->skip_rows = build_skip_table(*cfg, nullptr);
+        const size_t tb = (size_t)env->skip_rows * SKIP_NB * sizeof(double);
+        double* h = (double*)malloc(tb);
+        build_skip_table(*cfg, h);
+        if ((e = cudaMalloc((void**)&env->d_skip, tb)) != cudaSuccess ||
+            (e = cudaMemcpy(env->d_skip, h, tb, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            free(h);
+            be_env_destroy(env);
+            return set_cuda_error(e, "be_env_create: skip table");
+        }
+        free(h);
+    }
     rc = launch_env_reset(env, nullptr, 0);
     if (rc) {
         be_env_destroy(env);
@@ -136,6 +204,7 @@ int32_t be_env_destroy(be_env* env) {
     cudaFree(env->reps);
     cudaFree(env->d_counter);
     cudaFree(env->d_status);
+    cudaFree(env->d_skip);
     delete env;
     return BE_OK;
 }

@@ -56,6 +56,7 @@ struct TierC {
     int max_batch;
     int tokens;
     int tier;
+    const double* skip;  // this tier's skip table [n][SKIP_NB] (smem or global), or NULL
 };
 
 // Reward constants (reward.py:45-126) staged in shared memory.
@@ -101,14 +102,15 @@ __device__ __forceinline__ void load_score(Score& s, const be_cfg& c, const Scor
 }
 
 // lane -> (tier, constants); lanes beyond the replica count get tier = -1.
-__device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane) {
+__device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane, const double* skip_tab = nullptr) {
     TierC tc;
     tc.alpha = 1.0;
     tc.beta = 0.0;
     tc.max_batch = 1;
     tc.tokens = 1;
     tc.tier = -1;
-    int acc = 0;
+    tc.skip = nullptr;
+    int acc = 0, row = 0;
 #pragma unroll
     for (int m = 0; m < BE_MAX_TIERS; ++m) {
         if (m < c.n_tiers) {
@@ -119,8 +121,10 @@ __device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane) {
                 tc.max_batch = c.tiers[m].max_batch;
                 tc.tokens = c.tiers[m].tokens_per_request;
                 tc.tier = m;
+                tc.skip = skip_tab ? skip_tab + (size_t)row * SKIP_NB : nullptr;
             }
             acc += r;
+            row += c.tiers[m].max_batch + 1;
         }
     }
     return tc;
@@ -174,115 +178,44 @@ __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Sc
 // stay inside one binade [2^e, 2^(e+1)), every double there is an integer
 // multiple of u = 2^(e-52) and t is one, so RN(t + alpha) = t + RN_u(alpha)
 // and RN(. + c) = . + RN_u(c), where RN_u rounds to the nearest multiple of u
-// (ties excluded below, as they would depend on the parity of t / u).  Hence
-// k cycles advance t by exactly k * (a + b) * u, a = RN_u(alpha) / u,
-// b = RN_u(c) / u — the same bits the iteration-by-iteration recurrence
-// produces.  Anything outside those conditions falls back to single steps.
-
-// round(x * 2^(52-e)) to an integer; false on a rounding tie or overflow.
-__device__ __forceinline__ bool scaled_round(double x, int e, long long& out) {
-    if (x == 0.0) {
-        out = 0;
-        return true;
-    }
-    long long bits = __double_as_longlong(x);
-    int ex = (int)((bits >> 52) & 0x7ff);
-    if (ex == 0 || ex == 0x7ff || bits < 0) return false;
-    long long mx = (bits & 0xfffffffffffffLL) | (1LL << 52);
-    int s = e - (ex - 1023);  // right shift
-    if (s <= 0) {
-        if (s < -9) return false;
-        out = mx << (-s);
-        return true;
-    }
-    if (s >= 60) {
-        out = 0;
-        return true;
-    }
-    long long q = mx >> s;
-    long long rem = mx & ((1LL << s) - 1);
-    long long half = 1LL << (s - 1);
-    if (rem == half) return false;
-    out = q + (rem > half ? 1 : 0);
-    return true;
-}
-
-// floor(x / d) for 0 <= x < 2^53, 1 <= d: reciprocal estimate + exact integer fix-up
-// (a 64-bit integer division is a ~70-instruction software sequence on the GPU).
-__device__ __forceinline__ long long div_floor(long long x, long long d, double inv_d) {
-    long long q = (long long)((double)x * inv_d);
-    long long rem = x - q * d;
-    while (rem < 0) {
-        --q;
-        rem += d;
-    }
-    while (rem >= d) {
-        ++q;
-        rem -= d;
-    }
-    return q;
-}
+// (ties excluded, as they would depend on the parity of t / u).  Hence k
+// cycles advance t by exactly k * D, D = RN_u(alpha) + RN_u(c) — the same bits
+// the iteration-by-iteration recurrence produces.  D depends only on (tier, n,
+// binade): the host tabulates it once per env (build_skip_table, api.cu; 0 =
+// "do not skip": a rounding tie, or the binade is outside the table) and the
+// kernels stage the table in shared memory.  Skipping keeps every operand at
+// or below (2^53 - 2) u, the second-largest double of the binade.
 
 // Number k <= kmax of whole START->END cycles that can be jumped from a START
-// at time t (t < until) with constant increment; writes the time after k cycles.
-// Per-lane cache of the binade increment d = a + b (and 1/d), valid for one
-// (binade exponent, batch size) pair: recomputed only when either changes.
-struct SkipCache {
-    int e;       // biased exponent of the binade, -1 = empty
-    int n;       // n_active the increment was computed for
-    long long d; // increment in units of u; <= 0 = skipping impossible here
-    double inv_d;
-};
-
-__device__ __forceinline__ void skip_cache_reset(SkipCache& s) {
-    s.e = -1;
-    s.n = -1;
-    s.d = 0;
-    s.inv_d = 0.0;
-}
-
-__device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int n, int kmax,
-                                           double until, double& t_out, SkipCache& sc) {
-    long long bits = __double_as_longlong(t);
-    int ext = (int)((bits >> 52) & 0x7ff);
-    if (kmax <= 0 || ext == 0 || ext == 0x7ff || bits < 0) return 0;
-    int e = ext - 1023;
-    long long T0 = (bits & 0xfffffffffffffLL) | (1LL << 52);
-    if (ext != sc.e || n != sc.n) {
-        long long a, b;
-        sc.e = ext;
-        sc.n = n;
-        sc.d = (scaled_round(alpha, e, a) && scaled_round(c, e, b)) ? a + b : 0;
-        sc.inv_d = sc.d > 0 ? __drcp_rn((double)sc.d) : 0.0;
+// at time t (0 < t < until); writes the time after k cycles.  `tab` is this
+// tier's table, indexed [n][binade - SKIP_ELO].
+__device__ __forceinline__ int skip_cycles(double t, const double* __restrict__ tab, int n, int kmax,
+                                           double until, double& t_out) {
+    if (kmax <= 0) return 0;
+    const int hi = __double2hiint(t);
+    const int ib = ((hi >> 20) & 0x7ff) - (1023 + SKIP_ELO);
+    if ((unsigned)ib >= (unsigned)SKIP_NB || hi < 0) return 0;
+    const double D = tab[n * SKIP_NB + ib];
+    if (!(D > 0.0)) return 0;
+    // (2^53 - 2) u: same exponent as t, mantissa all ones but the last bit
+    const double top = __hiloint2double(hi | 0x000fffff, (int)0xfffffffe);
+    // x = min(top, until) - t is exact: both operands are multiples of u in t's binade
+    const double x = __dsub_rn(until < top ? until : top, t);
+    // k D <= x  <=>  RN(k D - x) <= 0 (rounding never changes a sign)
+    double q;
+    if (__fma_rn((double)kmax, D, -x) <= 0.0) {
+        q = (double)kmax;  // common case: the next completion comes first
+    } else {
+        // floor(x / D) < kmax: float-reciprocal estimate, one refinement, exact sign fix-ups
+        const double r = (double)__fdividef(1.0f, (float)D);
+        q = floor(__dmul_rn(x, r));
+        q = __dadd_rn(q, floor(__dmul_rn(__fma_rn(-q, D, x), r)));
+        while (__fma_rn(q, D, -x) > 0.0) q = __dsub_rn(q, 1.0);
+        while (__fma_rn(__dadd_rn(q, 1.0), D, -x) <= 0.0) q = __dadd_rn(q, 1.0);
     }
-    const long long d = sc.d;
-    if (d <= 0) return 0;
-    const long long TOP = 1LL << 53;
-    long long x = TOP - 2 - T0;  // T0 + k d <= 2^53 - 2 keeps every operand in the binade
-    // horizon: the k-th END must satisfy t_k <= until, i.e. k d <= floor(until/u) - T0
-    long long ub = __double_as_longlong(until);
-    int exu = (int)((ub >> 52) & 0x7ff);
-    if (exu != 0x7ff) {  // finite
-        int sh = (exu - 1023) - e;  // until >= t  =>  sh >= 0
-        if (sh < 0) return 0;
-        if (sh < 10) {
-            long long mu = (ub & 0xfffffffffffffLL) | (1LL << 52);
-            long long xu = (mu << sh) - T0;  // floor(until / u) - T0: exact
-            if (xu < x) x = xu;
-        }
-    }
-    if (x < d) return 0;
-    long long k;
-    unsigned long long lo = (unsigned long long)kmax * (unsigned long long)d;
-    if (__umul64hi((unsigned long long)kmax, (unsigned long long)d) == 0 && lo <= (unsigned long long)x)
-        k = kmax;  // common case: the next completion comes first (no division)
-    else
-        k = div_floor(x, d, sc.inv_d);
-    if (k > kmax) k = kmax;
-    if (k <= 0) return 0;
-    long long Tk = T0 + k * d;
-    t_out = __longlong_as_double(((long long)(e + 1023) << 52) | (Tk - (1LL << 52)));
-    return (int)k;
+    if (!(q > 0.0)) return 0;
+    t_out = __fma_rn(q, D, t);  // t + k D is a multiple of u inside the binade: exact
+    return (int)q;
 }
 
 // ---------------------------------------------------------------------------
@@ -291,8 +224,7 @@ __device__ __forceinline__ int skip_cycles(double t, double alpha, double c, int
 // processed, START at the horizon stays pending (simcore.py:120).
 // Returns false if the iteration counter would overflow.
 __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double until, Slot* ring,
-                                             uint32_t mask, const Score& sc, const RecOut& o,
-                                             bool skip, SkipCache& skc) {
+                                             uint32_t mask, const Score& sc, const RecOut& o) {
     while (r.kind != K_NONE) {
         if (r.kind == K_START) {
             if (!(r.t < until)) break;
@@ -304,11 +236,10 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
                 r.n_running = n_active;
             }
             double c = __dmul_rn(tc.beta, (double)n_active);
-            if (skip) {
+            if (tc.skip) {
                 int K = r.h_join + tc.tokens - r.iters;  // ENDs until the head completes
                 double tn;
-                int k = skip_cycles(r.t, tc.alpha, c, n_active, min(K - 1, (1 << 30) - r.iters), until,
-                                    tn, skc);
+                int k = skip_cycles(r.t, tc.skip, n_active, min(K - 1, (1 << 30) - r.iters), until, tn);
                 if (k > 0) {
                     r.t = tn;
                     r.iters += k;
@@ -406,77 +337,82 @@ __device__ __forceinline__ double estimator_observe(Estimator& est, double t, bo
 }
 
 // ---------------------------------------------------------------------------
-// Q-network forward for one state, spread over the warp (policy.py:111-118):
-// lane l owns hidden units j = l + 32k.  Weights in shared memory:
-// sW1 [D][H] (as BEQN1), sb1 [H], sW2t [M][H] (transposed), sb2 [M].
-// Result q[] is bit-identical on every lane (xor-butterfly sums commute).
-// Same forward over a group of LPE lanes (LPE = 16: two environments per
-// warp); lane g of the group owns hidden units j = g + LPE k.
+// Q-network forward for one state over a group of LPE lanes (policy.py:111-118;
+// LPE = 16: two environments per warp).  Lane g of the group owns hidden units
+// j = g + LPE k.  Shared-memory layout (stage_qnet), chosen so one hidden unit
+// costs 1 + ceil((2M+1)/2) loads, all bank-conflict free:
+//   task rows  [T][H]        W1[t][j] + b1[j]   (the one-hot input selects one;
+//                                                 b1 is folded in at staging)
+//   pairs      [NP][H] double2   consecutive entries of v_j = (W1[T+0][j] ..
+//                                W1[T+M-1][j], W1[T+M][j] (rate), W2[j][0..M-1])
+//   odd        [H]            v_j[2M] when 2M+1 is odd (always)
+//   b2         [M]
+// Result q[] is bit-identical on every lane of the group (xor-butterfly sums
+// commute).  (Measured: a second accumulator set for shorter DFMA chains is
+// slower here — more live registers for no latency win.)
+template <int M>
+struct QLayout {
+    static constexpr int NV = 2 * M + 1;  // per-hidden-unit values besides the task row
+    static constexpr int NP = NV / 2;
+    __host__ __device__ static size_t doubles(int T, int H) { return (size_t)(T + NV) * H + M; }
+};
+
+template <int M>
+__device__ __forceinline__ void stage_qnet(const double* __restrict__ w1, const double* __restrict__ b1,
+                                           const double* __restrict__ w2, const double* __restrict__ b2,
+                                           int T, int H, double* sw) {
+    constexpr int NV = QLayout<M>::NV, NP = QLayout<M>::NP;
+    for (int k = threadIdx.x; k < T * H; k += blockDim.x) sw[k] = __dadd_rn(w1[k], b1[k % H]);
+    double* pairs = sw + (size_t)T * H;
+    for (int k = threadIdx.x; k < NV * H; k += blockDim.x) {
+        const int v = k / H, j = k % H;
+        // v < M: tier inputs, v == M: rate input (W1 rows T..T+M); v > M: W2[j][v-M-1]
+        const double x = v <= M ? w1[(size_t)(T + v) * H + j] : w2[(size_t)j * M + (v - M - 1)];
+        if (v < 2 * NP) pairs[((size_t)(v >> 1) * H + j) * 2 + (v & 1)] = x;
+        else pairs[(size_t)2 * NP * H + j] = x;
+    }
+    double* sb2 = sw + (size_t)(T + NV) * H;
+    for (int k = threadIdx.x; k < M; k += blockDim.x) sb2[k] = b2[k];
+}
+
 template <int M, int LPE>
-__device__ __forceinline__ void qnet_group(const double* __restrict__ sW1,
-                                           const double* __restrict__ sW2t,
-                                           const double* __restrict__ sb2, int T, int H, int task,
+__device__ __forceinline__ void qnet_group(const double* __restrict__ sw, int T, int H, int task,
                                            const double (&xt)[M], double xr, double (&q)[M]) {
+    constexpr int NV = QLayout<M>::NV, NP = QLayout<M>::NP;
     const int g = threadIdx.x & (LPE - 1);
-    double acc[M];
+    const double* wtask = sw + (size_t)task * H;
+    const double2* pairs = reinterpret_cast<const double2*>(sw + (size_t)T * H);
+    const double* odd = sw + (size_t)T * H + (size_t)2 * NP * H;
+    const double* sb2 = sw + (size_t)(T + NV) * H;
+    double a[M];
 #pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = 0.0;
-    const double* wtask = sW1 + task * H;
-    const double* wtier = sW1 + T * H;
-    const double* wrate = sW1 + (T + M) * H;
-#pragma unroll 4
+    for (int m = 0; m < M; ++m) a[m] = 0.0;
+#pragma unroll 8
     for (int j = g; j < H; j += LPE) {
-        double pre = wtask[j];  // W1[task][j] + b1[j] (folded at staging)
+        double v[NV];
 #pragma unroll
-        for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], wtier[m * H + j], pre);
-        pre = __fma_rn(xr, wrate[j], pre);
+        for (int p = 0; p < NP; ++p) {
+            const double2 w = pairs[(size_t)p * H + j];
+            v[2 * p] = w.x;
+            v[2 * p + 1] = w.y;
+        }
+        if (NV & 1) v[NV - 1] = odd[j];
+        double pre = wtask[j];
+#pragma unroll
+        for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], v[m], pre);
+        pre = __fma_rn(xr, v[M], pre);
         const long long pb = __double_as_longlong(pre);
-        const double h = __longlong_as_double(pb & ~(pb >> 63));  // relu
+        const double h = __longlong_as_double(pb & ~(pb >> 63));
 #pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
+        for (int m = 0; m < M; ++m) a[m] = __fma_rn(h, v[M + 1 + m], a[m]);
     }
 #pragma unroll
     for (int off = LPE / 2; off > 0; off >>= 1) {
 #pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = __dadd_rn(acc[m], __shfl_xor_sync(FULL, acc[m], off));
+        for (int m = 0; m < M; ++m) a[m] = __dadd_rn(a[m], __shfl_xor_sync(FULL, a[m], off));
     }
 #pragma unroll
-    for (int m = 0; m < M; ++m) q[m] = __dadd_rn(acc[m], sb2[m]);
-}
-
-template <int M>
-__device__ __forceinline__ void qnet_warp(const double* __restrict__ sW1,
-                                          const double* __restrict__ sb1,
-                                          const double* __restrict__ sW2t,
-                                          const double* __restrict__ sb2, int T, int H, int task,
-                                          const double (&xt)[M], double xr, double (&q)[M]) {
-    int lane = threadIdx.x & 31;
-    double acc[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) acc[m] = 0.0;
-    const double* wtask = sW1 + task * H;
-    const double* wtier = sW1 + T * H;
-    const double* wrate = sW1 + (T + M) * H;
-#pragma unroll 4
-    for (int j = lane; j < H; j += 32) {
-        double pre = wtask[j];
-#pragma unroll
-        for (int m = 0; m < M; ++m) pre = __fma_rn(xt[m], wtier[m * H + j], pre);
-        pre = __fma_rn(xr, wrate[j], pre);  // b1 is folded into the task rows
-        // relu by sign-mask (3 integer ops instead of a compare/select chain);
-        // equals max(pre, 0) for every non-NaN input
-        const long long pb = __double_as_longlong(pre);
-        const double h = __longlong_as_double(pb & ~(pb >> 63));
-#pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = __dadd_rn(acc[m], __shfl_xor_sync(FULL, acc[m], off));
-    }
-#pragma unroll
-    for (int m = 0; m < M; ++m) q[m] = __dadd_rn(acc[m], sb2[m]);
+    for (int m = 0; m < M; ++m) q[m] = __dadd_rn(a[m], sb2[m]);
 }
 
 // np.argmax semantics: first NaN if any, else first maximum.

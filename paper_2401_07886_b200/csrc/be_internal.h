@@ -6,6 +6,11 @@
 
 #include "be200.h"
 
+// Skip table (exact iteration skipping, be_env.cuh): D per (tier, n in
+// [0, max_batch], binade e in [SKIP_ELO, SKIP_ELO + SKIP_NB)), doubles.
+constexpr int SKIP_NB = 32;
+constexpr int SKIP_ELO = -2;
+
 struct be_env {
     be_cfg cfg;
     int32_t E;        // environments
@@ -19,6 +24,8 @@ struct be_env {
     void* envs;       // step API: [E] EnvState
     int32_t* d_counter;
     int32_t* d_status;  // [0] code, [1] env
+    double* d_skip;     // skip table [sum_m (max_batch_m + 1)][SKIP_NB], NULL = skipping off
+    int32_t skip_rows;
 };
 
 namespace be {
@@ -30,10 +37,12 @@ void make_score_aux(const be_cfg& c, ScoreAux* aux);
 double tau_le(double theta, double w);
 double tau_ge(double theta, double w);
 int set_error(int code, const char* msg);
+// Host: tabulate the per-cycle increment D(tier, n, binade) (0 = do not skip).
+int build_skip_table(const be_cfg& c, double* out /* [rows][SKIP_NB] or NULL */);
 int set_cuda_error(cudaError_t e, const char* where);
 int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
                    const uint8_t* forced, const be_records* rec, cudaStream_t st);
-size_t rollout_smem_bytes(int T, int M, int H, bool policy);
+size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows = 0);
 int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st);
 int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
                     const double* true_rate, const uint8_t* forced, const be_qweights* W,

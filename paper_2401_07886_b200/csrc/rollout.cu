@@ -43,29 +43,13 @@ struct RolloutParams {
     int32_t R;  // replicas per env (= active lanes per group)
     int32_t* env_counter;
     int32_t* status;  // [0] = error code, [1] = first failing env
+    const double* skip;  // skip table (global), NULL = skipping off
+    int32_t skip_rows;
+    int32_t skip_smem;   // 1 = stage the skip table in shared memory
 };
 
 __device__ __forceinline__ void raise_status(int32_t* status, int code, int env) {
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
-}
-
-// Shared-memory staging: Score, then W1 [D][H] (task rows + b1), b1 [H], W2^T [M][H], b2 [M].
-template <int M>
-__device__ void stage_weights(const RolloutParams& p, double* sw, int T) {
-    const int H = p.H, D = T + M + 1;
-    // task rows carry the layer-1 bias: base[t][j] = W1[t][j] + b1[j] (the one-hot
-    // input selects exactly one of them); the forward then skips the bias add
-    for (int k = threadIdx.x; k < D * H; k += blockDim.x)
-        sw[k] = k < T * H ? __dadd_rn(p.w1[k], p.b1[k % H]) : p.w1[k];
-    double* sb1 = sw + D * H;
-    for (int k = threadIdx.x; k < H; k += blockDim.x) sb1[k] = p.b1[k];
-    double* sw2t = sb1 + H;
-    for (int k = threadIdx.x; k < M * H; k += blockDim.x) {
-        int m = k / H, j = k % H;
-        sw2t[k] = p.w2[j * M + m];
-    }
-    double* sb2 = sw2t + M * H;
-    for (int k = threadIdx.x; k < M; k += blockDim.x) sb2[k] = p.b2[k];
 }
 
 // Sum / min over the lanes of this lane's group (REDUX over the warp with the
@@ -93,22 +77,24 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
     const int T = p.cfg.n_tasks;
     const bool policy = p.forced == nullptr && p.static_tier < 0;
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
-    if (policy) stage_weights<M>(p, sw, T);
+    const int H = p.H;
+    if (policy) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
+    const double* skip_tab = p.skip;
+    if (p.skip && p.skip_smem) {  // after the weights (policy) or right after Score
+        double* st = sw + (policy ? QLayout<M>::doubles(T, H) : 0);
+        for (int k = threadIdx.x; k < p.skip_rows * SKIP_NB; k += blockDim.x) st[k] = p.skip[k];
+        skip_tab = st;
+    }
     __syncthreads();
-    const int H = p.H, D = T + M + 1;
-    const double* sW1 = sw;
-    const double* sW2t = sw + D * H + H;
-    const double* sb2 = sW2t + M * H;
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPE - 1);       // lane within the env group
     const int grp = LPE == 32 ? 0 : lane / LPE;
     const int g0 = grp * LPE;              // first lane of the group
     const unsigned gmask = LPE == 32 ? FULL : (0xffffu << g0);
-    const TierC tc = lane_tier(p.cfg, gl);
+    const TierC tc = lane_tier(p.cfg, gl, skip_tab);
     const bool active_lane = tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
-    const bool skip = p.cfg.skip_ahead != 0;
     const bool true_rate = p.cfg.estimator_true_rate != 0;
     const bool reset_segs = p.cfg.reset_between_segments != 0;
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -128,8 +114,6 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
     Slot* ring = p.rings;
     Rep r;
     rep_reset(r);
-    SkipCache skc;
-    skip_cache_reset(skc);
     Estimator est;
     est.n = 0;
 #pragma unroll
@@ -158,7 +142,6 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
                 ring = p.rings + ((size_t)env * p.R + (active_lane ? gl : 0)) * ((size_t)mask + 1);
                 rep_reset(r);
                 r.head = 0;
-                skip_cache_reset(skc);
                 est.n = 0;
                 ok = true;
                 bad = false;
@@ -186,7 +169,7 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
         if (live) {
             while (i >= next_seg) {  // segment boundaries (evalkit.py:186-192)
                 if (reset_segs && i == next_seg && i > 0) {
-                    if (active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out, skip, skc);
+                    if (active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out);
                     rep_reset(r);
                     est.n = 0;
                 }
@@ -194,7 +177,7 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
                 ++seg;
                 next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
             }
-            if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out, skip, skc);
+            if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out);
             // true-rate mode never reads the arrival window (workload.py:241-242)
             rate = true_rate ? cur_rate : estimator_observe(est, U, false, cur_rate, p.cfg.prior_rate);
         }
@@ -212,7 +195,7 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
 #pragma unroll
             for (int m = 0; m < M; ++m) xt[m] = __dmul_rn((double)obs[m], inv_scale[m]);
             const double xr = __dmul_rn(rate, inv_rate_scale);
-            qnet_group<M, LPE>(sW1, sW2t, sb2, T, H, task, xt, xr, q);
+            qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
             tier = argmax_first<M>(q);
             if (live && p.rec.q && gl < M) {
 #pragma unroll
@@ -241,7 +224,7 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
         const bool gfail = (__ballot_sync(FULL, live && (!ok || bad)) & gmask) != 0;
         const bool gbad = (__ballot_sync(FULL, live && bad) & gmask) != 0;
         if (!dead && (gfail || i >= n)) {
-            if (!gfail && active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out, skip, skc);
+            if (!gfail && active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out);
             const bool drain_fail = (__ballot_sync(gmask, !ok) & gmask) != 0;
             if (gl == 0) {
                 if (gbad) raise_status(p.status, BE_EINVAL, env);
@@ -252,9 +235,10 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
     }
 }
 
-size_t rollout_smem_bytes(int T, int M, int H, bool policy) {
+size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows) {
     size_t s = (sizeof(Score) + 15) & ~size_t(15);
-    if (policy) s += sizeof(double) * ((size_t)(T + M + 1) * H + H + (size_t)M * H + M);
+    if (policy) s += sizeof(double) * ((size_t)(T + 2 * M + 1) * H + M);  // QLayout<M>::doubles
+    s += sizeof(double) * (size_t)skip_rows * SKIP_NB;
     return s;
 }
 
@@ -283,7 +267,7 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
 
 template <int M>
 static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
-    if (p.R <= 16 && (p.H == 0 || p.H % 16 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms);
+    if (p.R <= 16 && (p.H == 0 || p.H % 32 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms);
     return launch_rollout_m<M, 32>(p, smem, st, sms);
 }
 
@@ -317,7 +301,11 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
         p.w2 = W->w2;
         p.b2 = W->b2;
     }
-    size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy);
+    p.skip = env->d_skip;
+    p.skip_rows = env->skip_rows;
+    // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
+    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows) <= 100 * 1024;
+    size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0);
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
     switch (M) {

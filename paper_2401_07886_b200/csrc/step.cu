@@ -73,6 +73,7 @@ struct StepParams {
     double* x_out;
     int32_t* status;
     int32_t drain;
+    const double* skip;  // skip table (global), NULL = skipping off
 };
 
 template <int M>
@@ -84,34 +85,25 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     const int H = p.H, D = T + M + 1;
     const bool policy = !p.drain && p.forced == nullptr && p.static_tier < 0;
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
-    if (policy) {
-        for (int k = threadIdx.x; k < D * H; k += blockDim.x)
-            sw[k] = k < T * H ? __dadd_rn(p.w1[k], p.b1[k % H]) : p.w1[k];  // b1 folded
-        for (int k = threadIdx.x; k < H; k += blockDim.x) sw[D * H + k] = p.b1[k];
-        for (int k = threadIdx.x; k < M * H; k += blockDim.x) sw[D * H + H + k] = p.w2[(k % H) * M + k / H];
-        for (int k = threadIdx.x; k < M; k += blockDim.x) sw[D * H + H + M * H + k] = p.b2[k];
-    }
+    if (policy) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
     __syncthreads();
     const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (e >= p.E) return;
     const int lane = threadIdx.x & 31;
-    const TierC tc = lane_tier(p.cfg, lane);
+    const TierC tc = lane_tier(p.cfg, lane, p.skip);  // skip table read through L1
     const bool al = tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
     Slot* ring = p.rings + ((size_t)e * p.R + (al ? lane : 0)) * ((size_t)mask + 1);
     Rep r;
     if (al) r = reps_of(p.state, e, p.R)[lane];
     else rep_reset(r);
-    SkipCache skc;
-    skip_cache_reset(skc);
     EnvState* es = state_of(p.state, e, p.E, p.R);
     // records are indexed by request id modulo rec_ld (a ring for long runs)
     // complete() writes at base + id; id is the 24-bit slot id.
     RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, (int64_t)e * p.rec_ld};
     bool ok = true;
-    const bool skip = p.cfg.skip_ahead != 0;
     if (p.drain) {
-        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out, skip, skc);
+        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out);
         if (al) reps_of(p.state, e, p.R)[lane] = r;
         const bool all_ok = __all_sync(FULL, ok);
         if (!all_ok && lane == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
@@ -119,7 +111,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     }
     const double U = p.arrival[e];
     const int task = p.task[e];
-    if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out, skip, skc);
+    if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out);
     Estimator est;
 #pragma unroll
     for (int k = 0; k < 5; ++k) est.w[k] = es->w[k];
@@ -152,7 +144,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
                 tier = (int)below(rnd.x[2], (uint32_t)M);
             }
         }
-        qnet_warp<M>(sw, sw + D * H, sw + D * H + H, sw + D * H + H + M * H, T, H, task, xt, xr, q);
+        qnet_group<M, 32>(sw, T, H, task, xt, xr, q);
         if (!explore) tier = argmax_first<M>(q);
     }
     if (lane < M) {
@@ -246,6 +238,7 @@ static StepParams base_params(be_env* env, int64_t rec_ld, const be_records* rec
     p.rec = *rec;
     p.status = env->d_status;
     p.static_tier = -1;
+    p.skip = env->d_skip;
     return p;
 }
 

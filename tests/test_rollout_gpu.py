@@ -159,3 +159,40 @@ def test_reducer_matches_reference(cuda, name):
     assert int(red.bucket_miss[0, 0]) == int(np.sum(g["realized"] > dl[g["task"]]))
     assert int(red.bucket_req[0, 0]) == len(g["arrival"])
     assert float(red.bucket_reward[0, 0]) == pytest.approx(float(np.sum(g["reward"])), rel=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_skip_table_random_tiers_match_oracle(cuda, seed):
+    """Exact iteration skipping (host-tabulated per-(tier, n, binade) increments)
+    against the oracle's one-iteration-at-a-time recurrence on random,
+    mostly non-dyadic tier constants (alpha in (0.1, 40), beta in {0, dyadic,
+    non-dyadic}), few tokens, arrivals quantised to force END == arrival ties,
+    and traces that cross many binades."""
+    rng = np.random.default_rng(100 + seed)
+    M = int(rng.integers(1, 4))
+    tiers = []
+    for m in range(M):
+        beta = [0.0, 0.25, 1.2, float(rng.uniform(0.01, 3.0)), 1.0 / 3.0][int(rng.integers(0, 5))]
+        tiers.append(dict(replicas=int(rng.integers(1, 5)), alpha_ms=float(rng.uniform(0.1, 40.0)),
+                          beta_ms=beta, max_batch=int(rng.integers(1, 9)),
+                          tokens_per_request=int(rng.integers(1, 200))))
+    T = 2
+    reward = dict(tasks=[dict(name="a", deadline=40.0, kind="hard"), dict(name="b", deadline=25.0, kind="soft")],
+                  matrix=[[float(x) for x in rng.uniform(0, 1, M)] for _ in range(T)],
+                  decay=0.01, cutoff=0.1)
+    E, n = 24, 3000
+    arr = np.cumsum(rng.exponential(rng.uniform(5, 400), size=(E, n)), axis=1)
+    arr[::2] = np.floor(arr[::2] / 5.0) * 5.0  # quantised: ties between END and arrivals
+    tsk = rng.integers(0, T, size=(E, n)).astype(np.uint8)
+    forced = rng.integers(0, M, size=(E, n)).astype(np.uint8)
+    meta = dict(tiers=tiers, reward=reward)
+    tb = TraceBatch.from_arrays(arr, tsk, [[0]] * E, [[1.0]] * E)
+    ro = GreedyRollout(tiers_of(meta), reward_of(meta), E, n, None, estimator_mode="estimated",
+                       want_steps=True)
+    o = ro.run(tb, forced=torch.as_tensor(forced, device=cuda))
+    for e in range(E):
+        ref = oracle.run_eval_oracle(tiers=tiers, reward=reward, arrival=arr[e], task=tsk[e],
+                                     seg_start=[0], seg_rate=[1.0], forced_actions=forced[e])
+        for k in ("reward", "realized", "obs"):
+            got = getattr(o, k)[e, :n].cpu().numpy()
+            assert np.array_equal(got, ref[k]), f"env {e} {k} first diff {first_diff(got.ravel(), ref[k].ravel())}"
