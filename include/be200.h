@@ -256,7 +256,8 @@ typedef struct {
     int32_t nparam;
     int32_t _pad;
     double* loss;                /* [0] loss of the last backward, [1] loss of the last update */
-    int64_t* counters;           /* [0] Adam t, [1] gradient steps, [2] any update applied */
+    int64_t* counters;           /* [0] Adam t, [1] gradient steps, [2] any update applied,
+                                    [3] iteration index (be_train_iteration) */
     double* ring_states;         /* [C][D] */
     double* ring_next_states;    /* [C][D] */
     uint8_t* ring_actions;       /* [C] */
@@ -294,6 +295,32 @@ int32_t be_learner_backward_batch(be_learner* learner, const double* states,
 /* Adam/SGD on views.grad, then the target sync every target_sync_every steps. */
 int32_t be_learner_apply(be_learner* learner, int32_t explicit_batch, void* stream);
 int32_t be_learner_check(be_learner* learner, void* stream);
+
+/* One iteration of run_training's loop (trainer.py:374-401) for all E envs,
+ * with EVERY per-iteration value read from device memory — the iteration index
+ * `it` (views.counters[3]), epsilon_at(it) (trainer.py:85-90), the Philox
+ * counters — so a CUDA graph of K iterations replays unchanged:
+ *   workload(it) -> be_env_step(epsilon_at(it), counter it; x/action into the
+ *   pending slot it % P) -> commit(it) -> update(s) -> it += 1.
+ * Bit-identical to driving be_learner_workload / be_env_step / be_learner_commit
+ * / be_learner_backward / be_learner_apply from the host with the same seeds.
+ * phase 0: whole iteration; each update is ONE fused kernel (Double-Q targets,
+ *          Huber backward, tile reduction and Adam in the last CTA to finish).
+ * phase 1: (update_index 0: env part, then) the gradients of update
+ *          `update_index` into views.grad — all-reduce them here (DP learner);
+ * phase 2: optimizer step of update `update_index`; the last one advances it. */
+typedef struct {
+    uint64_t workload_seed, policy_seed, sample_seed;
+    double epsilon_start, epsilon_end;
+    int64_t epsilon_decay_steps;  /* int(epsilon_decay_fraction * total_iterations) */
+    int32_t updates_per_step;
+    int32_t phase;
+    int32_t update_index;
+    int32_t _pad;
+} be_train_iter_cfg;
+
+int32_t be_train_iteration(be_learner* learner, be_env* env, const be_train_iter_cfg* cfg,
+                           void* stream);
 
 #ifdef __cplusplus
 }

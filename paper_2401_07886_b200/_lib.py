@@ -92,6 +92,14 @@ class BeLearnerCfg(ctypes.Structure):
                 ("regime_mean_seconds", ctypes.c_double), ("regime_mean_requests", ctypes.c_double)]
 
 
+class BeTrainIterCfg(ctypes.Structure):
+    _fields_ = [("workload_seed", ctypes.c_uint64), ("policy_seed", ctypes.c_uint64),
+                ("sample_seed", ctypes.c_uint64), ("epsilon_start", ctypes.c_double),
+                ("epsilon_end", ctypes.c_double), ("epsilon_decay_steps", ctypes.c_int64),
+                ("updates_per_step", ctypes.c_int32), ("phase", ctypes.c_int32),
+                ("update_index", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+
+
 class BeLearnerViews(ctypes.Structure):
     _fields_ = [("online", BeQWeights), ("target", BeQWeights), ("params", ctypes.c_void_p),
                 ("grad", ctypes.c_void_p), ("nparam", ctypes.c_int32), ("_pad", ctypes.c_int32),
@@ -138,6 +146,7 @@ SIGNATURES = {
     "be_learner_backward_batch": (_I32, [_P, _P, _P, _P, _P, _P, _I32, _P]),
     "be_learner_apply": (_I32, [_P, _I32, _P]),
     "be_learner_check": (_I32, [_P, _P]),
+    "be_train_iteration": (_I32, [_P, _P, ctypes.POINTER(BeTrainIterCfg), _P]),
 }
 
 _lib = None

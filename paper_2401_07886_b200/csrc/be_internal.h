@@ -50,6 +50,11 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
                     int64_t rec_ld, const be_records* rec, int32_t* obs_out, double* rate_out,
                     uint8_t* action_out, double* q_out, double* x_out, cudaStream_t st);
 int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st);
+int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
+                        const double* true_rate, const be_qweights* W, uint64_t seed,
+                        const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
+                        int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
+                        double* x_base, cudaStream_t st);
 size_t env_state_bytes_per_env(int R);
 int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* reward, int window,
                   const double* thetas, int n_theta, int n_buckets, int64_t* win_counts,

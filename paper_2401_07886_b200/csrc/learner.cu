@@ -35,9 +35,10 @@ constexpr int LTHREADS = 256;  // one thread per hidden unit (looping for H > 25
 __global__ void train_workload_kernel(int E, double* state, double log_lo, double log_hi,
                                       int equal_time, double mean_seconds, double mean_requests,
                                       int n_tasks, uint64_t seed, uint64_t step, double* arrival,
-                                      uint8_t* task, double* rate_out) {
+                                      uint8_t* task, double* rate_out, const int64_t* step_dev) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
+    if (step_dev) step = (uint64_t)*step_dev;  // be_train_iteration: iteration index on device
     double t = state[3 * e], rate = state[3 * e + 1], left = state[3 * e + 2];
     P4 a = philox4x32_10(step * 2, (uint64_t)e, seed);
     if (left <= 0.0) {
@@ -79,6 +80,7 @@ struct CommitParams {
     double* rr;              // ring rewards [C]
     double* rc;              // ring continue flags [C]
     int32_t* status;
+    const int64_t* step_dev;  // be_train_iteration: `step` read from device memory
 };
 
 // A transition j is ready when its reward is known and j <= step - 1 (its next
@@ -89,7 +91,8 @@ __global__ void commit_kernel(const CommitParams p) {
     const int lane = threadIdx.x & 31;
     if (e >= p.E) return;
     int64_t lo = p.low[e];
-    const int64_t hi = p.step - 1;  // inclusive upper candidate
+    const int64_t step = p.step_dev ? *p.step_dev : p.step;
+    const int64_t hi = step - 1;  // inclusive upper candidate
     int64_t base = WRITE ? p.offset[e] : 0;
     int total = 0;
     int64_t new_low = lo;
@@ -134,7 +137,7 @@ __global__ void commit_kernel(const CommitParams p) {
         } else {
             p.low[e] = new_low;
             // the pending ring must hold every uncommitted request
-            if (p.step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0)
+            if (step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0)
                 p.status[1] = e;
         }
     }
@@ -207,6 +210,9 @@ struct LearnParams {
     int32_t huber;
     double* partial;  // [nCTA][P + 1]: grads w1,b1,w2,b2 then loss
     int64_t* sample_idx;  // [B] (optional debug output)
+    // be_train_iteration: Philox counter = (*iter_dev) * ups + uidx
+    const int64_t* iter_dev;
+    int32_t ups, uidx;
 };
 
 __device__ __forceinline__ double relu_d(double x) {
@@ -244,7 +250,82 @@ __device__ void forward_rows(const double* x, int D, int H, int M, const double*
     (void)red;
 }
 
-__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
+struct ApplyParams {
+    int32_t nparam;
+    double* params;   // online [nparam] (w1, b1, w2, b2 contiguous)
+    double* target;   // [nparam]
+    double* m;
+    double* v;
+    const double* grad;
+    int64_t* counters;  // [0] adam t, [1] grad steps, [2] updates applied flag, [3] iteration
+    double lr, beta1, beta2, eps;
+    int32_t adam;
+    int64_t sync_every;
+    const int64_t* ring_state;
+    int64_t min_size;
+    int32_t sampling;
+    double* loss;        // current loss
+    double* last_loss;   // persisted "last_loss" for logs
+    int32_t advance;     // 1: counters[3] += 1 afterwards (last update of a be_train_iteration)
+};
+
+// Adam (trainer.py:190-199) or SGD (:202-208), then the target sync
+// (trainer.py:288-289) — all parameters, by one CTA.
+__device__ void apply_update(const ApplyParams& p) {
+    __shared__ double bc[2];
+    __shared__ int do_sync;
+    if (threadIdx.x == 0) {
+        const int64_t t = p.counters[0] + 1;
+        bc[0] = 1.0 - pow(p.beta1, (double)t);
+        bc[1] = 1.0 - pow(p.beta2, (double)t);
+        const int64_t gs = p.counters[1] + 1;  // step_index = grad_steps + 1
+        do_sync = (gs % p.sync_every) == 0;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < p.nparam; k += blockDim.x) {
+        const double gk = p.grad[k];
+        double w = p.params[k];
+        if (p.adam) {
+            double mk = __dadd_rn(__dmul_rn(p.m[k], p.beta1), __dmul_rn(1.0 - p.beta1, gk));
+            double vk = __dadd_rn(__dmul_rn(p.v[k], p.beta2), __dmul_rn(__dmul_rn(1.0 - p.beta2, gk), gk));
+            p.m[k] = mk;
+            p.v[k] = vk;
+            const double num = __dmul_rn(p.lr, __ddiv_rn(mk, bc[0]));
+            const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, bc[1])), p.eps);
+            w = __dsub_rn(w, __ddiv_rn(num, den));
+        } else {
+            w = __dsub_rn(w, __dmul_rn(p.lr, gk));
+        }
+        p.params[k] = w;
+        if (do_sync) p.target[k] = w;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        p.counters[0] += 1;
+        p.counters[1] += 1;
+        p.counters[2] = 1;
+        *p.last_loss = *p.loss;
+    }
+}
+
+__global__ void learner_apply_kernel(const ApplyParams p) {
+    if (!(p.sampling && p.ring_state[1] < p.min_size)) apply_update(p);
+    if (p.advance && threadIdx.x == 0) p.counters[3] += 1;
+}
+
+// Fused update (be_train_iteration, single GPU): the CTA that finishes its
+// row tile last sums every tile's partials in tile order (the same fixed order
+// as learner_reduce_kernel) and applies the optimizer step — one launch per
+// update: Double-Q targets, Huber backward, reduction, Adam, target sync.
+struct FuseParams {
+    int32_t fused;
+    unsigned* done;  // arrival counter of the CTAs (reset by the last one)
+    double* grad;
+    double* loss;
+    ApplyParams ap;
+};
+
+__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p, const FuseParams f) {
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
     double* xs = lsm;                    // [LROWS][D]
@@ -262,7 +343,12 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     const int row0 = blockIdx.x * LROWS;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    if (p.sampling && p.ring_state[1] < p.min_size) return;  // warm-up: no update
+    if (p.sampling && p.ring_state[1] < p.min_size) {  // warm-up: no update
+        if (f.fused && f.ap.advance && blockIdx.x == 0 && threadIdx.x == 0) f.ap.counters[3] += 1;
+        return;
+    }
+    const uint64_t counter = p.iter_dev ? (uint64_t)(*p.iter_dev) * (uint64_t)p.ups + (uint64_t)p.uidx
+                                        : p.counter;
 
     // ---- gather the batch rows (ReplayBuffer.sample: rng.integers(0, size, B))
     for (int k = threadIdx.x; k < LROWS; k += blockDim.x) {
@@ -270,7 +356,7 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         int64_t src = b < p.B ? b : 0;
         if (p.sampling) {
             const uint64_t size = (uint64_t)p.ring_state[1];
-            P4 rn = philox4x32_10(p.counter, (uint64_t)b, p.seed);
+            P4 rn = philox4x32_10(counter, (uint64_t)b, p.seed);
             const uint64_t r64 = ((uint64_t)rn.x[0] << 32) | rn.x[1];
             src = (int64_t)(((unsigned __int128)r64 * size) >> 64);
             if (p.sample_idx) p.sample_idx[b] = src;
@@ -346,6 +432,26 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, lrow[row]);
         out[nparam] = s;
     }
+    if (!f.fused) return;
+    __threadfence();  // publish this tile's partials
+    __syncthreads();
+    __shared__ int last;
+    if (threadIdx.x == 0) last = atomicAdd(f.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int k = threadIdx.x; k <= nparam; k += blockDim.x) {
+        double s = 0.0;
+        for (int t = 0; t < (int)gridDim.x; ++t) s = __dadd_rn(s, __ldcg(p.partial + (size_t)t * (nparam + 1) + k));
+        if (k < nparam) f.grad[k] = s;
+        else *f.loss = __ddiv_rn(s, (double)p.B);
+    }
+    __syncthreads();
+    apply_update(f.ap);
+    if (threadIdx.x == 0) {
+        *f.done = 0u;
+        if (f.ap.advance) f.ap.counters[3] += 1;
+    }
 }
 
 // Sum the per-tile partials in tile order -> grad[nparam], loss.
@@ -358,64 +464,6 @@ __global__ void learner_reduce_kernel(int n_tiles, int nparam, int B, const doub
         for (int t = 0; t < n_tiles; ++t) s = __dadd_rn(s, partial[(size_t)t * (nparam + 1) + k]);
         if (k < nparam) grad[k] = s;
         else *loss = __ddiv_rn(s, (double)B);
-    }
-}
-
-struct ApplyParams {
-    int32_t nparam;
-    double* params;   // online [nparam] (w1, b1, w2, b2 contiguous)
-    double* target;   // [nparam]
-    double* m;
-    double* v;
-    const double* grad;
-    int64_t* counters;  // [0] adam t, [1] grad steps, [2] updates applied flag
-    double lr, beta1, beta2, eps;
-    int32_t adam;
-    int64_t sync_every;
-    const int64_t* ring_state;
-    int64_t min_size;
-    int32_t sampling;
-    double* loss;        // current loss
-    double* last_loss;   // persisted "last_loss" for logs
-};
-
-// Adam (trainer.py:190-199) or SGD (:202-208), then the target sync
-// (trainer.py:288-289) — one CTA, all parameters.
-__global__ void learner_apply_kernel(const ApplyParams p) {
-    if (p.sampling && p.ring_state[1] < p.min_size) return;
-    __shared__ double bc[2];
-    __shared__ int do_sync;
-    if (threadIdx.x == 0) {
-        const int64_t t = p.counters[0] + 1;
-        bc[0] = 1.0 - pow(p.beta1, (double)t);
-        bc[1] = 1.0 - pow(p.beta2, (double)t);
-        const int64_t gs = p.counters[1] + 1;  // step_index = grad_steps + 1
-        do_sync = (gs % p.sync_every) == 0;
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < p.nparam; k += blockDim.x) {
-        const double gk = p.grad[k];
-        double w = p.params[k];
-        if (p.adam) {
-            double mk = __dadd_rn(__dmul_rn(p.m[k], p.beta1), __dmul_rn(1.0 - p.beta1, gk));
-            double vk = __dadd_rn(__dmul_rn(p.v[k], p.beta2), __dmul_rn(__dmul_rn(1.0 - p.beta2, gk), gk));
-            p.m[k] = mk;
-            p.v[k] = vk;
-            const double num = __dmul_rn(p.lr, __ddiv_rn(mk, bc[0]));
-            const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, bc[1])), p.eps);
-            w = __dsub_rn(w, __ddiv_rn(num, den));
-        } else {
-            w = __dsub_rn(w, __dmul_rn(p.lr, gk));
-        }
-        p.params[k] = w;
-        if (do_sync) p.target[k] = w;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        p.counters[0] += 1;
-        p.counters[1] += 1;
-        p.counters[2] = 1;
-        *p.last_loss = *p.loss;
     }
 }
 
@@ -449,12 +497,18 @@ struct be_learner {
     int64_t* offset;
     int32_t* status;
     double* wl_state;  // [E][3]
+    // be_train_iteration: per-env arrival / task / true rate of the current iteration
+    double* it_arrival;
+    uint8_t* it_task;
+    double* it_rate;
+    unsigned* done;    // fused-update CTA arrival counter
 };
 
 static void learner_free(be_learner* L) {
     void* ptrs[] = {L->params, L->target, L->m, L->v, L->grad, L->partial, L->loss, L->counters,
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
-                    L->preward, L->low, L->count, L->offset, L->status, L->wl_state};
+                    L->preward, L->low, L->count, L->offset, L->status, L->wl_state,
+                    L->it_arrival, L->it_task, L->it_rate, L->done};
     for (void* p : ptrs) cudaFree(p);
     delete L;
 }
@@ -493,7 +547,8 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->ring_state, 64}, {(void**)&L->px, P * E * D * 8}, {(void**)&L->pa, P * E},
         {(void**)&L->pflags, E * P}, {(void**)&L->preward, E * P * 8}, {(void**)&L->low, E * 8},
         {(void**)&L->count, E * 4}, {(void**)&L->offset, E * 8}, {(void**)&L->status, 64},
-        {(void**)&L->wl_state, E * 3 * 8}};
+        {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
+        {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -502,6 +557,8 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         }
         cudaMemset(*a.p, 0, a.n);
     }
+    // configured here, not at launch time: launches may be captured in a CUDA graph
+    cudaFuncSetAttribute(learner_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         learner_free(L);
@@ -576,15 +633,14 @@ int32_t be_learner_workload(be_learner* L, uint64_t seed, int64_t step, double* 
     const int E = c.n_envs;
     train_workload_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
         E, L->wl_state, log(c.rate_low), log(c.rate_high), c.regime_equal_time, c.regime_mean_seconds,
-        c.regime_mean_requests, c.n_tasks, seed, (uint64_t)step, arrival_ms, task, true_rate);
+        c.regime_mean_requests, c.n_tasks, seed, (uint64_t)step, arrival_ms, task, true_rate, nullptr);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "workload launch");
 }
 
-int32_t be_learner_commit(be_learner* L, int64_t step, void* stream) {
-    if (!L || step < 0) return set_error(BE_EINVAL, "bad argument");
-    cudaStream_t st = (cudaStream_t)stream;
+static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cudaStream_t st) {
     CommitParams p{};
+    p.step_dev = step_dev;
     p.E = L->cfg.n_envs;
     p.D = L->D;
     p.P = L->cfg.pending_capacity;
@@ -613,9 +669,18 @@ int32_t be_learner_commit(be_learner* L, int64_t step, void* stream) {
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "commit launch");
 }
 
+int32_t be_learner_commit(be_learner* L, int64_t step, void* stream) {
+    if (!L || step < 0) return set_error(BE_EINVAL, "bad argument");
+    return commit_impl(L, step, nullptr, (cudaStream_t)stream);
+}
+
+static ApplyParams apply_params(be_learner* L, int32_t explicit_batch, int32_t advance);
+
 static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* a, const double* r,
                                  const double* s2, const double* c, int32_t B, uint64_t seed,
-                                 uint64_t counter, int64_t* sample_idx, cudaStream_t st) {
+                                 uint64_t counter, int64_t* sample_idx, cudaStream_t st,
+                                 const int64_t* iter_dev = nullptr, int32_t ups = 1, int32_t uidx = 0,
+                                 int32_t fused = 0, int32_t advance = 0) {
     const be_learner_cfg& cf = L->cfg;
     if (B != cf.batch) return set_error(BE_EINVAL, "batch size differs from the learner config");
     LearnParams p{};
@@ -647,18 +712,25 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     p.huber = cf.huber;
     p.partial = L->partial;
     p.sample_idx = sample_idx;
+    p.iter_dev = iter_dev;
+    p.ups = ups;
+    p.uidx = uidx;
+    FuseParams f{};
+    f.fused = fused;
+    if (fused) {
+        f.done = L->done;
+        f.grad = L->grad;
+        f.loss = L->loss;
+        f.ap = apply_params(L, sampling ? 0 : 1, advance);
+    }
     const size_t smem = sizeof(double) * (2 * LROWS * D + 2 * LROWS * H + 4 * LROWS * M + 3 * LROWS) +
                         sizeof(int) * LROWS;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(learner_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = true;
-    }
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "hidden too large for the learner tile");
-    learner_partial_kernel<<<L->n_tiles, LTHREADS, smem, st>>>(p);
-    learner_reduce_kernel<<<(L->nparam + 256) / 256, 256, 0, st>>>(
-        L->n_tiles, L->nparam, B, L->partial, L->grad, L->loss, L->ring_state, p.min_size,
-        sampling ? 1 : 0);
+    learner_partial_kernel<<<L->n_tiles, LTHREADS, smem, st>>>(p, f);
+    if (!fused)
+        learner_reduce_kernel<<<(L->nparam + 256) / 256, 256, 0, st>>>(
+            L->n_tiles, L->nparam, B, L->partial, L->grad, L->loss, L->ring_state, p.min_size,
+            sampling ? 1 : 0);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner launch");
 }
@@ -679,8 +751,7 @@ int32_t be_learner_backward_batch(be_learner* L, const double* states, const uin
                                  (cudaStream_t)stream);
 }
 
-int32_t be_learner_apply(be_learner* L, int32_t explicit_batch, void* stream) {
-    if (!L) return set_error(BE_EINVAL, "NULL learner");
+static ApplyParams apply_params(be_learner* L, int32_t explicit_batch, int32_t advance) {
     const be_learner_cfg& cf = L->cfg;
     ApplyParams p{};
     p.nparam = L->nparam;
@@ -701,9 +772,72 @@ int32_t be_learner_apply(be_learner* L, int32_t explicit_batch, void* stream) {
     p.sampling = explicit_batch ? 0 : 1;
     p.loss = L->loss;
     p.last_loss = L->loss + 1;
-    learner_apply_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(p);
+    p.advance = advance;
+    return p;
+}
+
+int32_t be_learner_apply(be_learner* L, int32_t explicit_batch, void* stream) {
+    if (!L) return set_error(BE_EINVAL, "NULL learner");
+    learner_apply_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(apply_params(L, explicit_batch, 0));
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "apply launch");
+}
+
+int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* c, void* stream) {
+    if (!L || !env || !c) return set_error(BE_EINVAL, "NULL argument");
+    const be_learner_cfg& cf = L->cfg;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (env->E != cf.n_envs || env->cfg.n_tiers != cf.n_tiers || env->cfg.n_tasks != cf.n_tasks)
+        return set_error(BE_EINVAL, "env and learner shapes differ");
+    if (c->updates_per_step < 0 || c->phase < 0 || c->phase > 2 || c->update_index < 0 ||
+        (c->phase > 0 && c->update_index >= c->updates_per_step))
+        return set_error(BE_EINVAL, "bad phase / update index");
+    if (!(cf.rate_low > 0) || cf.rate_high < cf.rate_low)
+        return set_error(BE_EINVAL, "need 0 < rate_low <= rate_high");
+    const int64_t* it = L->counters + 3;
+    const int E = cf.n_envs, D = L->D, H = cf.hidden, M = cf.n_tiers;
+    int rc;
+    if (c->phase == 0 || (c->phase == 1 && c->update_index == 0)) {
+        // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156)
+        train_workload_kernel<<<(E + 255) / 256, 256, 0, st>>>(
+            E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
+            cf.regime_mean_seconds, cf.regime_mean_requests, cf.n_tasks, c->workload_seed, 0,
+            L->it_arrival, L->it_task, L->it_rate, it);
+        be_qweights W;
+        W.hidden = H;
+        W.w1 = L->params;
+        W.b1 = L->params + D * H;
+        W.w2 = L->params + D * H + H;
+        W.b2 = L->params + D * H + H + H * M;
+        be_records rec{};
+        rec.flags = L->pflags;
+        rec.reward = L->preward;
+        rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                 c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                 cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st);
+        if (rc) return rc;
+        rc = commit_impl(L, 0, it, st);
+        if (rc) return rc;
+    }
+    const int ups = c->updates_per_step;
+    if (c->phase == 0) {
+        for (int u = 0; u < ups; ++u) {
+            rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch,
+                                       c->sample_seed, 0, nullptr, st, it, ups, u, 1, u == ups - 1);
+            if (rc) return rc;
+        }
+        if (ups == 0) {  // no learner: still advance the iteration
+            learner_apply_kernel<<<1, 32, 0, st>>>(apply_params(L, 2, 1));
+        }
+    } else if (c->phase == 1) {
+        rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch,
+                                   c->sample_seed, 0, nullptr, st, it, ups, c->update_index, 0, 0);
+        if (rc) return rc;
+    } else {
+        learner_apply_kernel<<<1, 1024, 0, st>>>(apply_params(L, 0, c->update_index == ups - 1));
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "train iteration launch");
 }
 
 int32_t be_learner_check(be_learner* L, void* stream) {

@@ -74,7 +74,20 @@ struct StepParams {
     int32_t* status;
     int32_t drain;
     const double* skip;  // skip table (global), NULL = skipping off
+    // device-step mode (be_train_iteration): epsilon, Philox counter and the
+    // pending slot of x_out / action_out come from the iteration index *iter_dev
+    const int64_t* iter_dev;
+    double eps_start, eps_end;
+    int64_t eps_decay;
+    int32_t pending_P;
 };
+
+// TrainConfig.epsilon_at (trainer.py:85-90), same IEEE operations as the host
+__device__ __forceinline__ double epsilon_at(int64_t it, double start, double end, int64_t decay) {
+    if (decay <= 0) return end;
+    const double frac = fmin(1.0, __ddiv_rn((double)it, (double)decay));
+    return __dadd_rn(start, __dmul_rn(__dsub_rn(end, start), frac));
+}
 
 template <int M>
 __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
@@ -137,9 +150,16 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
         tier = p.static_tier;
     } else {
         // select_action (policy.py:125-132): explore with probability epsilon
-        if (p.epsilon > 0.0) {
-            P4 rnd = philox4x32_10(p.counter, (uint64_t)e, p.seed);
-            if (u01(rnd.x[0], rnd.x[1]) < p.epsilon) {
+        double epsilon = p.epsilon;
+        uint64_t counter = p.counter;
+        if (p.iter_dev) {
+            const int64_t it = *p.iter_dev;
+            epsilon = epsilon_at(it, p.eps_start, p.eps_end, p.eps_decay);
+            counter = (uint64_t)it;
+        }
+        if (epsilon > 0.0) {
+            P4 rnd = philox4x32_10(counter, (uint64_t)e, p.seed);
+            if (u01(rnd.x[0], rnd.x[1]) < epsilon) {
                 explore = true;
                 tier = (int)below(rnd.x[2], (uint32_t)M);
             }
@@ -156,7 +176,14 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
             }
         }
     }
-    if (p.x_out && lane < D) {
+    double* x_out = p.x_out;
+    uint8_t* action_out = p.action_out;
+    if (p.iter_dev) {  // pending slot it % P of the learner's deferred-reward store
+        const size_t slot = (size_t)(*p.iter_dev % p.pending_P);
+        if (x_out) x_out += slot * (size_t)p.E * D;
+        if (action_out) action_out += slot * (size_t)p.E;
+    }
+    if (x_out && lane < D) {
         // encode (policy.py:52-65): [onehot(task), obs/scale, rate/rate_scale]
         double v = 0.0;
         if (lane < T) v = lane == task ? 1.0 : 0.0;
@@ -164,7 +191,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
         for (int m = 0; m < M; ++m)
             if (lane == T + m) v = xt[m];
         if (lane == T + M) v = xr;
-        p.x_out[(size_t)e * D + lane] = v;
+        x_out[(size_t)e * D + lane] = v;
     }
     unsigned key = (tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)lane) : 0xffffffffu;
     unsigned best = __reduce_min_sync(FULL, key);
@@ -177,7 +204,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     if (al) reps_of(p.state, e, p.R)[lane] = r;
     if (lane == 0) {
         if (p.rate_out) p.rate_out[e] = rate;
-        if (p.action_out) p.action_out[e] = (uint8_t)tier;
+        if (action_out) action_out[e] = (uint8_t)tier;
 #pragma unroll
         for (int k = 0; k < 5; ++k) es->w[k] = est.w[k];
         es->n = est.n;
@@ -270,6 +297,32 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
         p.b2 = W->b2;
     }
     size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, policy ? p.H : 0, policy);
+    return dispatch_step(p, smem, st);
+}
+
+int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
+                        const double* true_rate, const be_qweights* W, uint64_t seed,
+                        const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
+                        int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
+                        double* x_base, cudaStream_t st) {
+    StepParams p = base_params(env, rec_ld, rec);
+    p.arrival = arrival;
+    p.task = task;
+    p.true_rate = true_rate;
+    p.seed = seed;
+    p.action_out = action_base;
+    p.x_out = x_base;
+    p.iter_dev = iter_dev;
+    p.eps_start = eps_start;
+    p.eps_end = eps_end;
+    p.eps_decay = eps_decay;
+    p.pending_P = pending_P;
+    p.H = W->hidden;
+    p.w1 = W->w1;
+    p.b1 = W->b1;
+    p.w2 = W->w2;
+    p.b2 = W->b2;
+    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, p.H, true);
     return dispatch_step(p, smem, st);
 }
 

@@ -167,3 +167,25 @@ def test_learner_matches_reference_golden(cuda, loss, opt):
         assert np.max(np.abs(p_dev - p_ref)) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))
         t_dev = flat(params_of(L.target_net().__dict__))
         assert np.max(np.abs(t_dev - gl["target"][step - 1])) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))
+
+
+def test_training_modes_bit_identical(cuda):
+    """run_training through the host-driven C ABI, the device-resident
+    be_train_iteration (eager) and its CUDA-graph replay give bit-identical
+    networks, replay contents and logs (the graph path is the same algorithm)."""
+    tiers, rw = default_tiers(), RewardSpec.default()
+    cfg = TrainConfig(batch_size=64, buffer_capacity=20_000, warmup=600, total_iterations=250,
+                      log_every=50, seed=5, target_sync_every=7)
+    out = {}
+    for mode in ("host", "device", "graph"):
+        out[mode] = run_training(tiers, rw, cfg, n_envs=33, updates_per_step=2, mode=mode,
+                                 graph_chunk=25)
+    ref = out["host"]
+    assert ref.updates > 100 and ref.transitions > 3000
+    for mode in ("device", "graph"):
+        r = out[mode]
+        assert r.updates == ref.updates and r.transitions == ref.transitions, mode
+        for a, b in zip(r.net.params(), ref.net.params()):
+            assert np.array_equal(a, b), mode
+        assert [(x.step, x.loss, x.mean_recent_reward, x.epsilon) for x in r.log] == \
+               [(x.step, x.loss, x.mean_recent_reward, x.epsilon) for x in ref.log], mode

@@ -6,11 +6,17 @@ from paper_2401_07886_b200 import default_tiers, RewardSpec
 from paper_2401_07886_b200.trainer import TrainConfig, run_training
 E = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 500
+mode = sys.argv[3] if len(sys.argv) > 3 else "graph"
+ups = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 cfg = TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=its,
                   log_every=its, seed=3)
+run_training(default_tiers(), RewardSpec.default(), TrainConfig(batch_size=512, buffer_capacity=1 << 20,
+             warmup=10_000, total_iterations=100, log_every=100, seed=3), n_envs=E, mode=mode,
+             updates_per_step=ups)  # warm (module load, allocator)
+torch.cuda.synchronize()
 t0 = time.time()
-res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=E)
+res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=E, mode=mode, updates_per_step=ups)
 torch.cuda.synchronize()
 dt = time.time() - t0
-print(f"E={E} its={its}: {dt:.2f}s  {its/dt:.1f} it/s  {E*its/dt:.3e} env-steps/s  "
+print(f"mode={mode} E={E} its={its} ups={ups}: {dt:.2f}s  {its/dt:.1f} it/s  {E*its/dt:.3e} env-steps/s  "
       f"updates={res.updates} ({res.updates/dt:.1f}/s) transitions={res.transitions} log={res.log[-1]}")
