@@ -16,6 +16,8 @@
  *   be_qnet_route_f64                select_action / argmax(forward) policy.py:111-132
  *   be_reduce_eval                   windowed + threshold_counts,  evalkit.py:217-241,
  *                                    miss_fractions_by_rate        evalkit.py:61-68
+ *   be_reduce_selection              selection_distribution counts evalkit.py:244-262
+ *   be_windowed                      windowed series               evalkit.py:217-226
  *   be_trace_gen_stable              gen_stable (Philox, on device) workload.py:120-141
  *   be_trace_gen                     gen_stable / gen_unpredictable_* workload.py:94-209
  *   be_learner_*                     train_step / _StepKernel /    trainer.py:211-290
@@ -177,6 +179,17 @@ int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const do
                        int32_t n_buckets, int64_t* win_counts, int64_t* n_windows,
                        int64_t* bucket_miss, int64_t* bucket_req, double* bucket_reward,
                        void* stream);
+
+/* Selection counts for selection_distribution (evalkit.py:244-262): counts
+ * [T][K][M] int64 (ADDED to: zero them first) of requests per (task, rate
+ * bucket of the request's segment = trace->seg_bucket, tier = flags & 0x3f). */
+int32_t be_reduce_selection(const be_trace_soa* trace, const uint8_t* flags, int32_t n_tasks,
+                            int32_t n_tiers, int32_t n_buckets, int64_t* counts, void* stream);
+
+/* windowed (evalkit.py:217-226) per env: out[e][k] = (c[k+w] - c[k]) / w for
+ * k in [0, n_e - w], c the sequential fp64 prefix sum of reward[e][:]. */
+int32_t be_windowed(const be_trace_soa* trace, const double* reward, int32_t window, double* out,
+                    void* stream);
 
 /* On-device gen_stable (workload.py:120-141) with Philox4x32-10 keyed by
  * (seed, env_offset + e): per env one Poisson segment at rate[e] req/s, exponential gaps

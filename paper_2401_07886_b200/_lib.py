@@ -133,6 +133,8 @@ SIGNATURES = {
                                  _P, _P, _P]),
     "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
                               _P, _P, _P]),
+    "be_reduce_selection": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _I32, _I32, _I32, _P, _P]),
+    "be_windowed": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _I32, _P, _P]),
     "be_trace_gen_stable": (_I32, [_I32, _I64, _I64, _I64, _P, _I32, _U64, _P, _P, _P]),
     "be_trace_gen": (_I32, [ctypes.POINTER(BeGenCfg), _I32, _I64, _I64, _U64, _P, _P, _P, _P, _P, _P,
                             _P, _P]),

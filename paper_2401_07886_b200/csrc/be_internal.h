@@ -68,4 +68,7 @@ int launch_tracegen_general(const be_gen_cfg* cfg, int E, int64_t env_offset, in
                             uint64_t seed, double* arrival, uint8_t* task, int64_t* n_events,
                             int64_t* seg_count, int64_t* seg_start, double* seg_rate,
                             int32_t* status, cudaStream_t st);
+int launch_selection(const be_trace_soa* tr, const uint8_t* flags, int T, int M, int K,
+                     int64_t* counts, cudaStream_t st);
+int launch_windowed(const be_trace_soa* tr, const double* reward, int w, double* out, cudaStream_t st);
 }  // namespace be

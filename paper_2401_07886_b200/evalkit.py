@@ -398,3 +398,103 @@ def run_eval_batch(policy, traces: Union[TraceBatch, Sequence], tiers, reward_sp
     K = 1 if buckets is None else len(buckets)
     red = reduce_eval(tb, o.flags, o.reward, thresholds, K)
     return o, red
+
+
+# --------------------------------------------------------------- secondary reducers
+# evalkit.py:212-297.  The per-request work (selection counts, windowed series)
+# runs on the device; the O(K) post-processing mirrors the reference on the host.
+
+def bucket_segments(trace: TraceBatch, rate_buckets: Sequence[float]) -> TraceBatch:
+    """Map every segment to the nearest rate bucket (first minimum, like the
+    np.argmin in selection_distribution, evalkit.py:257) -> trace.seg_bucket."""
+    b = torch.as_tensor(np.asarray(rate_buckets, np.float64), device=trace.device)
+    trace.seg_bucket = torch.argmin((trace.seg_rate[:, None] - b[None, :]).abs(), dim=1).to(torch.int32)
+    return trace
+
+
+def selection_counts(trace: TraceBatch, flags: torch.Tensor, n_tasks: int, n_tiers: int,
+                     n_buckets: int, stream=None) -> torch.Tensor:
+    """int64 [T, K, M] request counts per (task, rate bucket, tier) over all envs
+    (be_reduce_selection; buckets from trace.seg_bucket)."""
+    counts = torch.zeros((n_tasks, n_buckets, n_tiers), dtype=torch.int64, device=trace.device)
+    L = _lib.load()
+    _lib.check(L.be_reduce_selection(trace.soa(), flags.data_ptr(), int(n_tasks), int(n_tiers),
+                                     int(n_buckets), counts.data_ptr(), _lib.stream_ptr(stream)))
+    return counts
+
+
+def selection_distribution(runs, rate_buckets: Sequence[float], n_tasks: int, n_tiers: int,
+                           flags: Optional[torch.Tensor] = None) -> np.ndarray:
+    """evalkit.py:244-262: tier-selection frequency per (task, rate bucket), (T, K, M).
+
+    `runs`: a TraceBatch (with `flags` = RolloutOutputs.flags of its rollout — the
+    counting runs on the device), or a sequence of EvalRun (reference or ours)."""
+    buckets = np.asarray(rate_buckets, dtype=float)
+    if isinstance(runs, TraceBatch):
+        if flags is None:
+            raise ValueError("need the rollout flags for a TraceBatch")
+        bucket_segments(runs, buckets)
+        counts = selection_counts(runs, flags, n_tasks, n_tiers, buckets.size).cpu().numpy().astype(float)
+    else:
+        if not runs:
+            raise ValueError("need at least one run")
+        counts = np.zeros((n_tasks, buckets.size, n_tiers))
+        for run in runs:
+            for r in run.records:
+                k = int(np.argmin(np.abs(buckets - r.segment_rate)))
+                counts[r.task_id, k, r.tier_id] += 1
+    totals = counts.sum(axis=2, keepdims=True)
+    with np.errstate(invalid="ignore"):
+        return np.where(totals > 0, counts / np.maximum(totals, 1), 0.0)
+
+
+def riemann_usage(freq: np.ndarray, rate_buckets: Sequence[float], task_id: int, tier_id: int) -> float:
+    """evalkit.py:265-270: left-endpoint Riemann sum over the sweep."""
+    rates = np.asarray(rate_buckets, dtype=float)
+    return float(np.sum(freq[task_id, :-1, tier_id] * np.diff(rates)))
+
+
+def hardware_utility(run_or_rewards, gpu_count: int):
+    """evalkit.py:273-277: per-request reward / GPUs backing the system."""
+    if gpu_count < 1:
+        raise ValueError("gpu_count must be >= 1")
+    r = run_or_rewards.rewards() if hasattr(run_or_rewards, "rewards") else run_or_rewards
+    return r / gpu_count
+
+
+def trial_band(series):
+    """evalkit.py:280-288: pointwise mean and population std across trials."""
+    if len(series) < 2:
+        raise ValueError("need at least two runs")
+    if isinstance(series, torch.Tensor):
+        return series.mean(dim=0), series.std(dim=0, unbiased=False)
+    if len({len(s) for s in series}) != 1:
+        raise ValueError("runs must have equal length")
+    stack = np.asarray(series, dtype=float)
+    return stack.mean(axis=0), stack.std(axis=0)
+
+
+def collapse_rate(miss_by_rate: dict, rates: Sequence[float], threshold: float = 0.5):
+    """evalkit.py:291-297: lowest swept rate whose miss fraction exceeds threshold."""
+    for rate in rates:
+        if miss_by_rate.get(rate, 0.0) > threshold:
+            return float(rate)
+    return None
+
+
+def running_average(values) -> np.ndarray:
+    """evalkit.py:212-214."""
+    v = np.asarray(values, dtype=float)
+    return np.cumsum(v) / np.arange(1, v.size + 1)
+
+
+def windowed(trace: TraceBatch, reward: torch.Tensor, window: int = WINDOW, stream=None) -> torch.Tensor:
+    """evalkit.py:217-226 for every env on the device: f64 [E, ld]; row e holds its
+    n_e - window + 1 trailing means first (bit-identical to the reference)."""
+    if window < 1:
+        raise ValueError("window must be >= 1")
+    out = torch.full((trace.n_envs, trace.ld), float("nan"), dtype=torch.float64, device=trace.device)
+    L = _lib.load()
+    _lib.check(L.be_windowed(trace.soa(), reward.data_ptr(), int(window), out.data_ptr(),
+                             _lib.stream_ptr(stream)))
+    return out

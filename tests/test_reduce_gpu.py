@@ -1,10 +1,13 @@
 """Evaluation reducer (be_reduce_eval) vs the oracle restatement of
 evalkit.windowed / threshold_counts (evalkit.py:217-241) and the per-rate
 miss fractions (evalkit.py:61-68): counts bit-exact, reward sums to 1e-12."""
+import os
+
 import numpy as np
 import pytest
 import torch
 
+import goldens
 from oracle import oracle
 from paper_2401_07886_b200 import InvalidParameterError, TraceBatch, reduce_eval
 
@@ -70,3 +73,80 @@ def test_reduce_rejects_bad_args(cuda):
         reduce_eval(tb, f, r, thresholds=(1.5,))
     with pytest.raises(InvalidParameterError):
         reduce_eval(tb, f, r, thresholds=(0.9,), window=7)
+
+
+def _evalstats():
+    z = np.load(os.path.join(goldens.GOLDEN, "evalstats.npz"))
+    return {k: z[k] for k in z.files}
+
+
+@pytest.mark.parametrize("name", ["stable_trained", "unpredictable-1_trained", "single-task-0_trained",
+                                  "stable_static1"])
+def test_selection_and_secondary_reducers_match_reference(cuda, name):
+    """selection_distribution / riemann_usage / collapse_rate / hardware_utility /
+    running_average vs the reference's own outputs on the golden records
+    (tests/golden/make_evalstats_golden.py); counting runs on the device."""
+    from paper_2401_07886_b200.evalkit import (STABLE_SWEEP_RATES, collapse_rate, hardware_utility,
+                                               riemann_usage, running_average, selection_distribution)
+    ref = _evalstats()
+    g = goldens.load(name)
+    m = g["meta"]
+    n = len(g["arrival"])
+    tb = TraceBatch.from_arrays(g["arrival"], g["task"], list(g["seg_start"]), list(g["seg_rate"]))
+    flags = torch.as_tensor(g["tier"].astype(np.uint8)[None, :], device=cuda)
+    T, M = len(m["reward"]["tasks"]), len(m["tiers"])
+    freq = selection_distribution(tb, STABLE_SWEEP_RATES, T, M, flags=flags)
+    assert np.array_equal(freq, ref[f"{name}__freq"])
+    rie = np.array([[riemann_usage(freq, STABLE_SWEEP_RATES, t, k) for k in range(M)] for t in range(T)])
+    assert np.array_equal(rie, ref[f"{name}__riemann"])
+    rates = np.empty(n)
+    starts = list(g["seg_start"]) + [n]
+    for k in range(len(g["seg_start"])):
+        rates[starts[k]:starts[k + 1]] = g["seg_rate"][k]
+    dl = np.array([t["deadline"] for t in m["reward"]["tasks"]])
+    miss = {float(r): float(np.mean((g["realized"] > dl[g["task"]])[rates == r])) for r in np.unique(rates)}
+    c = collapse_rate(miss, sorted(miss))
+    want = ref[f"{name}__collapse"]
+    assert (c is None and np.isnan(want)) or c == float(want)
+    assert np.array_equal(hardware_utility(g["reward"], 8), ref[f"{name}__hwutil"])
+    assert np.array_equal(running_average(g["reward"]), ref[f"{name}__running"])
+
+
+def test_windowed_series_and_trial_band_match_reference(cuda):
+    from paper_2401_07886_b200.evalkit import trial_band, windowed
+    ref = _evalstats()
+    gs = [goldens.load(f"unpredictable-1_static{k}") for k in range(3)]
+    tb = TraceBatch.from_arrays(np.stack([g["arrival"] for g in gs]), np.stack([g["task"] for g in gs]),
+                                [list(g["seg_start"]) for g in gs], [list(g["seg_rate"]) for g in gs])
+    rw = torch.as_tensor(np.stack([g["reward"] for g in gs]), device=cuda)
+    w = windowed(tb, rw)
+    n = len(gs[0]["reward"]) - 19
+    for k, g in enumerate(gs):
+        assert np.array_equal(w[k, :n].cpu().numpy(), oracle.windowed(g["reward"]))
+    mean, std = trial_band([w[k, :n].cpu().numpy() for k in range(3)])
+    assert np.array_equal(mean, ref["band_mean"]) and np.array_equal(std, ref["band_std"])
+
+
+def test_selection_counts_many_envs(cuda):
+    """Ragged multi-env batch: device (task, bucket, tier) counts == numpy."""
+    from paper_2401_07886_b200.evalkit import selection_counts
+    rng = np.random.default_rng(4)
+    E, ld, T, M, K = 77, 700, 4, 3, 5
+    n = rng.integers(0, ld + 1, E)
+    task = rng.integers(0, T, (E, ld)).astype(np.uint8)
+    flags = (rng.integers(0, M, (E, ld)) | 0x40 | (rng.integers(0, 2, (E, ld)) << 7)).astype(np.uint8)
+    ss, sr, sb = [], [], []
+    want = np.zeros((T, K, M), np.int64)
+    for e in range(E):
+        cuts = sorted(set([0] + list(rng.integers(1, max(2, n[e]), rng.integers(0, 6)))))
+        ss.append(cuts)
+        sr.append([1.0] * len(cuts))
+        sb.append(list(rng.integers(0, K, len(cuts))))
+        bounds = cuts[1:] + [n[e]]
+        for s0, s1, b in zip(cuts, bounds, sb[-1]):
+            for i in range(s0, min(s1, n[e])):
+                want[task[e, i], b, flags[e, i] & 0x3F] += 1
+    tb = TraceBatch.from_arrays(np.sort(rng.uniform(0, 1e6, (E, ld)), axis=1), task, ss, sr,
+                                n_events=n, seg_bucket=sb)
+    got = selection_counts(tb, torch.as_tensor(flags, device=cuda), T, M, K).cpu().numpy()
+    assert np.array_equal(got, want)
