@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=2401)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ring-capacity", type=int, default=0, help="per-replica FIFO slots (0 = auto)")
+    ap.add_argument("--no-training", action="store_true", help="skip the config-3 training probe")
     return ap.parse_args()
 
 
@@ -161,7 +163,7 @@ def run_reference(a):
         return
     procs = len(os.sched_getaffinity(0))
     per_step = []
-    samples = host_traces(procs * 3, a.requests, a.seed)
+    samples = host_traces(procs * 6, a.requests, a.seed)
     seconds = max(2.0, min(8.0, 150.0 / max(1, a.steps + a.warmup)))
     for i in range(a.warmup + a.steps):
         r = cpu_rollout(samples, seconds, procs)
@@ -182,6 +184,33 @@ def run_reference(a):
 
 
 # ----------------------------------------------------------------- GPU side
+def training_probe(dev, world):
+    """BASELINE configs[2] (config 3): 4096 envs feeding a 1,048,576-transition
+    device replay ring, batch-512 Double-Q/Huber/Adam updates of the 8-256-3
+    Q-MLP (fp64), one update per iteration (= per 4096 env-steps).  Reported
+    beside the headline (not part of `value`); device time of the loop."""
+    from paper_2401_07886_b200 import RewardSpec, default_tiers
+    from paper_2401_07886_b200.trainer import TrainConfig, run_training
+    its = 3000
+    cfg = TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=its,
+                      log_every=its, seed=11)
+    kw = dict(n_envs=4096, updates_per_step=1, device=dev)
+    run_training(default_tiers(), RewardSpec.default(),
+                 TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=50,
+                             log_every=50, seed=11), **kw)  # warm
+    t = {}
+    res = run_training(default_tiers(), RewardSpec.default(), cfg, timing=t, **kw)
+    s = t["loop_ms"] / 1e3
+    return dict(workload="config3: 4096 envs (TrainingWorkload, Philox), replay 1,048,576, batch 512, "
+                         "Q-MLP 8-256-3 fp64, Adam lr 1e-4, Huber, target sync 500, epsilon 1.0->0.05",
+                iterations=its, updates=res.updates, updates_per_step=1,
+                iterations_per_s=its / s, updates_per_s=res.updates / s,
+                env_steps_per_s=4096 * its / s, transitions=res.transitions,
+                final_loss=res.log[-1].loss if res.log else None, n_gpus=world,
+                note="per GPU; device time of the training loop (be_train_iteration, fused update kernel)")
+
+
+
 class ClockSampler:
     def __init__(self, index):
         self.index = index
@@ -256,14 +285,15 @@ def main():
     tb = TraceBatch.generate_stable(load_rates(gids), N, N_TASKS, a.seed, device=dev,
                                     buckets=[g % N_LOADS for g in gids], env_offset=gid0)
     ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False,
-                       device=dev)
+                       device=dev, ring_capacity=a.ring_capacity or None)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         o = ro.launch(tb, net)
         return o, reduce_eval(tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
 
-    for _ in range(a.warmup):
+    ro.run(tb, net)  # settles the ("auto") replica ring capacity; counts as warm-up
+    for _ in range(a.warmup - 1):
         step()
     ro.env.check()
     torch.cuda.synchronize()
@@ -298,7 +328,8 @@ def main():
     # ------------------------------------------------ end to end (host buffers)
     host = pin_trace(tb)
     se = StreamingEvaluator(net, tiers, rw, E, N, enc, estimator_mode="true-rate",
-                            thresholds=THRESHOLDS, n_buckets=N_LOADS, device=dev)
+                            thresholds=THRESHOLDS, n_buckets=N_LOADS, device=dev,
+                            ring_capacity=ro.ring_capacity)
     se.result(se.submit(host))  # warm
     if world > 1:
         dist.barrier()
@@ -326,21 +357,36 @@ def main():
     r_ms = statistics.mean(rollout_ms)
     achieved = ALG_BYTES_STEP * E * N / (r_ms / 1e3) / 1e9
     traffic = None
+    issue = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    clocks = clk.summary()
     if os.path.exists(prof):
         pj = json.load(open(prof))
         k = pj.get("kernels", {}).get("rollout", {})
         if k.get("envs") == E and k.get("requests") == N:
             traffic = k.get("dram_bytes")
+            # the real ceiling of the env step: warp-instruction issue
+            inst = k.get("smsp__inst_executed.sum")
+            if inst and clocks.get("sm_mhz"):
+                sms = torch.cuda.get_device_properties(dev).multi_processor_count
+                per_step = inst / (E * N)
+                ach = per_step * E * N / (r_ms / 1e3)
+                pk = sms * 4 * clocks["sm_mhz"] * 1e6
+                issue = dict(bound="issue", achieved=ach, peak=pk, unit="warp-inst/s", frac=ach / pk,
+                             warp_inst_per_env_step=per_step,
+                             source=f"smsp__inst_executed.sum of {k.get('source', 'ncu')} ({k.get('tag')}) "
+                                    f"x live steps/s; peak = {sms} SMs x 4 schedulers x sampled SM clock")
     red_ms = statistics.mean(reduce_ms)
     red_gbs = ALG_BYTES_REDUCE * E * N / (red_ms / 1e3) / 1e9
+
+    train = None if a.no_training else training_probe(dev, world)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         procs = len(os.sched_getaffinity(0))
         # the same workload bits: device-generated traces of the first envs
-        arr = tb.arrival[: procs * 3].cpu().numpy()
-        tsk = tb.task[: procs * 3].cpu().numpy()
+        arr = tb.arrival[: procs * 24].cpu().numpy()
+        tsk = tb.task[: procs * 24].cpu().numpy()
         samples = [(arr[i], tsk[i], load_rates([i])[0]) for i in range(arr.shape[0])]
         cpu = cpu_rollout(samples, a.cpu_seconds, procs)
 
@@ -366,7 +412,8 @@ def main():
                                   frac=red_gbs / hbm_peak, ms=red_ms,
                                   algorithmic_bytes_per_request=ALG_BYTES_REDUCE),
             kernel_ms=dict(rollout=r_ms, reduce=red_ms),
-            e2e=e2e, cpu_baseline=cpu, clocks=clk.summary(),
+            issue_roofline=issue, training=train,
+            e2e=e2e, cpu_baseline=cpu, clocks=clocks,
             results=dict(load_multipliers=list(range(1, N_LOADS + 1)), **stats))
         print(json.dumps(line), flush=True)
     if world > 1:

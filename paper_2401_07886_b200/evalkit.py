@@ -148,7 +148,14 @@ class GreedyRollout:
     """Reusable fused rollout for trace batches of a fixed shape.
 
     Owns the env handle (replica rings) and the output buffers, so repeated
-    runs allocate nothing.  Every run re-initialises the envs in-kernel."""
+    runs allocate nothing.  Every run re-initialises the envs in-kernel.
+
+    ring_capacity=None ("auto"): the per-replica FIFO rings start small
+    (AUTO_RING_START slots, so the rings of the envs in flight stay resident in
+    L2) and `run` grows them 4x and re-runs when a ring overflows — overflow is
+    always detected on the device; results do not depend on the capacity."""
+
+    AUTO_RING_START = 64
 
     def __init__(self, tiers, reward_spec, n_envs: int, ld: int, encoding=None, *,
                  estimator_mode: str = "estimated", prior_rate: float = 1.0,
@@ -157,12 +164,18 @@ class GreedyRollout:
                  device=None):
         self.device = _lib.require_cuda(device)
         R = sum(int(t.replicas) for t in tiers)
+        self._auto_ring = ring_capacity is None
         if ring_capacity is None:
             free, _ = torch.cuda.mem_get_info(self.device)
-            ring_capacity = default_ring_capacity(ld, n_envs, R, budget_bytes=int(free * 0.35))
-        self.env = EnvBatch(tiers, reward_spec, n_envs, encoding, estimator_mode=estimator_mode,
-                            prior_rate=prior_rate, reset_between_segments=reset_between_segments,
-                            ring_capacity=ring_capacity, skip_ahead=skip_ahead, device=self.device)
+            self._ring_max = default_ring_capacity(ld, n_envs, R, budget_bytes=int(free * 0.35))
+            ring_capacity = min(self._ring_max, self.AUTO_RING_START)
+        else:
+            self._ring_max = int(ring_capacity)
+        self._env_args = (tiers, reward_spec, n_envs, encoding)
+        self._env_kw = dict(estimator_mode=estimator_mode, prior_rate=prior_rate,
+                            reset_between_segments=reset_between_segments, skip_ahead=skip_ahead,
+                            device=self.device)
+        self.env = EnvBatch(*self._env_args, ring_capacity=ring_capacity, **self._env_kw)
         self.n_envs, self.ld, self.M = int(n_envs), int(ld), len(tiers)
         dev = self.device
         self.out = RolloutOutputs(
@@ -172,6 +185,18 @@ class GreedyRollout:
             obs=torch.zeros((n_envs, ld, self.M), dtype=torch.int32, device=dev) if want_steps else None,
             rate=torch.zeros((n_envs, ld), dtype=torch.float64, device=dev) if want_steps else None,
             q=torch.zeros((n_envs, ld, self.M), dtype=torch.float64, device=dev) if want_steps else None)
+
+    @property
+    def ring_capacity(self) -> int:
+        return self.env.ring_capacity
+
+    def _grow_ring(self) -> bool:
+        cap = self.env.ring_capacity
+        if not self._auto_ring or cap >= self._ring_max:
+            return False
+        self.env.close()
+        self.env = EnvBatch(*self._env_args, ring_capacity=min(self._ring_max, cap * 4), **self._env_kw)
+        return True
 
     def launch(self, trace: TraceBatch, policy=None, static_tier: int = -1,
                forced: Optional[torch.Tensor] = None, stream=None) -> RolloutOutputs:
@@ -197,9 +222,15 @@ class GreedyRollout:
 
     def run(self, trace: TraceBatch, policy=None, static_tier: int = -1,
             forced: Optional[torch.Tensor] = None, stream=None) -> RolloutOutputs:
-        o = self.launch(trace, policy, static_tier, forced, stream)
-        self.env.check(stream)  # sync + raise on ring overflow / bad action
-        return o
+        """Synchronous rollout; with an "auto" ring it grows and re-runs on overflow."""
+        while True:
+            o = self.launch(trace, policy, static_tier, forced, stream)
+            try:
+                self.env.check(stream)  # sync + raise on ring overflow / bad action
+                return o
+            except _lib.CapacityError:
+                if not self._grow_ring():
+                    raise
 
 
 def _policy_args(policy, n_tiers):
@@ -301,6 +332,10 @@ class StreamingEvaluator:
         if self.static_tier < 0 and encoding is None:
             encoding = StateEncoding(n_tasks=len(reward_spec.tasks),
                                      batch_scales=tuple(float(t.max_batch) for t in tiers))
+        if ring_capacity is None:  # double-buffered: no re-run on overflow, size for the worst case
+            free, _ = torch.cuda.mem_get_info(self.device)
+            ring_capacity = default_ring_capacity(ld, n_envs, sum(int(t.replicas) for t in tiers),
+                                                  budget_bytes=int(free * 0.35))
         self.ro = GreedyRollout(tiers, reward_spec, n_envs, ld, encoding,
                                 estimator_mode=estimator_mode, ring_capacity=ring_capacity,
                                 want_realized=False, device=self.device)

@@ -242,7 +242,8 @@ class _DevPtr:
 def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=None,
                  completion_log=None, *, n_envs: int = 1, updates_per_step: int = 1,
                  pending_capacity: int = 4096, ring_capacity: int = 1024, device=None,
-                 world=None, mode: str = "device", graph_chunk: int = 0) -> TrainResult:
+                 world=None, mode: str = "device", graph_chunk: int = 0,
+                 timing: Optional[dict] = None) -> TrainResult:
     """trainer.py:333-406 on the GPU for `n_envs` lockstep environments.
 
     Every iteration: TrainingWorkload arrivals (Philox), one env step with
@@ -260,7 +261,9 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     All three give bit-identical results for the same seed.
     `world`: optional torch.distributed group — gradients are all-reduced (mean)
     between backward and the optimizer step (data-parallel learner; "graph" then
-    runs as "device", the collective stays outside the graph)."""
+    runs as "device", the collective stays outside the graph).
+    `timing`: optional dict, receives the device time of the iteration loop
+    ("loop_ms", CUDA events on the launching stream; setup excluded)."""
     n_tasks, n_tiers = len(reward_spec.tasks), len(reward_spec.matrix[0])
     if len(tiers) != n_tiers:
         raise ValueError("tier count must match reward matrix width")
@@ -313,6 +316,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         loss = float(learner.loss[1]) if gs > 0 else math.nan
         log.append(LogRow(it + 1, loss, mean_recent, cfg.epsilon_at(it)))
 
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_begin.record()
     if mode == "host":
         _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
                        log_every, log_row)
@@ -367,8 +372,12 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                 it += 1
             if it % log_every == 0:
                 log_row(it - 1)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_end.record()
     learner.check()
     env.check()
+    if timing is not None:
+        timing["loop_ms"] = t_begin.elapsed_time(t_end)
     res = TrainResult(net=learner.net(), log=log, updates=int(learner.counters[1]),
                       transitions=int(learner.ring_state[2]))
     learner.close()

@@ -12,14 +12,14 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 echo "smoke exit $?" >> gpurun_out/smoke_$tag.log
 timeout 900 python bench.py > gpurun_out/bench_$tag.json 2> gpurun_out/bench_$tag.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$tag.json 2> gpurun_out/bench_ref_$tag.err
-timeout 300 python tools/probe_train.py 4096 2000 > gpurun_out/train_$tag.log 2>&1
+timeout 300 python tools/probe_train.py 4096 3000 device > gpurun_out/train_$tag.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-    --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+    --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-training \
     > gpurun_out/launches_bench_$tag.json 2> gpurun_out/launches_bench_$tag.err
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:rollout_kernel -s 1 -c 1 \
-    -o gpurun_out/prof_rollout_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    -o gpurun_out/prof_rollout_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-training \
     > /dev/null 2> gpurun_out/prof_rollout_$tag.err
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_kernel -s 1 -c 1 \
-    -o gpurun_out/prof_reduce_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+    -o gpurun_out/prof_reduce_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-training \
     > /dev/null 2> gpurun_out/prof_reduce_$tag.err
 ls -la gpurun_out
