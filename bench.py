@@ -267,10 +267,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; ranks beyond the visible GPUs share them (tests on a 1-GPU box)
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # BE_DIST_BACKEND=gloo: several ranks on one GPU (multi-rank path test); NCCL otherwise
+        backend = os.environ.get("BE_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_2401_07886_b200 import (GreedyRollout, RewardSpec, StateEncoding, TraceBatch,
                                        default_tiers, load_checkpoint, reduce_eval)
     from paper_2401_07886_b200.evalkit import StreamingEvaluator, pin_trace

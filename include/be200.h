@@ -282,6 +282,7 @@ typedef struct {
     uint8_t* pending_flags;      /* [E][P]:    be_records.flags with rec_ld = P */
     double* pending_reward;      /* [E][P]:    be_records.reward with rec_ld = P */
     double* workload_state;      /* [E][3] time_ms, rate, requests left in the regime */
+    int64_t* gate;               /* [1] update gate for be_train_iteration(use_gate = 1) */
 } be_learner_views_t;
 
 int32_t be_learner_create(const be_learner_cfg* cfg, int32_t device, be_learner** out);
@@ -319,9 +320,13 @@ int32_t be_learner_check(be_learner* learner, void* stream);
  * / be_learner_backward / be_learner_apply from the host with the same seeds.
  * phase 0: whole iteration; each update is ONE fused kernel (Double-Q targets,
  *          Huber backward, tile reduction and Adam in the last CTA to finish).
- * phase 1: (update_index 0: env part, then) the gradients of update
- *          `update_index` into views.grad — all-reduce them here (DP learner);
- * phase 2: optimizer step of update `update_index`; the last one advances it. */
+ * phase 3: the env part only (workload, env step, commits);
+ * phase 1: the gradients of update `update_index` into views.grad — all-reduce
+ *          them here (DP learner);
+ * phase 2: optimizer step of update `update_index`; the last one advances it.
+ * use_gate = 1 (phases 1/2): the update runs iff *views.gate != 0 instead of the
+ * local "replay holds max(batch, warmup) transitions" test — the DP learner
+ * all-reduces (MIN) that readiness so every rank updates in the same iterations. */
 typedef struct {
     uint64_t workload_seed, policy_seed, sample_seed;
     double epsilon_start, epsilon_end;
@@ -329,7 +334,7 @@ typedef struct {
     int32_t updates_per_step;
     int32_t phase;
     int32_t update_index;
-    int32_t _pad;
+    int32_t use_gate;
 } be_train_iter_cfg;
 
 int32_t be_train_iteration(be_learner* learner, be_env* env, const be_train_iter_cfg* cfg,

@@ -97,7 +97,7 @@ class BeTrainIterCfg(ctypes.Structure):
                 ("sample_seed", ctypes.c_uint64), ("epsilon_start", ctypes.c_double),
                 ("epsilon_end", ctypes.c_double), ("epsilon_decay_steps", ctypes.c_int64),
                 ("updates_per_step", ctypes.c_int32), ("phase", ctypes.c_int32),
-                ("update_index", ctypes.c_int32), ("_pad", ctypes.c_int32)]
+                ("update_index", ctypes.c_int32), ("use_gate", ctypes.c_int32)]
 
 
 class BeLearnerViews(ctypes.Structure):
@@ -109,7 +109,7 @@ class BeLearnerViews(ctypes.Structure):
                 ("ring_cont", ctypes.c_void_p), ("ring_state", ctypes.c_void_p),
                 ("pending_x", ctypes.c_void_p), ("pending_action", ctypes.c_void_p),
                 ("pending_flags", ctypes.c_void_p), ("pending_reward", ctypes.c_void_p),
-                ("workload_state", ctypes.c_void_p)]
+                ("workload_state", ctypes.c_void_p), ("gate", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p

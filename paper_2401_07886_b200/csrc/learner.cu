@@ -213,6 +213,7 @@ struct LearnParams {
     // be_train_iteration: Philox counter = (*iter_dev) * ups + uidx
     const int64_t* iter_dev;
     int32_t ups, uidx;
+    const int64_t* gate;  // non-NULL: update iff *gate != 0 (DP learner, all-reduced readiness)
 };
 
 __device__ __forceinline__ double relu_d(double x) {
@@ -267,6 +268,7 @@ struct ApplyParams {
     double* loss;        // current loss
     double* last_loss;   // persisted "last_loss" for logs
     int32_t advance;     // 1: counters[3] += 1 afterwards (last update of a be_train_iteration)
+    const int64_t* gate; // non-NULL: apply iff *gate != 0
 };
 
 // Adam (trainer.py:190-199) or SGD (:202-208), then the target sync
@@ -309,7 +311,7 @@ __device__ void apply_update(const ApplyParams& p) {
 }
 
 __global__ void learner_apply_kernel(const ApplyParams p) {
-    if (!(p.sampling && p.ring_state[1] < p.min_size)) apply_update(p);
+    if (!(p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size))) apply_update(p);
     if (p.advance && threadIdx.x == 0) p.counters[3] += 1;
 }
 
@@ -343,7 +345,7 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     const int row0 = blockIdx.x * LROWS;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    if (p.sampling && p.ring_state[1] < p.min_size) {  // warm-up: no update
+    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) {  // warm-up: no update
         if (f.fused && f.ap.advance && blockIdx.x == 0 && threadIdx.x == 0) f.ap.counters[3] += 1;
         return;
     }
@@ -457,8 +459,13 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
 // Sum the per-tile partials in tile order -> grad[nparam], loss.
 __global__ void learner_reduce_kernel(int n_tiles, int nparam, int B, const double* partial,
                                       double* grad, double* loss, const int64_t* ring_state,
-                                      int64_t min_size, int sampling) {
-    if (sampling && ring_state[1] < min_size) return;
+                                      int64_t min_size, int sampling, const int64_t* gate) {
+    if (gate ? *gate == 0 : (sampling && ring_state[1] < min_size)) {
+        // no update this iteration: a zero gradient keeps a DP all-reduce well defined
+        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nparam; k += gridDim.x * blockDim.x)
+            grad[k] = 0.0;
+        return;
+    }
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= nparam; k += gridDim.x * blockDim.x) {
         double s = 0.0;
         for (int t = 0; t < n_tiles; ++t) s = __dadd_rn(s, partial[(size_t)t * (nparam + 1) + k]);
@@ -502,13 +509,14 @@ struct be_learner {
     uint8_t* it_task;
     double* it_rate;
     unsigned* done;    // fused-update CTA arrival counter
+    int64_t* gate;     // DP update gate (be_train_iteration use_gate)
 };
 
 static void learner_free(be_learner* L) {
     void* ptrs[] = {L->params, L->target, L->m, L->v, L->grad, L->partial, L->loss, L->counters,
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
                     L->preward, L->low, L->count, L->offset, L->status, L->wl_state,
-                    L->it_arrival, L->it_task, L->it_rate, L->done};
+                    L->it_arrival, L->it_task, L->it_rate, L->done, L->gate};
     for (void* p : ptrs) cudaFree(p);
     delete L;
 }
@@ -548,7 +556,7 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->pflags, E * P}, {(void**)&L->preward, E * P * 8}, {(void**)&L->low, E * 8},
         {(void**)&L->count, E * 4}, {(void**)&L->offset, E * 8}, {(void**)&L->status, 64},
         {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
-        {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}};
+        {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -622,6 +630,7 @@ int32_t be_learner_views(be_learner* L, be_learner_views_t* v) {
     v->pending_flags = L->pflags;
     v->pending_reward = L->preward;
     v->workload_state = L->wl_state;
+    v->gate = L->gate;
     return BE_OK;
 }
 
@@ -680,7 +689,8 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
                                  const double* s2, const double* c, int32_t B, uint64_t seed,
                                  uint64_t counter, int64_t* sample_idx, cudaStream_t st,
                                  const int64_t* iter_dev = nullptr, int32_t ups = 1, int32_t uidx = 0,
-                                 int32_t fused = 0, int32_t advance = 0) {
+                                 int32_t fused = 0, int32_t advance = 0,
+                                 const int64_t* gate = nullptr) {
     const be_learner_cfg& cf = L->cfg;
     if (B != cf.batch) return set_error(BE_EINVAL, "batch size differs from the learner config");
     LearnParams p{};
@@ -715,6 +725,7 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     p.iter_dev = iter_dev;
     p.ups = ups;
     p.uidx = uidx;
+    p.gate = gate;
     FuseParams f{};
     f.fused = fused;
     if (fused) {
@@ -730,7 +741,7 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     if (!fused)
         learner_reduce_kernel<<<(L->nparam + 256) / 256, 256, 0, st>>>(
             L->n_tiles, L->nparam, B, L->partial, L->grad, L->loss, L->ring_state, p.min_size,
-            sampling ? 1 : 0);
+            sampling ? 1 : 0, p.gate);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner launch");
 }
@@ -789,15 +800,16 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
     cudaStream_t st = (cudaStream_t)stream;
     if (env->E != cf.n_envs || env->cfg.n_tiers != cf.n_tiers || env->cfg.n_tasks != cf.n_tasks)
         return set_error(BE_EINVAL, "env and learner shapes differ");
-    if (c->updates_per_step < 0 || c->phase < 0 || c->phase > 2 || c->update_index < 0 ||
-        (c->phase > 0 && c->update_index >= c->updates_per_step))
+    if (c->updates_per_step < 0 || c->phase < 0 || c->phase > 3 || c->update_index < 0 ||
+        ((c->phase == 1 || c->phase == 2) && c->update_index >= c->updates_per_step))
         return set_error(BE_EINVAL, "bad phase / update index");
     if (!(cf.rate_low > 0) || cf.rate_high < cf.rate_low)
         return set_error(BE_EINVAL, "need 0 < rate_low <= rate_high");
     const int64_t* it = L->counters + 3;
     const int E = cf.n_envs, D = L->D, H = cf.hidden, M = cf.n_tiers;
     int rc;
-    if (c->phase == 0 || (c->phase == 1 && c->update_index == 0)) {
+    const int64_t* gate = c->use_gate ? L->gate : nullptr;
+    if (c->phase == 0 || c->phase == 3) {
         // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156)
         train_workload_kernel<<<(E + 255) / 256, 256, 0, st>>>(
             E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
@@ -831,10 +843,13 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         }
     } else if (c->phase == 1) {
         rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch,
-                                   c->sample_seed, 0, nullptr, st, it, ups, c->update_index, 0, 0);
+                                   c->sample_seed, 0, nullptr, st, it, ups, c->update_index, 0, 0,
+                                   gate);
         if (rc) return rc;
-    } else {
-        learner_apply_kernel<<<1, 1024, 0, st>>>(apply_params(L, 0, c->update_index == ups - 1));
+    } else if (c->phase == 2) {
+        ApplyParams ap = apply_params(L, 0, c->update_index == ups - 1);
+        ap.gate = gate;
+        learner_apply_kernel<<<1, 1024, 0, st>>>(ap);
     }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "train iteration launch");

@@ -133,6 +133,7 @@ class DeviceLearner:
         self.params = _wrap(v.params, (self.nparam,), torch.float64, self.device)
         self.grad = _wrap(v.grad, (self.nparam,), torch.float64, self.device)
         self.target = _wrap(v.target.w1, (self.nparam,), torch.float64, self.device)
+        self.gate = _wrap(v.gate, (1,), torch.int64, self.device)
         self.loss = _wrap(v.loss, (2,), torch.float64, self.device)
         self.counters = _wrap(v.counters, (8,), torch.int64, self.device)
         self.ring_state = _wrap(v.ring_state, (8,), torch.int64, self.device)
@@ -260,8 +261,9 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                apply) driven from Python — the reference loop's structure.
     All three give bit-identical results for the same seed.
     `world`: optional torch.distributed group — gradients are all-reduced (mean)
-    between backward and the optimizer step (data-parallel learner; "graph" then
-    runs as "device", the collective stays outside the graph).
+    between backward and the optimizer step (data-parallel learner; always runs
+    as "device": readiness is all-reduced so every rank updates in the same
+    iterations, and the collectives stay outside any graph).
     `timing`: optional dict, receives the device time of the iteration loop
     ("loop_ms", CUDA events on the launching stream; setup excluded)."""
     n_tasks, n_tiers = len(reward_spec.tasks), len(reward_spec.matrix[0])
@@ -286,8 +288,9 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         import torch.distributed as dist
         dist.broadcast(learner.params, 0)
         dist.broadcast(learner.target, 0)
-        if mode == "graph":
-            mode = "device"
+        # the DP update gate (all ranks update in the same iterations) lives in the
+        # device-resident iteration; the collective stays outside any graph
+        mode = "device"
     env = EnvBatch(tiers, reward_spec, E, encoding, estimator_mode=cfg.estimator_mode,
                    prior_rate=cfg.prior_rate, ring_capacity=ring_capacity, device=dev)
     # SeedSequence(seed).spawn(4) -> init, env, policy, sample (trainer.py:351-353); a
@@ -327,6 +330,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         tic.epsilon_start, tic.epsilon_end = float(cfg.epsilon_start), float(cfg.epsilon_end)
         tic.epsilon_decay_steps = int(cfg.epsilon_decay_fraction * total)
         tic.updates_per_step = int(updates_per_step)
+        min_size = max(int(cfg.batch_size), int(cfg.warmup))
+        gate_b = torch.empty(1, dtype=torch.bool, device=dev)
 
         def iteration():
             if world is None:
@@ -335,7 +340,14 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                                                          _lib.stream_ptr()))
                 return
             import torch.distributed as dist
+            tic.phase, tic.update_index, tic.use_gate = 3, 0, 1
+            _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
+                                                     _lib.stream_ptr()))
             for u in range(updates_per_step):
+                # every rank updates in the same iterations: readiness all-reduced (MIN)
+                torch.ge(learner.ring_state[1:2], min_size, out=gate_b)
+                learner.gate.copy_(gate_b)
+                dist.all_reduce(learner.gate, op=dist.ReduceOp.MIN)
                 tic.phase, tic.update_index = 1, u
                 _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
                                                          _lib.stream_ptr()))
@@ -345,7 +357,7 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                 _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
                                                          _lib.stream_ptr()))
             if updates_per_step == 0:
-                tic.phase, tic.update_index = 0, 0
+                tic.phase, tic.update_index, tic.use_gate = 0, 0, 0
                 _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
                                                          _lib.stream_ptr()))
 

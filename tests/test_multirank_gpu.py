@@ -1,0 +1,73 @@
+"""Multi-rank paths on one GPU (the GPU box has one device; NCCL refuses two
+ranks on one GPU, so these use the gloo backend with CUDA tensors — the
+collectives are the same torch.distributed calls the NCCL path makes):
+  * data-parallel learner (run_training(world=...)): gradients all-reduced
+    between backward and Adam -> replicas stay bit-identical, shards differ;
+  * bench.py under torchrun with 2 ranks: env-sharded rollout, max-over-ranks
+    timing, end-of-run statistics all-reduce, one JSON line from rank 0."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _dp_worker(rank, world, port, out):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2401_07886_b200 import RewardSpec, default_tiers
+    from paper_2401_07886_b200.trainer import TrainConfig, run_training
+    cfg = TrainConfig(batch_size=64, buffer_capacity=20_000, warmup=500, total_iterations=120,
+                      log_every=60, seed=4)
+    res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=16, updates_per_step=1,
+                       world=dist.group.WORLD)
+    out[rank] = ([p.copy() for p in res.net.params()], res.updates, res.transitions,
+                 [(r.loss, r.mean_recent_reward) for r in res.log])
+    dist.destroy_process_group()
+
+
+def test_data_parallel_learner_replicas_identical(cuda):
+    world, port = 2, _port()
+    out = mp.Manager().dict()
+    mp.spawn(_dp_worker, args=(world, port, out), nprocs=world, join=True)
+    (p0, u0, t0, l0), (p1, u1, t1, l1) = out[0], out[1]
+    assert u0 == u1 > 0
+    for a, b in zip(p0, p1):  # one all-reduced gradient per update: identical replicas
+        assert np.array_equal(a, b)
+    assert len(l0) == len(l1) == 2
+    assert t0 != t1 or l0 != l1  # the env shards (and their batches) are independent
+
+
+def test_bench_two_ranks_one_gpu(cuda, tmp_path):
+    env = dict(os.environ, BE_DIST_BACKEND="gloo", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--envs", "2048", "--requests", "2000",
+           "--no-cpu-baseline", "--no-training"]
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["total_envs"] == 4096
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
+    assert sum(d["results"]["requests"]) == 4096 * 2000
