@@ -303,6 +303,7 @@ def main():
     for _ in range(a.warmup - 1):
         step()
     ro.env.check()
+    ro.env.screen_stats(reset=True)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
@@ -324,6 +325,7 @@ def main():
     if world > 1:
         dist.barrier()
     ro.env.check()
+    n_screened, n_fallback = ro.env.screen_stats(reset=True)
     ms = t_start.elapsed_time(t_end)
     rollout_ms = [e[0].elapsed_time(e[1]) for e in ev]
     reduce_ms = [e[1].elapsed_time(e[2]) for e in ev]
@@ -420,6 +422,10 @@ def main():
                                   algorithmic_bytes_per_request=ALG_BYTES_REDUCE),
             kernel_ms=dict(rollout=r_ms, reduce=red_ms),
             issue_roofline=issue, training=train,
+            q_screen=dict(decisions=n_screened, fp64_fallbacks=n_fallback,
+                          fallback_frac=n_fallback / max(n_screened, 1),
+                          note="certified fp32 decision screen (FFMA2) with exact fp64 fallback; "
+                               "decisions identical to the fp64 path (DESIGN.md §4.1)"),
             e2e=e2e, cpu_baseline=cpu, clocks=clocks,
             results=dict(load_multipliers=list(range(1, N_LOADS + 1)), **stats))
         print(json.dumps(line), flush=True)

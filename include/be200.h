@@ -85,6 +85,10 @@ typedef struct {
     double prior_rate;               /* RateEstimator.prior_rate */
     int32_t ring_capacity;           /* per-replica FIFO slots (power of two) */
     int32_t skip_ahead;              /* 1 = exact closed-form iteration skipping (default) */
+    int32_t q_screen;                /* 1 = greedy rollout decides with a certified fp32 screen and
+                                        falls back to fp64 where it cannot certify (default;
+                                        decisions identical); 0 = fp64 for every decision */
+    int32_t _pad2;
 } be_cfg;
 
 /* Trace batch: WorkloadTrace (workload.py:39-91) for E envs, SoA, env-major. */
@@ -135,6 +139,10 @@ size_t be_env_device_bytes(const be_env* env);
 int32_t be_env_reset(be_env* env, const uint8_t* mask, void* stream);
 /* Sync `stream` and report latched device errors (ring overflow, ...). */
 int32_t be_env_check(be_env* env, void* stream);
+/* Counters of the certified fp32 decision screen of be_rollout_greedy, summed
+ * over all rollouts since the last reset: out[0] = screened decisions,
+ * out[1] = decisions that fell back to fp64.  Synchronises the device. */
+int32_t be_env_screen_stats(be_env* env, int64_t* out, int32_t reset);
 
 /* One env step for all E envs (evalkit.py:193-205 / trainer.py:375-395):
  * advance every replica to arrival_ms[e], score completions into `rec`

@@ -47,7 +47,8 @@ class BeCfg(ctypes.Structure):
                 ("batch_scales", ctypes.c_double * MAX_TIERS), ("rate_scale", ctypes.c_double),
                 ("estimator_true_rate", ctypes.c_int32), ("reset_between_segments", ctypes.c_int32),
                 ("prior_rate", ctypes.c_double), ("ring_capacity", ctypes.c_int32),
-                ("skip_ahead", ctypes.c_int32)]
+                ("skip_ahead", ctypes.c_int32), ("q_screen", ctypes.c_int32),
+                ("_pad2", ctypes.c_int32)]
 
 
 class BeTraceSoa(ctypes.Structure):
@@ -124,6 +125,7 @@ SIGNATURES = {
     "be_env_device_bytes": (_SZ, [_P]),
     "be_env_reset": (_I32, [_P, _P, _P]),
     "be_env_check": (_I32, [_P, _P]),
+    "be_env_screen_stats": (_I32, [_P, _P, _I32]),
     "be_env_step": (_I32, [_P, _P, _P, _P, _P, ctypes.POINTER(BeQWeights), _I32, _D, _U64, _U64,
                            _I64, ctypes.POINTER(BeRecords), _P, _P, _P, _P, _P, _P]),
     "be_env_drain": (_I32, [_P, _I64, ctypes.POINTER(BeRecords), _P]),

@@ -165,11 +165,13 @@ int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env*
     if ((e = cudaMalloc(&env->rings, env->ring_bytes)) != cudaSuccess ||
         (e = cudaMalloc(&env->reps, state)) != cudaSuccess ||
         (e = cudaMalloc((void**)&env->d_counter, 64)) != cudaSuccess ||
-        (e = cudaMalloc((void**)&env->d_status, 64)) != cudaSuccess) {
+        (e = cudaMalloc((void**)&env->d_status, 64)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&env->d_screen, 16)) != cudaSuccess) {
         be_env_destroy(env);
         return set_cuda_error(e, "be_env_create: cudaMalloc");
     }
     cudaMemset(env->d_status, 0, 64);
+    cudaMemset(env->d_screen, 0, 16);
     env->envs = nullptr;
     if (cfg->skip_ahead) {
         env->skip_rows = build_skip_table(*cfg, nullptr);
@@ -205,6 +207,7 @@ int32_t be_env_destroy(be_env* env) {
     cudaFree(env->d_counter);
     cudaFree(env->d_status);
     cudaFree(env->d_skip);
+    cudaFree(env->d_screen);
     delete env;
     return BE_OK;
 }
@@ -241,6 +244,19 @@ int32_t be_env_check(be_env* env, void* stream) {
     else
         snprintf(msg, sizeof(msg), "env %d: device error %d", st[1], st[0]);
     return set_error(st[0], msg);
+}
+
+int32_t be_env_screen_stats(be_env* env, int64_t* out, int32_t reset) {
+    if (!env || !out) return set_error(BE_EINVAL, "NULL argument");
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return set_cuda_error(e, "be_env_screen_stats: sync");
+    unsigned long long h[2];
+    e = cudaMemcpy(h, env->d_screen, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return set_cuda_error(e, "be_env_screen_stats: copy");
+    out[0] = (int64_t)h[0];
+    out[1] = (int64_t)h[1];
+    if (reset) cudaMemset(env->d_screen, 0, sizeof(h));
+    return BE_OK;
 }
 
 int32_t be_rollout_greedy(be_env* env, const be_trace_soa* trace, const be_qweights* W,

@@ -415,6 +415,194 @@ __device__ __forceinline__ void qnet_group(const double* __restrict__ sw, int T,
     for (int m = 0; m < M; ++m) q[m] = __dadd_rn(a[m], sb2[m]);
 }
 
+// ---------------------------------------------------------------------------
+// Certified fp32 screening of the greedy decision (fused rollout fast path).
+//
+// The decision only needs the argmax of q = relu(x W1 + b1) W2 + b2.  The
+// screen evaluates q in fp32 with packed FFMA2 (two hidden units per
+// instruction, half the shared-memory bytes of the fp64 path) together with
+// a rigorous bound |q32_m - q_m| <= B_m on its error against exact
+// arithmetic on the fp64 inputs; if the fp32 leader beats every other action
+// by more than the sum of the two bounds, it IS the exact argmax (unique, so
+// the first-max tie rule cannot matter) and the fp64 evaluation is skipped.
+// Otherwise (about 1% of trained-policy states: near-ties, huge rate inputs,
+// non-finite values) the caller falls back to qnet_group in fp64, so every
+// decision equals the fp64 path's.  Q values are never taken from the screen
+// (runs that record q use the fp64 path throughout).
+//
+// Error bound (u = 2^-24, gamma_n = n u / (1 - n u)).  Per hidden unit j the
+// layer-1 value is four chained FMAs on operands each rounded once to fp32:
+// |pre32_j - pre_j| <= (gamma_4 + 2u + O(u^2)) P_j <= 7u P_j with
+// P_j = |W1[t][j] + b1[j]| + sum_i |x_i| |W1[T+i][j]|; relu is 1-Lipschitz
+// and |h32_j| <= (1 + 7u) P_j.  Every layer-2 term passes through
+// L = H/(2 LPE) chained FFMA2 + 1 pair add + log2(LPE) butterfly adds + 1 bias
+// add roundings, with W2 rounded once: |q32_m - q_m| <= ((L + 1)(1 + 8u) + 7) u
+// S_m, S_m = sum_j |W2[j][m]| P_j + |b2[m]|.  The kernel uses K = (L + 16) u
+// (slack >= 8u also covers the fp32 evaluation of S_m itself, whose terms are
+// all non-negative and rounded upward) and stores the tables K * S split as
+// A[t][m] (task row + bias) and C[i][m] (per input i), so
+// B_m = A[t][m] + sum_i |x_i| C[i][m].  The comparison runs in fp64.
+template <int M>
+struct QsLayout {
+    static constexpr int NV = 2 * M + 1;  // per-hidden-unit values besides the task row
+    static constexpr int NQ4 = NV / 2;    // float4 arrays (two values x two units)
+    // floats: task rows [T][H] + values [NV][H] + A [T][M] + C [M+1][M] + b2 [M]
+    __host__ __device__ static size_t floats(int T, int H) {
+        return (size_t)(T + NV) * H + (size_t)T * M + (size_t)(M + 1) * M + M;
+    }
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+    float2 d;
+    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+        : "=f"(d.x), "=f"(d.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return d;
+}
+
+// Lane g of a group owns hidden-unit pairs (j0, j1) = (g + 2p LPE, g + 2p LPE + LPE),
+// stored at pair index P = p LPE + g so that a group's loads are consecutive.
+template <int LPE>
+__device__ __forceinline__ int screen_unit(int P, int half) {
+    const int p = P / LPE, g = P % LPE;
+    return g + 2 * p * LPE + half * LPE;
+}
+
+// All threads of the CTA; the caller synchronises before use.  Requires
+// H % (2 LPE) == 0.
+template <int M, int LPE>
+__device__ __forceinline__ void stage_qscreen(const double* __restrict__ w1, const double* __restrict__ b1,
+                                              const double* __restrict__ w2, const double* __restrict__ b2,
+                                              int T, int H, float* sf) {
+    constexpr int NV = QsLayout<M>::NV, NQ4 = QsLayout<M>::NQ4;
+    const int H2 = H / 2;
+    auto val = [&](int v, int j) -> double {  // v < M: tier inputs, v == M: rate, v > M: W2[j][v-M-1]
+        return v <= M ? w1[(size_t)(T + v) * H + j] : w2[(size_t)j * M + (v - M - 1)];
+    };
+    float2* tr2 = reinterpret_cast<float2*>(sf);
+    for (int k = threadIdx.x; k < T * H2; k += blockDim.x) {
+        const int t = k / H2, P = k % H2;
+        const int j0 = screen_unit<LPE>(P, 0), j1 = screen_unit<LPE>(P, 1);
+        tr2[k] = make_float2(__double2float_rn(__dadd_rn(w1[(size_t)t * H + j0], b1[j0])),
+                             __double2float_rn(__dadd_rn(w1[(size_t)t * H + j1], b1[j1])));
+    }
+    float4* q4 = reinterpret_cast<float4*>(sf + (size_t)T * H);
+    for (int k = threadIdx.x; k < NQ4 * H2; k += blockDim.x) {
+        const int q = k / H2, P = k % H2;
+        const int j0 = screen_unit<LPE>(P, 0), j1 = screen_unit<LPE>(P, 1);
+        q4[k] = make_float4(__double2float_rn(val(2 * q, j0)), __double2float_rn(val(2 * q, j1)),
+                            __double2float_rn(val(2 * q + 1, j0)), __double2float_rn(val(2 * q + 1, j1)));
+    }
+    float2* o2 = reinterpret_cast<float2*>(sf + (size_t)T * H + (size_t)2 * NQ4 * H);
+    for (int P = threadIdx.x; P < H2; P += blockDim.x)
+        o2[P] = make_float2(__double2float_rn(val(NV - 1, screen_unit<LPE>(P, 0))),
+                            __double2float_rn(val(NV - 1, screen_unit<LPE>(P, 1))));
+    // bound tables: one warp per sum, fp64 accumulation, rounded up to fp32
+    float* bA = sf + (size_t)(T + NV) * H;
+    float* bC = bA + T * M;
+    float* b2f = bC + (M + 1) * M;
+    int lg = 0;
+    while ((1 << lg) < LPE) ++lg;
+    const double K = (double)(H / (2 * LPE) + 2 + lg + 16) * 0x1p-24;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int s = warp; s < (T + M + 1) * M; s += nw) {
+        const int r = s / M, m = s % M;  // r < T: task row; else input T + (r - T)
+        double acc = 0.0;
+        for (int j = lane; j < H; j += 32) {
+            const double a = r < T ? fabs(__dadd_rn(w1[(size_t)r * H + j], b1[j])) : fabs(w1[(size_t)r * H + j]);
+            acc = __fma_rn(fabs(w2[(size_t)j * M + m]), a, acc);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(FULL, acc, off));
+        if (lane == 0) {
+            if (r < T) bA[r * M + m] = __double2float_ru(__dmul_ru(K, __dadd_ru(acc, fabs(b2[m]))));
+            else bC[(r - T) * M + m] = __double2float_ru(__dmul_ru(K, acc));
+        }
+    }
+    for (int m = threadIdx.x; m < M; m += blockDim.x) b2f[m] = __double2float_rn(b2[m]);
+}
+
+// Returns true if `tier` is certified to be the exact greedy decision; the
+// result is identical on every lane of the group.
+template <int M, int LPE>
+__device__ __forceinline__ bool qnet_screen(const float* __restrict__ sf, int T, int H, int task,
+                                            const double (&xt)[M], double xr, int& tier) {
+    constexpr int NV = QsLayout<M>::NV, NQ4 = QsLayout<M>::NQ4;
+    const int g = threadIdx.x & (LPE - 1);
+    const int H2 = H / 2;
+    const float2* tr2 = reinterpret_cast<const float2*>(sf) + (size_t)task * H2;
+    const float4* q4 = reinterpret_cast<const float4*>(sf + (size_t)T * H);
+    const float2* o2 = reinterpret_cast<const float2*>(sf + (size_t)T * H + (size_t)2 * NQ4 * H);
+    const float* bA = sf + (size_t)(T + NV) * H;
+    const float* bC = bA + T * M;
+    const float* b2f = bC + (M + 1) * M;
+    float x32[M + 1];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x32[m] = __double2float_rn(xt[m]);
+    x32[M] = __double2float_rn(xr);
+    float2 a[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) a[m] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int P = g; P < H2; P += LPE) {
+        float2 v[NV];
+#pragma unroll
+        for (int q = 0; q < NQ4; ++q) {
+            const float4 w = q4[(size_t)q * H2 + P];
+            v[2 * q] = make_float2(w.x, w.y);
+            v[2 * q + 1] = make_float2(w.z, w.w);
+        }
+        v[NV - 1] = o2[P];
+        float2 pre = tr2[P];
+#pragma unroll
+        for (int m = 0; m <= M; ++m) pre = ffma2(make_float2(x32[m], x32[m]), v[m], pre);
+        const float2 h = make_float2(fmaxf(pre.x, 0.f), fmaxf(pre.y, 0.f));
+#pragma unroll
+        for (int m = 0; m < M; ++m) a[m] = ffma2(h, v[M + 1 + m], a[m]);
+    }
+    float q[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) q[m] = __fadd_rn(a[m].x, a[m].y);
+#pragma unroll
+    for (int off = LPE / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) q[m] = __fadd_rn(q[m], __shfl_xor_sync(FULL, q[m], off));
+    }
+    int best = 0;
+    bool fin = true;
+    float bv = 0.f;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        q[m] = __fadd_rn(q[m], b2f[m]);
+        fin = fin && isfinite(q[m]);
+        if (m == 0 || q[m] > bv) {
+            best = m;
+            bv = q[m];
+        }
+    }
+    float B[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        float b = bA[task * M + m];
+#pragma unroll
+        for (int i = 0; i <= M; ++i) b = __fmaf_ru(fabsf(x32[i]), bC[i * M + m], b);
+        B[m] = b;
+        fin = fin && isfinite(b);
+    }
+    float bb = B[0];
+#pragma unroll
+    for (int m = 1; m < M; ++m) bb = m == best ? B[m] : bb;
+    const double lo = __dsub_rd((double)bv, (double)bb);
+    bool sure = fin;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+        if (m != best) sure = sure && lo > __dadd_ru((double)q[m], (double)B[m]);
+    tier = best;
+    return sure;
+}
+
 // np.argmax semantics: first NaN if any, else first maximum.
 template <int M>
 __device__ __forceinline__ int argmax_first(const double (&q)[M]) {

@@ -26,6 +26,7 @@ struct be_env {
     int32_t* d_status;  // [0] code, [1] env
     double* d_skip;     // skip table [sum_m (max_batch_m + 1)][SKIP_NB], NULL = skipping off
     int32_t skip_rows;
+    unsigned long long* d_screen;  // [2] screened decisions, fp64 fallbacks (rollout)
 };
 
 namespace be {
@@ -42,7 +43,7 @@ int build_skip_table(const be_cfg& c, double* out /* [rows][SKIP_NB] or NULL */)
 int set_cuda_error(cudaError_t e, const char* where);
 int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
                    const uint8_t* forced, const be_records* rec, cudaStream_t st);
-size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows = 0);
+size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows = 0, bool screen = false);
 int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st);
 int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
                     const double* true_rate, const uint8_t* forced, const be_qweights* W,

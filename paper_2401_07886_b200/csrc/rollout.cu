@@ -46,6 +46,8 @@ struct RolloutParams {
     const double* skip;  // skip table (global), NULL = skipping off
     int32_t skip_rows;
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
+    int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
+    unsigned long long* screen_stats;  // [2] decisions screened, fp64 fallbacks (nullable)
 };
 
 __device__ __forceinline__ void raise_status(int32_t* status, int code, int env) {
@@ -70,7 +72,7 @@ __device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
 }
 
 template <int M, int LPE>
-__global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
+__global__ void __launch_bounds__(256, 2) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
@@ -79,13 +81,20 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     const int H = p.H;
     if (policy) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
+    // fp32 screen tables after the fp64 weights (16-byte aligned)
+    const bool screen = policy && p.screen;
+    float* sf = reinterpret_cast<float*>(
+        sw + ((policy ? QLayout<M>::doubles(T, H) : 0) + 1 & ~size_t(1)));
+    if (screen) stage_qscreen<M, LPE>(p.w1, p.b1, p.w2, p.b2, T, H, sf);
     const double* skip_tab = p.skip;
     if (p.skip && p.skip_smem) {  // after the weights (policy) or right after Score
-        double* st = sw + (policy ? QLayout<M>::doubles(T, H) : 0);
+        double* st = screen ? reinterpret_cast<double*>(sf + ((QsLayout<M>::floats(T, H) + 3) & ~size_t(3)))
+                            : sw + (policy ? QLayout<M>::doubles(T, H) : 0);
         for (int k = threadIdx.x; k < p.skip_rows * SKIP_NB; k += blockDim.x) st[k] = p.skip[k];
         skip_tab = st;
     }
     __syncthreads();
+    unsigned n_screened = 0, n_fallback = 0;  // per group leader (screen_stats)
 
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPE - 1);       // lane within the env group
@@ -195,8 +204,21 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
 #pragma unroll
             for (int m = 0; m < M; ++m) xt[m] = __dmul_rn((double)obs[m], inv_scale[m]);
             const double xr = __dmul_rn(rate, inv_rate_scale);
-            qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
-            tier = argmax_first<M>(q);
+            if (screen) {
+                // certified fp32 decision; exact fp64 evaluation only where it cannot certify
+                const bool sure = qnet_screen<M, LPE>(sf, T, H, task, xt, xr, tier);
+                if (__ballot_sync(FULL, live && !sure)) {
+                    qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
+                    if (!sure) tier = argmax_first<M>(q);
+                }
+                if (live && gl == 0) {
+                    ++n_screened;
+                    n_fallback += sure ? 0u : 1u;
+                }
+            } else {
+                qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
+                tier = argmax_first<M>(q);
+            }
             if (live && p.rec.q && gl < M) {
 #pragma unroll
                 for (int m = 0; m < M; ++m)
@@ -233,11 +255,20 @@ __global__ void __launch_bounds__(256) rollout_kernel(const RolloutParams p) {
             need = true;
         }
     }
+    if (p.screen_stats && screen) {
+        const unsigned a = __reduce_add_sync(FULL, n_screened), b = __reduce_add_sync(FULL, n_fallback);
+        if (lane == 0) {
+            atomicAdd(&p.screen_stats[0], (unsigned long long)a);
+            atomicAdd(&p.screen_stats[1], (unsigned long long)b);
+        }
+    }
 }
 
-size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows) {
+size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool screen) {
     size_t s = (sizeof(Score) + 15) & ~size_t(15);
-    if (policy) s += sizeof(double) * ((size_t)(T + 2 * M + 1) * H + M);  // QLayout<M>::doubles
+    if (policy) s += sizeof(double) * (((size_t)(T + 2 * M + 1) * H + M + 1) & ~size_t(1));  // QLayout<M>::doubles
+    if (policy && screen)  // QsLayout<M>::floats, rounded to 16 bytes
+        s += sizeof(float) * (((size_t)(T + 2 * M + 1) * H + (size_t)T * M + (size_t)(M + 1) * M + M + 3) & ~size_t(3));
     s += sizeof(double) * (size_t)skip_rows * SKIP_NB;
     return s;
 }
@@ -301,11 +332,17 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
         p.w2 = W->w2;
         p.b2 = W->b2;
     }
+    // the screen needs H % (2 LPE) == 0 (LPE = 16 for <= 16 replicas, else 32); runs that
+    // record Q values use the fp64 path throughout
+    const int lpe = (env->R <= 16 && (!policy || p.H % 32 == 0)) ? 16 : 32;
+    p.screen = policy && env->cfg.q_screen && !rec->q && p.H % (2 * lpe) == 0 &&
+               rollout_smem_bytes(T, M, p.H, true, 0, true) <= 200 * 1024;
+    p.screen_stats = p.screen ? env->d_screen : nullptr;
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
     // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
-    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows) <= 100 * 1024;
-    size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0);
+    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <= 100 * 1024;
+    size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0, p.screen);
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
     switch (M) {

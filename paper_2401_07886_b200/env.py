@@ -28,7 +28,7 @@ def _get(o, name, default=None):
 
 def make_cfg(tiers: Sequence, reward_spec, encoding=None, *, estimator_mode: str = "estimated",
              prior_rate: float = 1.0, reset_between_segments: bool = False,
-             ring_capacity: int = 1024, skip_ahead: bool = True) -> _lib.BeCfg:
+             ring_capacity: int = 1024, skip_ahead: bool = True, q_screen: bool = True) -> _lib.BeCfg:
     """Pack ModelTierSpec / RewardSpec / StateEncoding / RateEstimator settings."""
     if estimator_mode not in ("estimated", "true-rate"):
         raise _lib.InvalidParameterError("mode must be one of ('estimated', 'true-rate')")
@@ -75,6 +75,7 @@ def make_cfg(tiers: Sequence, reward_spec, encoding=None, *, estimator_mode: str
     c.prior_rate = float(prior_rate)
     c.ring_capacity = int(ring_capacity)
     c.skip_ahead = 1 if skip_ahead else 0
+    c.q_screen = 1 if q_screen else 0
     return c
 
 
@@ -95,7 +96,7 @@ class EnvBatch:
     def __init__(self, tiers, reward_spec, n_envs: int, encoding=None, *,
                  estimator_mode: str = "estimated", prior_rate: float = 1.0,
                  reset_between_segments: bool = False, ring_capacity: int = 1024,
-                 skip_ahead: bool = True, device=None):
+                 skip_ahead: bool = True, q_screen: bool = True, device=None):
         self.device = _lib.require_cuda(device)
         self.tiers = list(tiers)
         self.reward_spec = reward_spec
@@ -105,7 +106,7 @@ class EnvBatch:
         self.n_tasks = reward_spec.n_tasks if hasattr(reward_spec, "n_tasks") else len(reward_spec.tasks)
         self.cfg = make_cfg(tiers, reward_spec, encoding, estimator_mode=estimator_mode,
                             prior_rate=prior_rate, reset_between_segments=reset_between_segments,
-                            ring_capacity=ring_capacity, skip_ahead=skip_ahead)
+                            ring_capacity=ring_capacity, skip_ahead=skip_ahead, q_screen=q_screen)
         self.ring_capacity = int(ring_capacity)
         self._L = _lib.load()
         h = ctypes.c_void_p()
@@ -134,6 +135,13 @@ class EnvBatch:
 
     def check(self, stream=None) -> None:
         _lib.check(self._L.be_env_check(self._h, _lib.stream_ptr(stream)))
+
+    def screen_stats(self, reset: bool = False) -> tuple:
+        """(screened decisions, fp64 fallbacks) of the greedy rollout's certified
+        fp32 decision screen since the last reset (synchronises the device)."""
+        out = (ctypes.c_int64 * 2)()
+        _lib.check(self._L.be_env_screen_stats(self._h, out, 1 if reset else 0))
+        return int(out[0]), int(out[1])
 
     def reset(self, mask: Optional[torch.Tensor] = None, stream=None) -> None:
         _lib.check(self._L.be_env_reset(self._h, _lib.ptr(mask), _lib.stream_ptr(stream)))

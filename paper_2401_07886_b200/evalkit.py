@@ -161,7 +161,7 @@ class GreedyRollout:
                  estimator_mode: str = "estimated", prior_rate: float = 1.0,
                  reset_between_segments: bool = False, ring_capacity: Optional[int] = None,
                  skip_ahead: bool = True, want_realized: bool = True, want_steps: bool = False,
-                 device=None):
+                 q_screen: bool = True, device=None):
         self.device = _lib.require_cuda(device)
         R = sum(int(t.replicas) for t in tiers)
         self._auto_ring = ring_capacity is None
@@ -174,7 +174,7 @@ class GreedyRollout:
         self._env_args = (tiers, reward_spec, n_envs, encoding)
         self._env_kw = dict(estimator_mode=estimator_mode, prior_rate=prior_rate,
                             reset_between_segments=reset_between_segments, skip_ahead=skip_ahead,
-                            device=self.device)
+                            q_screen=q_screen, device=self.device)
         self.env = EnvBatch(*self._env_args, ring_capacity=ring_capacity, **self._env_kw)
         self.n_envs, self.ld, self.M = int(n_envs), int(ld), len(tiers)
         dev = self.device

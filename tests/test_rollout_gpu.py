@@ -196,3 +196,82 @@ def test_skip_table_random_tiers_match_oracle(cuda, seed):
         for k in ("reward", "realized", "obs"):
             got = getattr(o, k)[e, :n].cpu().numpy()
             assert np.array_equal(got, ref[k]), f"env {e} {k} first diff {first_diff(got.ravel(), ref[k].ravel())}"
+
+
+# ---------------------------------------------------------------------------
+# Certified fp32 decision screen (be_env.cuh qnet_screen): runs that do not
+# record Q values decide with the screen and fall back to fp64 where it cannot
+# certify; every decision must still equal the reference's.
+POLICY_NAMES = [n for n in NAMES if goldens.load(n)["meta"]["static_tier"] < 0]
+
+
+@pytest.mark.parametrize("name", POLICY_NAMES)
+def test_screened_rollout_matches_reference(cuda, name):
+    g = goldens.load(name)
+    m = g["meta"]
+    arr, tsk = g["arrival"][None], g["task"][None]
+    tb = TraceBatch.from_arrays(arr, tsk, [list(g["seg_start"])], [list(g["seg_rate"])])
+    ro = GreedyRollout(tiers_of(m), reward_of(m), 1, tb.ld, enc_of(m),
+                       estimator_mode=m["estimator_mode"], reset_between_segments=m["reset"],
+                       want_steps=False)
+    ro.env.screen_stats(reset=True)
+    o = ro.run(tb, QNetwork.from_any(goldens.net_for(m)))
+    assert_env_equal(o, 0, g)
+    screened, fallback = ro.env.screen_stats()
+    assert screened == len(g["arrival"])
+    assert 0 <= fallback <= screened
+
+
+def test_screen_equals_fp64_on_large_batch(cuda):
+    """Screen on vs off over many envs of device-generated traces (bench-like
+    workload, trained policy): identical flags and rewards bit for bit."""
+    from paper_2401_07886_b200 import RewardSpec, StateEncoding, default_tiers, load_checkpoint
+    import os
+    E, N = 1024, 4000
+    tiers, rw = default_tiers(), RewardSpec.default()
+    enc = StateEncoding(4, tuple(float(t.max_batch) for t in tiers))
+    net = load_checkpoint(os.path.join(goldens.GOLDEN, "trained_seed7.beqn"))
+    rates = [3.0 * (1 + (e % 10)) for e in range(E)]
+    tb = TraceBatch.generate_stable(rates, N, 4, 11, device=cuda)
+    outs = []
+    for screen in (True, False):
+        ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False,
+                           q_screen=screen)
+        ro.env.screen_stats(reset=True)
+        o = ro.run(tb, net)
+        outs.append((o.flags.clone(), o.reward.clone(), ro.env.screen_stats()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    screened, fallback = outs[0][2]
+    assert screened == E * N and fallback < 0.1 * screened
+    assert outs[1][2] == (0, 0)
+
+
+def test_screen_falls_back_on_exact_ties(cuda):
+    """Two actions with identical Q everywhere: the screen can never certify,
+    so every decision comes from the fp64 path (first maximum, np.argmax)."""
+    g = goldens.load("unpredictable-1_mixed1")
+    m = g["meta"]
+    net = {k: v.copy() for k, v in goldens.net_for(m).items()}
+    net["w2"][:, 2] = net["w2"][:, 1]
+    net["b2"][2] = net["b2"][1]
+    net["b2"][1:] += 50.0  # tiers 1/2 dominate tier 0
+    tb = TraceBatch.from_arrays(g["arrival"][None], g["task"][None], [list(g["seg_start"])],
+                                [list(g["seg_rate"])])
+    res = []
+    for screen in (True, False):
+        ro = GreedyRollout(tiers_of(m), reward_of(m), 1, tb.ld, enc_of(m),
+                           estimator_mode=m["estimator_mode"], reset_between_segments=m["reset"],
+                           want_steps=False, q_screen=screen)
+        ro.env.screen_stats(reset=True)
+        o = ro.run(tb, QNetwork.from_any(net))
+        res.append((o.tier[0].cpu().numpy(), ro.env.screen_stats()))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert not np.any(res[0][0] == 2)  # first maximum wins the tie
+    n = len(g["arrival"])
+    assert res[0][1] == (n, n)
+    ref = oracle.run_eval_oracle(tiers=m["tiers"], reward=m["reward"], arrival=g["arrival"], task=g["task"],
+                                 seg_start=g["seg_start"], seg_rate=g["seg_rate"], net=net,
+                                 batch_scales=m["enc"]["batch_scales"],
+                                 estimator_mode=m["estimator_mode"], reset=m["reset"])
+    assert np.array_equal(res[0][0], ref["tier"])
