@@ -166,7 +166,8 @@ int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env*
         (e = cudaMalloc(&env->reps, state)) != cudaSuccess ||
         (e = cudaMalloc((void**)&env->d_counter, 64)) != cudaSuccess ||
         (e = cudaMalloc((void**)&env->d_status, 64)) != cudaSuccess ||
-        (e = cudaMalloc((void**)&env->d_screen, 16)) != cudaSuccess) {
+        (e = cudaMalloc((void**)&env->d_screen, 16)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&env->d_qpack, QPACK_MAX_DOUBLES * sizeof(double))) != cudaSuccess) {
         be_env_destroy(env);
         return set_cuda_error(e, "be_env_create: cudaMalloc");
     }
@@ -208,6 +209,7 @@ int32_t be_env_destroy(be_env* env) {
     cudaFree(env->d_status);
     cudaFree(env->d_skip);
     cudaFree(env->d_screen);
+    cudaFree(env->d_qpack);
     delete env;
     return BE_OK;
 }

@@ -10,6 +10,8 @@
 // [0, max_batch], binade e in [SKIP_ELO, SKIP_ELO + SKIP_NB)), doubles.
 constexpr int SKIP_NB = 32;
 constexpr int SKIP_ELO = -2;
+// largest packed fp64 Q-weight block (QLayout: (T + 2M + 1) H + M doubles)
+constexpr size_t QPACK_MAX_DOUBLES = (size_t)(BE_MAX_TASKS + 2 * BE_MAX_TIERS + 1) * 1024 + BE_MAX_TIERS;
 
 struct be_env {
     be_cfg cfg;
@@ -27,6 +29,7 @@ struct be_env {
     double* d_skip;     // skip table [sum_m (max_batch_m + 1)][SKIP_NB], NULL = skipping off
     int32_t skip_rows;
     unsigned long long* d_screen;  // [2] screened decisions, fp64 fallbacks (rollout)
+    double* d_qpack;    // packed fp64 Q weights for the screened rollout's fallback (max size)
 };
 
 namespace be {

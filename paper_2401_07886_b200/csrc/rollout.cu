@@ -17,6 +17,10 @@
 #include "be_env.cuh"
 #include "be_internal.h"
 
+#ifndef BE_ROLLOUT_MINB
+#define BE_ROLLOUT_MINB 2  // resident CTAs per SM the register allocation is capped for
+#endif
+
 namespace be {
 
 struct RolloutParams {
@@ -48,7 +52,16 @@ struct RolloutParams {
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
     unsigned long long* screen_stats;  // [2] decisions screened, fp64 fallbacks (nullable)
+    const double* qpack;  // screen on: the fp64 fallback's packed weights (QLayout) in global
+                          // memory (L1/L2-resident), so shared memory holds only the screen
 };
+
+// Packs the fp64 weights once per launch for the screened rollout's fallback.
+template <int M>
+__global__ void __launch_bounds__(256) stage_qpack_kernel(const double* w1, const double* b1, const double* w2,
+                                                          const double* b2, int T, int H, double* out) {
+    stage_qnet<M>(w1, b1, w2, b2, T, H, out);
+}
 
 __device__ __forceinline__ void raise_status(int32_t* status, int code, int env) {
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
@@ -72,7 +85,7 @@ __device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
 }
 
 template <int M, int LPE>
-__global__ void __launch_bounds__(256, 2) rollout_kernel(const RolloutParams p) {
+__global__ void __launch_bounds__(256, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
@@ -80,11 +93,12 @@ __global__ void __launch_bounds__(256, 2) rollout_kernel(const RolloutParams p) 
     const bool policy = p.forced == nullptr && p.static_tier < 0;
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     const int H = p.H;
-    if (policy) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
-    // fp32 screen tables after the fp64 weights (16-byte aligned)
+    // screen on: [Score | fp32 screen tables | skip table], fp64 weights in global (qpack);
+    // screen off: [Score | fp64 weights | skip table]
     const bool screen = policy && p.screen;
-    float* sf = reinterpret_cast<float*>(
-        sw + ((policy ? QLayout<M>::doubles(T, H) : 0) + 1 & ~size_t(1)));
+    if (policy && !screen) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
+    const double* qw = screen ? p.qpack : sw;
+    float* sf = reinterpret_cast<float*>(sw);
     if (screen) stage_qscreen<M, LPE>(p.w1, p.b1, p.w2, p.b2, T, H, sf);
     const double* skip_tab = p.skip;
     if (p.skip && p.skip_smem) {  // after the weights (policy) or right after Score
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(256, 2) rollout_kernel(const RolloutParams p) 
                 // certified fp32 decision; exact fp64 evaluation only where it cannot certify
                 const bool sure = qnet_screen<M, LPE>(sf, T, H, task, xt, xr, tier);
                 if (__ballot_sync(FULL, live && !sure)) {
-                    qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
+                    qnet_group<M, LPE>(qw, T, H, task, xt, xr, q);
                     if (!sure) tier = argmax_first<M>(q);
                 }
                 if (live && gl == 0) {
@@ -266,9 +280,9 @@ __global__ void __launch_bounds__(256, 2) rollout_kernel(const RolloutParams p) 
 
 size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool screen) {
     size_t s = (sizeof(Score) + 15) & ~size_t(15);
-    if (policy) s += sizeof(double) * (((size_t)(T + 2 * M + 1) * H + M + 1) & ~size_t(1));  // QLayout<M>::doubles
+    if (policy && !screen) s += sizeof(double) * ((size_t)(T + 2 * M + 1) * H + M);  // QLayout<M>::doubles
     if (policy && screen)  // QsLayout<M>::floats, rounded to 16 bytes
-        s += sizeof(float) * (((size_t)(T + 2 * M + 1) * H + (size_t)T * M + (size_t)(M + 1) * M + M + 3) & ~size_t(3));
+        s += sizeof(float) * (((size_t)(T + 2 * M + 1) * H + T + (M + 1) + M + 3) & ~size_t(3));
     s += sizeof(double) * (size_t)skip_rows * SKIP_NB;
     return s;
 }
@@ -298,6 +312,12 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
 
 template <int M>
 static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
+    if (p.screen) {
+        stage_qpack_kernel<M><<<1, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
+                                                 const_cast<double*>(p.qpack));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
+    }
     if (p.R <= 16 && (p.H == 0 || p.H % 32 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms);
     return launch_rollout_m<M, 32>(p, smem, st, sms);
 }
@@ -338,6 +358,7 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     p.screen = policy && env->cfg.q_screen && !rec->q && p.H % (2 * lpe) == 0 &&
                rollout_smem_bytes(T, M, p.H, true, 0, true) <= 200 * 1024;
     p.screen_stats = p.screen ? env->d_screen : nullptr;
+    p.qpack = env->d_qpack;
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
     // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
