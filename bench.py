@@ -194,7 +194,7 @@ def training_probe(dev, world):
     its = 3000
     cfg = TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=its,
                       log_every=its, seed=11)
-    kw = dict(n_envs=4096, updates_per_step=1, device=dev)
+    kw = dict(n_envs=4096, updates_per_step=1, device=dev, mode="graph" if world == 1 else "device")
     run_training(default_tiers(), RewardSpec.default(),
                  TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=50,
                              log_every=50, seed=11), **kw)  # warm
@@ -207,7 +207,9 @@ def training_probe(dev, world):
                 iterations_per_s=its / s, updates_per_s=res.updates / s,
                 env_steps_per_s=4096 * its / s, transitions=res.transitions,
                 final_loss=res.log[-1].loss if res.log else None, n_gpus=world,
-                note="per GPU; device time of the training loop (be_train_iteration, fused update kernel)")
+                mode=kw["mode"],
+                note="per GPU; device time of the training loop (be_train_iteration: workload, env step, "
+                     "single-pass commit, 128-tile learner + multi-CTA reduce/Adam; CUDA graph replay)")
 
 
 

@@ -357,14 +357,15 @@ struct QLayout {
     __host__ __device__ static size_t doubles(int T, int H) { return (size_t)(T + NV) * H + M; }
 };
 
+// (tid, nt): this thread's index among the nt threads that share the staging.
 template <int M>
 __device__ __forceinline__ void stage_qnet(const double* __restrict__ w1, const double* __restrict__ b1,
                                            const double* __restrict__ w2, const double* __restrict__ b2,
-                                           int T, int H, double* sw) {
+                                           int T, int H, double* sw, int tid, int nt) {
     constexpr int NV = QLayout<M>::NV, NP = QLayout<M>::NP;
-    for (int k = threadIdx.x; k < T * H; k += blockDim.x) sw[k] = __dadd_rn(w1[k], b1[k % H]);
+    for (int k = tid; k < T * H; k += nt) sw[k] = __dadd_rn(w1[k], b1[k % H]);
     double* pairs = sw + (size_t)T * H;
-    for (int k = threadIdx.x; k < NV * H; k += blockDim.x) {
+    for (int k = tid; k < NV * H; k += nt) {
         const int v = k / H, j = k % H;
         // v < M: tier inputs, v == M: rate input (W1 rows T..T+M); v > M: W2[j][v-M-1]
         const double x = v <= M ? w1[(size_t)(T + v) * H + j] : w2[(size_t)j * M + (v - M - 1)];
@@ -372,8 +373,24 @@ __device__ __forceinline__ void stage_qnet(const double* __restrict__ w1, const 
         else pairs[(size_t)2 * NP * H + j] = x;
     }
     double* sb2 = sw + (size_t)(T + NV) * H;
-    for (int k = threadIdx.x; k < M; k += blockDim.x) sb2[k] = b2[k];
+    for (int k = tid; k < M; k += nt) sb2[k] = b2[k];
 }
+
+template <int M>
+__device__ __forceinline__ void stage_qnet(const double* __restrict__ w1, const double* __restrict__ b1,
+                                           const double* __restrict__ w2, const double* __restrict__ b2,
+                                           int T, int H, double* sw) {
+    stage_qnet<M>(w1, b1, w2, b2, T, H, sw, threadIdx.x, blockDim.x);
+}
+
+// The packed fp64 layout in global memory (the screened rollout's fallback and
+// the step kernel read it through L1), grid-stride.
+template <int M>
+__global__ void __launch_bounds__(256) stage_qpack_kernel(const double* w1, const double* b1, const double* w2,
+                                                          const double* b2, int T, int H, double* out) {
+    stage_qnet<M>(w1, b1, w2, b2, T, H, out, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+constexpr int QPACK_CTAS = 16;
 
 template <int M, int LPE>
 __device__ __forceinline__ void qnet_group(const double* __restrict__ sw, int T, int H, int task,

@@ -5,7 +5,7 @@
 //   ReplayBuffer ring / sample       trainer.py:101-163   -> ring [C] + Philox sampling
 //   _StepKernel.compute              trainer.py:211-267   -> learner_partial_kernel (+ reduce)
 //   td_targets_double_q              trainer.py:166-174
-//   Adam / SGD, target sync          trainer.py:177-208, :276-290 -> learner_apply_kernel
+//   Adam / SGD, target sync          trainer.py:177-208, :276-290 -> learner_update_kernel
 //
 // All learner arithmetic is fp64 (an fp32 learner misses 1e-5 on
 // gradients by cancellation over the batch).  Gradients are reduced over row
@@ -26,7 +26,8 @@
 
 namespace be {
 
-constexpr int LROWS = 32;      // rows per learner CTA
+constexpr int LROWS = 4;       // rows per learner CTA (B = 512 -> 128 CTAs: latency, not work, bounds an update)
+constexpr int UTHREADS = 256;  // learner_update_kernel: 32 parameters x 8 tile slices per CTA
 constexpr int LTHREADS = 256;  // one thread per hidden unit (looping for H > 256)
 
 // --------------------------------------------------------------- workload
@@ -70,8 +71,6 @@ struct CommitParams {
     uint8_t* pflags;         // [E][P] completion flags (bit 6 = reward known)
     const double* preward;   // [E][P]
     int64_t* low;            // [E] oldest uncommitted request id
-    int32_t* count;          // [E] commits this step
-    const int64_t* offset;   // [E] exclusive scan of count (pass 2)
     int64_t* ring_state;     // [0] cursor, [1] size, [2] total commits
     int64_t capacity;
     double* rs;              // ring states [C][D]
@@ -81,47 +80,63 @@ struct CommitParams {
     double* rc;              // ring continue flags [C]
     int32_t* status;
     const int64_t* step_dev;  // be_train_iteration: `step` read from device memory
+    // single-pass commit (commit_fused_kernel): decoupled look-back scan state
+    unsigned long long* scan;  // [E / 8] (epoch << 40 | flag << 38 | value)
+    unsigned* ticket;          // [0] virtual CTA ticket, [1] epoch (both advanced by the last CTA)
 };
 
 // A transition j is ready when its reward is known and j <= step - 1 (its next
-// state x_{j+1} exists).  Pass 1 counts per env, pass 2 writes in id order.
-template <bool WRITE>
-__global__ void commit_kernel(const CommitParams p) {
-    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (e >= p.E) return;
-    int64_t lo = p.low[e];
+// state x_{j+1} exists).
+// The whole commit step in one launch (32 envs per CTA, one warp each): count the
+// ready transitions, exclusive scan of the counts in env-id order across CTAs by
+// decoupled look-back (virtual CTA ids from a ticket, so every predecessor has
+// started; scan entries are tagged with a per-launch epoch instead of being
+// cleared), write the transitions, and the last CTA advances the ring cursor.
+// Slots follow env-id order, then request-id order within an env (never an atomic cursor).
+constexpr int CENVS = 32;  // envs (warps) per commit CTA
+constexpr unsigned FULL_MASK = 0xffffffffu;
+
+__device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane, int64_t base, int64_t cursor,
+                                          bool write) {
     const int64_t step = p.step_dev ? *p.step_dev : p.step;
     const int64_t hi = step - 1;  // inclusive upper candidate
-    int64_t base = WRITE ? p.offset[e] : 0;
+    const int64_t lo = p.low[e];
     int total = 0;
     int64_t new_low = lo;
-    bool blocked = false;  // first not-ready id seen: low cannot pass it
+    bool blocked = false;
+    // pending slot of j0 (= j0 mod P) and ring slot of this env's first commit, kept
+    // incrementally: no 64-bit division inside the loop
+    int64_t r0 = lo % p.P;
+    const int64_t s0 = write ? (cursor + base) % p.capacity : 0;
     for (int64_t j0 = lo; j0 <= hi; j0 += 32) {
         const int64_t j = j0 + lane;
+        int64_t sj = r0 + lane;
+        while (sj >= p.P) sj -= p.P;
         bool ready = false, pend = false;
         if (j <= hi) {
-            // 0 = in flight (cleared at submit), 0x40|tier|miss = completed, 0x20 = committed
-            const uint8_t f = p.pflags[(int64_t)e * p.P + (j % p.P)];
+            const uint8_t f = p.pflags[(int64_t)e * p.P + sj];
             ready = (f & 0x40) != 0;
             pend = (f & 0x60) == 0;
         }
         const unsigned rb = __ballot_sync(0xffffffffu, ready);
         const unsigned pb = __ballot_sync(0xffffffffu, pend);
-        if (WRITE && ready) {
+        if (write && ready) {
             const int rank = __popc(rb & ((1u << lane) - 1u));
-            const int64_t slot = (p.ring_state[0] + base + total + rank) % p.capacity;
-            const int64_t sj = (j % p.P), sj1 = ((j + 1) % p.P);
+            int64_t slot = s0 + total + rank;
+            while (slot >= p.capacity) slot -= p.capacity;
+            const int64_t sj1 = sj + 1 == p.P ? 0 : sj + 1;
             for (int d = 0; d < p.D; ++d) {
                 p.rs[slot * p.D + d] = p.px[(sj * p.E + e) * p.D + d];
                 p.rs2[slot * p.D + d] = p.px[(sj1 * p.E + e) * p.D + d];
             }
             p.ra[slot] = p.pa[sj * p.E + e];
             p.rr[slot] = p.preward[(int64_t)e * p.P + sj];
-            p.rc[slot] = 1.0;  // no episode boundaries in training
-            p.pflags[(int64_t)e * p.P + sj] = 0x20;  // committed (cleared again at the next submit)
+            p.rc[slot] = 1.0;
+            p.pflags[(int64_t)e * p.P + sj] = 0x20;
         }
         total += __popc(rb);
+        r0 += 32;
+        while (r0 >= p.P) r0 -= p.P;
         if (!blocked) {
             if (pb) {
                 new_low = j0 + __ffs(pb) - 1;
@@ -131,58 +146,85 @@ __global__ void commit_kernel(const CommitParams p) {
             }
         }
     }
-    if (lane == 0) {
-        if (!WRITE) {
-            p.count[e] = total;
+    if (write && lane == 0) {
+        p.low[e] = new_low;
+        if (step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
+    }
+    return total;
+}
+
+__global__ void __launch_bounds__(CENVS * 32) commit_fused_kernel(const CommitParams p) {
+    __shared__ int vb_sh, cnt[CENVS];
+    __shared__ long long wpre[CENVS];
+    __shared__ long long excl_sh, cursor_sh;
+    __shared__ unsigned epoch_sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        // read the cursor and epoch before taking a ticket: the last CTA changes them
+        cursor_sh = __ldcg(p.ring_state);
+        epoch_sh = __ldcg(p.ticket + 1) & 0xffffffu;
+        __threadfence();
+        vb_sh = (int)atomicAdd(p.ticket, 1u);
+    }
+    __syncthreads();
+    const int vb = vb_sh, nb = (p.E + CENVS - 1) / CENVS;
+    const int e = vb * CENVS + warp;
+    const unsigned long long ep = (unsigned long long)epoch_sh << 40;
+    int c = 0;
+    if (e < p.E) c = commit_env(p, e, lane, 0, 0, false);
+    if (lane == 0) cnt[warp] = c;
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive prefix of the counts over this CTA's warps (inclusive scan - own)
+        const long long own = lane < CENVS ? cnt[lane] : 0;
+        long long inc = own;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long v = __shfl_up_sync(FULL_MASK, inc, off);
+            if (lane >= off) inc += v;
+        }
+        if (lane < CENVS) wpre[lane] = inc - own;
+        const long long agg = __shfl_sync(FULL_MASK, inc, 31);
+        long long excl = 0;
+        if (vb == 0) {
+            if (lane == 0) atomicExch(&p.scan[0], ep | (2ull << 38) | (unsigned long long)agg);
         } else {
-            p.low[e] = new_low;
-            // the pending ring must hold every uncommitted request
-            if (step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0)
-                p.status[1] = e;
+            if (lane == 0) atomicExch(&p.scan[vb], ep | (1ull << 38) | (unsigned long long)agg);
+            // warp-wide look-back over windows of 32 predecessors (nearest first)
+            for (int j = vb - 1;; j -= 32) {
+                const int idx = j - lane;
+                unsigned long long v = 2ull << 38;  // before the first CTA: prefix 0
+                if (idx >= 0) {
+                    do {
+                        v = atomicAdd(&p.scan[idx], 0ull);
+                    } while ((v >> 40) != (ep >> 40) || ((v >> 38) & 3ull) == 0);
+                }
+                const unsigned pb = __ballot_sync(FULL_MASK, ((v >> 38) & 3ull) == 2ull);
+                const int stop = pb ? __ffs(pb) - 1 : 31;  // lanes 0..stop contribute
+                long long val = lane <= stop ? (long long)(v & ((1ull << 38) - 1)) : 0;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(FULL_MASK, val, off);
+                excl += val;
+                if (pb) break;
+            }
+            if (lane == 0) atomicExch(&p.scan[vb], ep | (2ull << 38) | (unsigned long long)(excl + agg));
         }
-    }
-}
-
-// single-CTA exclusive scan of the per-env commit counts (env-id order)
-__global__ void commit_scan_kernel(int E, const int32_t* count, int64_t* offset, int64_t* ring_state,
-                                   int64_t capacity) {
-    __shared__ int64_t part[1024];
-    const int t = threadIdx.x;
-    const int per = (E + blockDim.x - 1) / blockDim.x;
-    int64_t s = 0;
-    for (int k = 0; k < per; ++k) {
-        const int e = t * per + k;
-        if (e < E) s += count[e];
-    }
-    part[t] = s;
-    __syncthreads();
-    if (t == 0) {
-        int64_t acc = 0;
-        for (int k = 0; k < (int)blockDim.x; ++k) {
-            const int64_t v = part[k];
-            part[k] = acc;
-            acc += v;
-        }
-        part[blockDim.x] = acc;  // blockDim <= 1023
-    }
-    __syncthreads();
-    int64_t acc = part[t];
-    for (int k = 0; k < per; ++k) {
-        const int e = t * per + k;
-        if (e < E) {
-            offset[e] = acc;
-            acc += count[e];
+        if (lane == 0) {
+            excl_sh = excl;
+            if (vb == nb - 1) {  // commits this step: advance the ring
+                const long long n = excl + agg;
+                p.ring_state[3] = n;
+                p.ring_state[0] = (cursor_sh + n) % p.capacity;
+                p.ring_state[1] = p.ring_state[1] + n < p.capacity ? p.ring_state[1] + n : p.capacity;
+                p.ring_state[2] += n;
+                p.ticket[1] = p.ticket[1] + 1u;
+                __threadfence();
+                p.ticket[0] = 0u;
+            }
         }
     }
     __syncthreads();
-    if (t == 0) ring_state[3] = part[blockDim.x];  // commits this step (applied after pass 2)
-}
-
-__global__ void commit_finish_kernel(int64_t* ring_state, int64_t capacity) {
-    const int64_t n = ring_state[3];
-    ring_state[0] = (ring_state[0] + n) % capacity;
-    ring_state[1] = ring_state[1] + n < capacity ? ring_state[1] + n : capacity;
-    ring_state[2] += n;
+    if (e < p.E) commit_env(p, e, lane, excl_sh + wpre[warp], cursor_sh, true);
 }
 
 // --------------------------------------------------------------- learner
@@ -223,16 +265,22 @@ __device__ __forceinline__ double relu_d(double x) {
 
 // Forward of LROWS rows through (W1,b1,W2,b2) into h (smem [LROWS][H]) and q
 // (smem [LROWS][M]); block-wide, fixed reduction order.
+// DM: compile-time upper bound of D (register-resident weight column).
+template <int DM>
 __device__ void forward_rows(const double* x, int D, int H, int M, const double* w1,
                              const double* b1, const double* w2, const double* b2, double* h,
-                             double* q, double* red) {
+                             double* q) {
     for (int j = threadIdx.x; j < H; j += blockDim.x) {
         const double bj = b1[j];
-        double wcol[32];
-        for (int d = 0; d < D; ++d) wcol[d] = w1[d * H + j];
+        double wcol[DM];
+#pragma unroll
+        for (int d = 0; d < DM; ++d) wcol[d] = d < D ? w1[d * H + j] : 0.0;
+#pragma unroll
         for (int row = 0; row < LROWS; ++row) {
             double acc = 0.0;
-            for (int d = 0; d < D; ++d) acc = __fma_rn(x[row * D + d], wcol[d], acc);
+#pragma unroll
+            for (int d = 0; d < DM; ++d)
+                if (d < D) acc = __fma_rn(x[row * D + d], wcol[d], acc);
             h[row * H + j] = relu_d(__dadd_rn(acc, bj));
         }
     }
@@ -248,7 +296,6 @@ __device__ void forward_rows(const double* x, int D, int H, int M, const double*
         if (lane == 0) q[pair] = __dadd_rn(acc, b2[m]);
     }
     __syncthreads();
-    (void)red;
 }
 
 struct ApplyParams {
@@ -257,7 +304,7 @@ struct ApplyParams {
     double* target;   // [nparam]
     double* m;
     double* v;
-    const double* grad;
+    double* grad;
     int64_t* counters;  // [0] adam t, [1] grad steps, [2] updates applied flag, [3] iteration
     double lr, beta1, beta2, eps;
     int32_t adam;
@@ -272,62 +319,124 @@ struct ApplyParams {
 };
 
 // Adam (trainer.py:190-199) or SGD (:202-208), then the target sync
-// (trainer.py:288-289) — all parameters, by one CTA.
-__device__ void apply_update(const ApplyParams& p) {
-    __shared__ double bc[2];
-    __shared__ int do_sync;
-    if (threadIdx.x == 0) {
-        const int64_t t = p.counters[0] + 1;
-        bc[0] = 1.0 - pow(p.beta1, (double)t);
-        bc[1] = 1.0 - pow(p.beta2, (double)t);
-        const int64_t gs = p.counters[1] + 1;  // step_index = grad_steps + 1
-        do_sync = (gs % p.sync_every) == 0;
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < p.nparam; k += blockDim.x) {
-        const double gk = p.grad[k];
-        double w = p.params[k];
-        if (p.adam) {
-            double mk = __dadd_rn(__dmul_rn(p.m[k], p.beta1), __dmul_rn(1.0 - p.beta1, gk));
-            double vk = __dadd_rn(__dmul_rn(p.v[k], p.beta2), __dmul_rn(__dmul_rn(1.0 - p.beta2, gk), gk));
-            p.m[k] = mk;
-            p.v[k] = vk;
-            const double num = __dmul_rn(p.lr, __ddiv_rn(mk, bc[0]));
-            const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, bc[1])), p.eps);
-            w = __dsub_rn(w, __ddiv_rn(num, den));
-        } else {
-            w = __dsub_rn(w, __dmul_rn(p.lr, gk));
-        }
-        p.params[k] = w;
-        if (do_sync) p.target[k] = w;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        p.counters[0] += 1;
-        p.counters[1] += 1;
-        p.counters[2] = 1;
-        *p.last_loss = *p.loss;
-    }
+// (trainer.py:288-289), one parameter per thread over many CTAs.  The
+// bias corrections and the sync decision come from the step counters, which
+// only the last CTA to finish advances (apply_finish), after every CTA read them.
+struct AdamCoef {
+    double bc0, bc1;
+    bool sync;
+};
+
+__device__ __forceinline__ AdamCoef adam_coef(const ApplyParams& p) {
+    AdamCoef a;
+    const int64_t t = p.counters[0] + 1;
+    a.bc0 = 1.0 - pow(p.beta1, (double)t);
+    a.bc1 = 1.0 - pow(p.beta2, (double)t);
+    const int64_t gs = p.counters[1] + 1;  // step_index = grad_steps + 1
+    a.sync = (gs % p.sync_every) == 0;
+    return a;
 }
 
-__global__ void learner_apply_kernel(const ApplyParams p) {
-    if (!(p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size))) apply_update(p);
-    if (p.advance && threadIdx.x == 0) p.counters[3] += 1;
+__device__ __forceinline__ void apply_elem(const ApplyParams& p, const AdamCoef& a, int k, double gk) {
+    double w = p.params[k];
+    if (p.adam) {
+        double mk = __dadd_rn(__dmul_rn(p.m[k], p.beta1), __dmul_rn(1.0 - p.beta1, gk));
+        double vk = __dadd_rn(__dmul_rn(p.v[k], p.beta2), __dmul_rn(__dmul_rn(1.0 - p.beta2, gk), gk));
+        p.m[k] = mk;
+        p.v[k] = vk;
+        const double num = __dmul_rn(p.lr, __ddiv_rn(mk, a.bc0));
+        const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, a.bc1)), p.eps);
+        w = __dsub_rn(w, __ddiv_rn(num, den));
+    } else {
+        w = __dsub_rn(w, __dmul_rn(p.lr, gk));
+    }
+    p.params[k] = w;
+    if (a.sync) p.target[k] = w;
 }
 
-// Fused update (be_train_iteration, single GPU): the CTA that finishes its
-// row tile last sums every tile's partials in tile order (the same fixed order
-// as learner_reduce_kernel) and applies the optimizer step — one launch per
-// update: Double-Q targets, Huber backward, reduction, Adam, target sync.
-struct FuseParams {
-    int32_t fused;
-    unsigned* done;  // arrival counter of the CTAs (reset by the last one)
-    double* grad;
-    double* loss;
+__device__ __forceinline__ void apply_finish(const ApplyParams& p) {
+    p.counters[0] += 1;
+    p.counters[1] += 1;
+    p.counters[2] = 1;
+    *p.last_loss = *p.loss;
+}
+
+__device__ __forceinline__ bool update_gated(const ApplyParams& p) {
+    return p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size);
+}
+
+// Everything after the row tiles.  A CTA owns 32 consecutive parameters
+// (k == nparam: the loss); warp w sums tiles [w n/8, (w + 1) n/8) in tile order
+// and warp 0 adds the 8 slice sums in slice order — one fixed tree for every
+// execution path, so host-driven, device-resident and graph runs agree bit for bit.
+//   reduce: grad[k] = that sum, loss = sum / B;
+//   apply:  the optimizer step from grad (reduce && apply: fused, one launch);
+//   neither: only advance the iteration counter (updates_per_step == 0).
+// Warm-up / DP gate closed: no update; a reduce-only launch zeroes grad (keeps a DP
+// all-reduce well defined); the iteration counter still advances.
+struct UpdateParams {
+    int32_t n_tiles, B, reduce, apply;
+    const double* partial;  // [n_tiles][nparam + 1]
+    unsigned* done;         // CTA arrival counter (reset by the last CTA)
     ApplyParams ap;
 };
 
-__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p, const FuseParams f) {
+__global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdateParams u) {
+    const ApplyParams& p = u.ap;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x * 32 + lane;
+    if (!u.reduce && !u.apply) {
+        if (k == 0 && warp == 0 && p.advance) p.counters[3] += 1;
+        return;
+    }
+    if (update_gated(p)) {
+        if (warp == 0) {
+            if (!u.apply && k < p.nparam) p.grad[k] = 0.0;
+            if (u.apply && p.advance && k == 0) p.counters[3] += 1;
+        }
+        return;
+    }
+    __shared__ double slice[UTHREADS / 32][32];
+    double gk = 0.0;
+    if (u.reduce) {
+        constexpr int NS = UTHREADS / 32;
+        const int per = (u.n_tiles + NS - 1) / NS;
+        const int t0 = warp * per, t1 = min(u.n_tiles, t0 + per);
+        double s = 0.0;
+        if (k <= p.nparam) {
+            const size_t ld = (size_t)p.nparam + 1;
+            const double* src = u.partial + k;
+#pragma unroll 8
+            for (int t = t0; t < t1; ++t) s = __dadd_rn(s, __ldcg(src + (size_t)t * ld));
+        }
+        slice[warp][lane] = s;
+        __syncthreads();
+        if (warp != 0) return;
+        s = slice[0][lane];
+#pragma unroll
+        for (int w = 1; w < NS; ++w) s = __dadd_rn(s, slice[w][lane]);
+        if (k < p.nparam) p.grad[k] = gk = s;
+        else if (k == p.nparam) *p.loss = __ddiv_rn(s, (double)u.B);
+    } else {
+        if (warp != 0) return;
+        if (k < p.nparam) gk = p.grad[k];
+    }
+    if (!u.apply) return;
+    // warp 0 only from here
+    const AdamCoef a = adam_coef(p);
+    if (k < p.nparam) apply_elem(p, a, k, gk);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && atomicAdd(u.done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        apply_finish(p);
+        if (p.advance) p.counters[3] += 1;
+        *u.done = 0u;
+    }
+}
+
+template <int DM>
+__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
     double* xs = lsm;                    // [LROWS][D]
@@ -345,10 +454,7 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     const int row0 = blockIdx.x * LROWS;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) {  // warm-up: no update
-        if (f.fused && f.ap.advance && blockIdx.x == 0 && threadIdx.x == 0) f.ap.counters[3] += 1;
-        return;
-    }
+    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) return;  // warm-up: no update
     const uint64_t counter = p.iter_dev ? (uint64_t)(*p.iter_dev) * (uint64_t)p.ups + (uint64_t)p.uidx
                                         : p.counter;
 
@@ -373,9 +479,9 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     }
     __syncthreads();
     // ---- Double-Q targets (trainer.py:240-243)
-    forward_rows(xs2, D, H, M, p.w1, p.b1, p.w2, p.b2, ht, q2, nullptr);
-    forward_rows(xs2, D, H, M, p.tw1, p.tb1, p.tw2, p.tb2, ht, q2t, nullptr);
-    forward_rows(xs, D, H, M, p.w1, p.b1, p.w2, p.b2, hh, q, nullptr);
+    forward_rows<DM>(xs2, D, H, M, p.w1, p.b1, p.w2, p.b2, ht, q2);
+    forward_rows<DM>(xs2, D, H, M, p.tw1, p.tb1, p.tw2, p.tb2, ht, q2t);
+    forward_rows<DM>(xs, D, H, M, p.w1, p.b1, p.w2, p.b2, hh, q);
     for (int k = threadIdx.x; k < LROWS; k += blockDim.x) {
         const bool valid = row0 + k < p.B;
         int best = 0;
@@ -403,26 +509,39 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     __syncthreads();
     // ---- backward over this tile's rows (trainer.py:256-263)
     for (int j = threadIdx.x; j < H; j += blockDim.x) {
-        double dw2[8], db1 = 0.0, dw1[32];
-        for (int m = 0; m < M; ++m) dw2[m] = 0.0;
-        for (int d = 0; d < D; ++d) dw1[d] = 0.0;
-        double w2j[8];
-        for (int m = 0; m < M; ++m) w2j[m] = p.w2[j * M + m];
+        double dw2[BE_MAX_TIERS], db1 = 0.0, dw1[DM], w2j[BE_MAX_TIERS];
+#pragma unroll
+        for (int m = 0; m < BE_MAX_TIERS; ++m) {
+            dw2[m] = 0.0;
+            w2j[m] = m < M ? p.w2[j * M + m] : 0.0;
+        }
+#pragma unroll
+        for (int d = 0; d < DM; ++d) dw1[d] = 0.0;
+#pragma unroll
         for (int row = 0; row < LROWS; ++row) {
             const double hv = hh[row * H + j];
             double dh = 0.0;
-            for (int m = 0; m < M; ++m) {
-                const double gm = g[row * M + m];
-                dw2[m] = __fma_rn(hv, gm, dw2[m]);
-                dh = __fma_rn(gm, w2j[m], dh);
+#pragma unroll
+            for (int m = 0; m < BE_MAX_TIERS; ++m) {
+                if (m < M) {
+                    const double gm = g[row * M + m];
+                    dw2[m] = __fma_rn(hv, gm, dw2[m]);
+                    dh = __fma_rn(gm, w2j[m], dh);
+                }
             }
             if (!(hv > 0.0)) dh = 0.0;  // dh[h <= 0] = 0
             db1 = __dadd_rn(db1, dh);
-            for (int d = 0; d < D; ++d) dw1[d] = __fma_rn(xs[row * D + d], dh, dw1[d]);
+#pragma unroll
+            for (int d = 0; d < DM; ++d)
+                if (d < D) dw1[d] = __fma_rn(xs[row * D + d], dh, dw1[d]);
         }
-        for (int d = 0; d < D; ++d) out[d * H + j] = dw1[d];
+#pragma unroll
+        for (int d = 0; d < DM; ++d)
+            if (d < D) out[d * H + j] = dw1[d];
         out[D * H + j] = db1;
-        for (int m = 0; m < M; ++m) out[D * H + H + j * M + m] = dw2[m];
+#pragma unroll
+        for (int m = 0; m < BE_MAX_TIERS; ++m)
+            if (m < M) out[D * H + H + j * M + m] = dw2[m];
     }
     if (threadIdx.x < M) {
         double s = 0.0;
@@ -433,44 +552,6 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         double s = 0.0;
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, lrow[row]);
         out[nparam] = s;
-    }
-    if (!f.fused) return;
-    __threadfence();  // publish this tile's partials
-    __syncthreads();
-    __shared__ int last;
-    if (threadIdx.x == 0) last = atomicAdd(f.done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    for (int k = threadIdx.x; k <= nparam; k += blockDim.x) {
-        double s = 0.0;
-        for (int t = 0; t < (int)gridDim.x; ++t) s = __dadd_rn(s, __ldcg(p.partial + (size_t)t * (nparam + 1) + k));
-        if (k < nparam) f.grad[k] = s;
-        else *f.loss = __ddiv_rn(s, (double)p.B);
-    }
-    __syncthreads();
-    apply_update(f.ap);
-    if (threadIdx.x == 0) {
-        *f.done = 0u;
-        if (f.ap.advance) f.ap.counters[3] += 1;
-    }
-}
-
-// Sum the per-tile partials in tile order -> grad[nparam], loss.
-__global__ void learner_reduce_kernel(int n_tiles, int nparam, int B, const double* partial,
-                                      double* grad, double* loss, const int64_t* ring_state,
-                                      int64_t min_size, int sampling, const int64_t* gate) {
-    if (gate ? *gate == 0 : (sampling && ring_state[1] < min_size)) {
-        // no update this iteration: a zero gradient keeps a DP all-reduce well defined
-        for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nparam; k += gridDim.x * blockDim.x)
-            grad[k] = 0.0;
-        return;
-    }
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= nparam; k += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int t = 0; t < n_tiles; ++t) s = __dadd_rn(s, partial[(size_t)t * (nparam + 1) + k]);
-        if (k < nparam) grad[k] = s;
-        else *loss = __ddiv_rn(s, (double)B);
     }
 }
 
@@ -500,8 +581,6 @@ struct be_learner {
     uint8_t* pflags; // [E][P]
     double* preward; // [E][P]
     int64_t* low;
-    int32_t* count;
-    int64_t* offset;
     int32_t* status;
     double* wl_state;  // [E][3]
     // be_train_iteration: per-env arrival / task / true rate of the current iteration
@@ -509,14 +588,16 @@ struct be_learner {
     uint8_t* it_task;
     double* it_rate;
     unsigned* done;    // fused-update CTA arrival counter
+    unsigned long long* scan;  // commit look-back state [(E + 7) / 8]
+    unsigned* ticket;          // commit ticket / epoch
     int64_t* gate;     // DP update gate (be_train_iteration use_gate)
 };
 
 static void learner_free(be_learner* L) {
     void* ptrs[] = {L->params, L->target, L->m, L->v, L->grad, L->partial, L->loss, L->counters,
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
-                    L->preward, L->low, L->count, L->offset, L->status, L->wl_state,
-                    L->it_arrival, L->it_task, L->it_rate, L->done, L->gate};
+                    L->preward, L->low, L->status, L->wl_state,
+                    L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket};
     for (void* p : ptrs) cudaFree(p);
     delete L;
 }
@@ -554,9 +635,10 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->rr, C * 8}, {(void**)&L->rc, C * 8}, {(void**)&L->ra, C},
         {(void**)&L->ring_state, 64}, {(void**)&L->px, P * E * D * 8}, {(void**)&L->pa, P * E},
         {(void**)&L->pflags, E * P}, {(void**)&L->preward, E * P * 8}, {(void**)&L->low, E * 8},
-        {(void**)&L->count, E * 4}, {(void**)&L->offset, E * 8}, {(void**)&L->status, 64},
+        {(void**)&L->status, 64},
         {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
-        {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64}};
+        {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64},
+        {(void**)&L->scan, ((E + CENVS - 1) / CENVS) * 8}, {(void**)&L->ticket, 64}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -566,7 +648,9 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         cudaMemset(*a.p, 0, a.n);
     }
     // configured here, not at launch time: launches may be captured in a CUDA graph
-    cudaFuncSetAttribute(learner_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(learner_partial_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(learner_partial_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(learner_partial_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         learner_free(L);
@@ -659,8 +743,6 @@ static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cud
     p.pflags = L->pflags;
     p.preward = L->preward;
     p.low = L->low;
-    p.count = L->count;
-    p.offset = L->offset;
     p.ring_state = L->ring_state;
     p.capacity = L->cfg.replay_capacity;
     p.rs = L->rs;
@@ -669,11 +751,9 @@ static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cud
     p.rr = L->rr;
     p.rc = L->rc;
     p.status = L->status;
-    const int blocks = (int)(((int64_t)p.E * 32 + 255) / 256);
-    commit_kernel<false><<<blocks, 256, 0, st>>>(p);
-    commit_scan_kernel<<<1, 1023, 0, st>>>(p.E, L->count, L->offset, L->ring_state, p.capacity);
-    commit_kernel<true><<<blocks, 256, 0, st>>>(p);
-    commit_finish_kernel<<<1, 1, 0, st>>>(L->ring_state, p.capacity);
+    p.scan = L->scan;
+    p.ticket = L->ticket;
+    commit_fused_kernel<<<(p.E + CENVS - 1) / CENVS, CENVS * 32, 0, st>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "commit launch");
 }
@@ -684,6 +764,23 @@ int32_t be_learner_commit(be_learner* L, int64_t step, void* stream) {
 }
 
 static ApplyParams apply_params(be_learner* L, int32_t explicit_batch, int32_t advance);
+
+static int launch_update(be_learner* L, int reduce, int apply, ApplyParams ap, const int64_t* gate,
+                         cudaStream_t st) {
+    UpdateParams u{};
+    u.n_tiles = L->n_tiles;
+    u.B = L->cfg.batch;
+    u.reduce = reduce;
+    u.apply = apply;
+    u.partial = L->partial;
+    u.done = L->done;
+    ap.gate = gate;
+    u.ap = ap;
+    const int blocks = (reduce || apply) ? (L->nparam + 32) / 32 : 1;  // 32 parameters (+ the loss) per CTA
+    learner_update_kernel<<<blocks, UTHREADS, 0, st>>>(u);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner update launch");
+}
 
 static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* a, const double* r,
                                  const double* s2, const double* c, int32_t B, uint64_t seed,
@@ -726,24 +823,16 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     p.ups = ups;
     p.uidx = uidx;
     p.gate = gate;
-    FuseParams f{};
-    f.fused = fused;
-    if (fused) {
-        f.done = L->done;
-        f.grad = L->grad;
-        f.loss = L->loss;
-        f.ap = apply_params(L, sampling ? 0 : 1, advance);
-    }
     const size_t smem = sizeof(double) * (2 * LROWS * D + 2 * LROWS * H + 4 * LROWS * M + 3 * LROWS) +
                         sizeof(int) * LROWS;
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "hidden too large for the learner tile");
-    learner_partial_kernel<<<L->n_tiles, LTHREADS, smem, st>>>(p, f);
-    if (!fused)
-        learner_reduce_kernel<<<(L->nparam + 256) / 256, 256, 0, st>>>(
-            L->n_tiles, L->nparam, B, L->partial, L->grad, L->loss, L->ring_state, p.min_size,
-            sampling ? 1 : 0, p.gate);
+    if (D <= 8) learner_partial_kernel<8><<<L->n_tiles, LTHREADS, smem, st>>>(p);
+    else if (D <= 16) learner_partial_kernel<16><<<L->n_tiles, LTHREADS, smem, st>>>(p);
+    else learner_partial_kernel<32><<<L->n_tiles, LTHREADS, smem, st>>>(p);
+    // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
     cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner launch");
+    if (e != cudaSuccess) return set_cuda_error(e, "learner launch");
+    return launch_update(L, 1, fused, apply_params(L, sampling ? 0 : 1, fused ? advance : 0), gate, st);
 }
 
 int32_t be_learner_backward(be_learner* L, uint64_t seed, uint64_t counter, int64_t* sample_idx,
@@ -789,9 +878,7 @@ static ApplyParams apply_params(be_learner* L, int32_t explicit_batch, int32_t a
 
 int32_t be_learner_apply(be_learner* L, int32_t explicit_batch, void* stream) {
     if (!L) return set_error(BE_EINVAL, "NULL learner");
-    learner_apply_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(apply_params(L, explicit_batch, 0));
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "apply launch");
+    return launch_update(L, 0, 1, apply_params(L, explicit_batch, 0), nullptr, (cudaStream_t)stream);
 }
 
 int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* c, void* stream) {
@@ -839,7 +926,8 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
             if (rc) return rc;
         }
         if (ups == 0) {  // no learner: still advance the iteration
-            learner_apply_kernel<<<1, 32, 0, st>>>(apply_params(L, 2, 1));
+            rc = launch_update(L, 0, 0, apply_params(L, 1, 1), nullptr, st);
+            if (rc) return rc;
         }
     } else if (c->phase == 1) {
         rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch,
@@ -847,9 +935,8 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                    gate);
         if (rc) return rc;
     } else if (c->phase == 2) {
-        ApplyParams ap = apply_params(L, 0, c->update_index == ups - 1);
-        ap.gate = gate;
-        learner_apply_kernel<<<1, 1024, 0, st>>>(ap);
+        rc = launch_update(L, 0, 1, apply_params(L, 0, c->update_index == ups - 1), gate, st);
+        if (rc) return rc;
     }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "train iteration launch");

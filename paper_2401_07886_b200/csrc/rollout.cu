@@ -56,13 +56,6 @@ struct RolloutParams {
                           // memory (L1/L2-resident), so shared memory holds only the screen
 };
 
-// Packs the fp64 weights once per launch for the screened rollout's fallback.
-template <int M>
-__global__ void __launch_bounds__(256) stage_qpack_kernel(const double* w1, const double* b1, const double* w2,
-                                                          const double* b2, int T, int H, double* out) {
-    stage_qnet<M>(w1, b1, w2, b2, T, H, out);
-}
-
 __device__ __forceinline__ void raise_status(int32_t* status, int code, int env) {
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
 }
@@ -313,7 +306,7 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
 template <int M>
 static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
     if (p.screen) {
-        stage_qpack_kernel<M><<<1, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
+        stage_qpack_kernel<M><<<QPACK_CTAS, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
                                                  const_cast<double*>(p.qpack));
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");

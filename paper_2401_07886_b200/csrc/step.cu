@@ -80,6 +80,7 @@ struct StepParams {
     double eps_start, eps_end;
     int64_t eps_decay;
     int32_t pending_P;
+    const double* qpack;  // packed fp64 weights (QLayout) in global memory, read through L1
 };
 
 // TrainConfig.epsilon_at (trainer.py:85-90), same IEEE operations as the host
@@ -90,18 +91,28 @@ __device__ __forceinline__ double epsilon_at(int64_t it, double start, double en
 }
 
 template <int M>
+__device__ __forceinline__ void step_env(const StepParams& p, int e, const Score& sc, const double* sw,
+                                         bool policy, int T, int H, int D);
+
+template <int M>
 __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
-    double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
     const int T = p.cfg.n_tasks;
     const int H = p.H, D = T + M + 1;
     const bool policy = !p.drain && p.forced == nullptr && p.static_tier < 0;
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
-    if (policy) stage_qnet<M>(p.w1, p.b1, p.w2, p.b2, T, H, sw);
     __syncthreads();
-    const int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (e >= p.E) return;
+    // persistent grid (one wave): the weights are staged once per CTA, then every
+    // warp steps envs warp_id, warp_id + n_warps, ...
+    const int n_warps = (gridDim.x * blockDim.x) >> 5;
+    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < p.E; e += n_warps)
+        step_env<M>(p, e, sc, p.qpack, policy, T, H, D);
+}
+
+template <int M>
+__device__ __forceinline__ void step_env(const StepParams& p, int e, const Score& sc, const double* sw,
+                                         bool policy, int T, int H, int D) {
     const int lane = threadIdx.x & 31;
     const TierC tc = lane_tier(p.cfg, lane, p.skip);  // skip table read through L1
     const bool al = tc.tier >= 0;
@@ -227,16 +238,30 @@ int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st) {
 template <int M>
 static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
     auto kern = env_step_kernel<M>;
+    if (p.qpack) {  // pack the (possibly just updated) weights for this step
+        stage_qpack_kernel<M><<<QPACK_CTAS, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
+                                                          const_cast<double*>(p.qpack));
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
+    }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     }
     int threads = 256;
-    int blocks = (int)(((long long)p.E * 32 + threads - 1) / threads);
-    kern<<<blocks, threads, smem, st>>>(p);
+    long long blocks = ((long long)p.E * 32 + threads - 1) / threads;
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+    kern<<<(unsigned)blocks, threads, smem, st>>>(p);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step launch");
 }
+
+static size_t step_smem_bytes() { return (sizeof(Score) + 15) & ~size_t(15); }
 
 static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st) {
     switch (p.cfg.n_tiers) {
@@ -296,8 +321,8 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
         p.w2 = W->w2;
         p.b2 = W->b2;
     }
-    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, policy ? p.H : 0, policy);
-    return dispatch_step(p, smem, st);
+    if (policy) p.qpack = env->d_qpack;
+    return dispatch_step(p, step_smem_bytes(), st);
 }
 
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
@@ -322,15 +347,14 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     p.b1 = W->b1;
     p.w2 = W->w2;
     p.b2 = W->b2;
-    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, p.H, true);
-    return dispatch_step(p, smem, st);
+    p.qpack = env->d_qpack;
+    return dispatch_step(p, step_smem_bytes(), st);
 }
 
 int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st) {
     StepParams p = base_params(env, rec_ld, rec);
     p.drain = 1;
-    size_t smem = rollout_smem_bytes(env->cfg.n_tasks, env->cfg.n_tiers, 0, false);
-    return dispatch_step(p, smem, st);
+    return dispatch_step(p, step_smem_bytes(), st);
 }
 
 }  // namespace be

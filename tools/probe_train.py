@@ -15,8 +15,10 @@ run_training(default_tiers(), RewardSpec.default(), TrainConfig(batch_size=512, 
              updates_per_step=ups)  # warm (module load, allocator)
 torch.cuda.synchronize()
 t0 = time.time()
-res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=E, mode=mode, updates_per_step=ups)
+tm = {}
+res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=E, mode=mode, updates_per_step=ups, timing=tm)
 torch.cuda.synchronize()
 dt = time.time() - t0
-print(f"mode={mode} E={E} its={its} ups={ups}: {dt:.2f}s  {its/dt:.1f} it/s  {E*its/dt:.3e} env-steps/s  "
+print(f"mode={mode} E={E} its={its} ups={ups}: loop {tm['loop_ms']:.1f} ms device = {its / tm['loop_ms'] * 1e3:.1f} it/s; "
+      f"wall incl. setup {dt:.2f}s  {its/dt:.1f} it/s  {E*its/dt:.3e} env-steps/s  "
       f"updates={res.updates} ({res.updates/dt:.1f}/s) transitions={res.transitions} log={res.log[-1]}")
