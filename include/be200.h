@@ -14,6 +14,8 @@
  *   be_env_drain                     ClusterSim.drain              simcore.py:151-153
  *   be_rollout_greedy                run_eval (whole trace)        evalkit.py:154-209
  *   be_qnet_route_f64                select_action / argmax(forward) policy.py:111-132
+ *   be_qnet_route_tc                 the same on the tensor cores   policy.py:111-132
+ *                                    (tcgen05 tf32, certified, fp64 fallback)
  *   be_reduce_eval                   windowed + threshold_counts,  evalkit.py:217-241,
  *                                    miss_fractions_by_rate        evalkit.py:61-68
  *   be_reduce_selection              selection_distribution counts evalkit.py:244-262
@@ -172,6 +174,25 @@ int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers
                           const double* x, int32_t batch, double epsilon, uint64_t philox_seed,
                           uint64_t philox_counter, double* q_out, uint8_t* action_out,
                           void* stream);
+
+/* The same router on the tensor cores (route_tc.cu): layer 1 as
+ * tcgen05.mma.kind::tf32 with a 3xTF32 split over 128-state tiles (TMEM
+ * accumulators, weights staged in shared memory by one bulk async copy),
+ * relu + layer 2 in fp32; each greedy decision is certified by an error bound
+ * or re-evaluated with the exact arithmetic of be_qnet_route_f64, so actions
+ * equal be_qnet_route_f64's.  q_out (nullable) is fp32 [batch][n_tiers]
+ * (within 1e-5 relative of the fp64 router).  Requires n_tiers <= 4,
+ * n_tasks + n_tiers + 2 <= 16, hidden a multiple of 32 in [32, 256]
+ * (be_qnet_route_tc_supported); `workspace` = device scratch of
+ * be_qnet_route_tc_workspace_bytes(hidden) bytes (16-byte aligned, not shared
+ * by concurrent calls); stats (nullable, device int64[2]) accumulates
+ * (states, fp64 re-evaluations). */
+int32_t be_qnet_route_tc_supported(int32_t n_tasks, int32_t n_tiers, int32_t hidden);
+size_t be_qnet_route_tc_workspace_bytes(int32_t hidden);
+int32_t be_qnet_route_tc(const be_qweights* W, int32_t n_tasks, int32_t n_tiers, const double* x,
+                         int32_t batch, double epsilon, uint64_t philox_seed, uint64_t philox_counter,
+                         float* q_out, uint8_t* action_out, void* workspace, int64_t* stats,
+                         void* stream);
 
 /* Evaluation reducer (evalkit.py:212-241, :61-74): per env a sequential fp64
  * prefix sum of rewards in request order, trailing `window` means, counts of

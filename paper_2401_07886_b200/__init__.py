@@ -11,7 +11,7 @@ from .specs import (ArrivalEvent, CheckpointError, ModelTierSpec, QNetwork, Rewa
                     load_checkpoint, save_checkpoint)
 from .trace import TraceBatch  # noqa: F401
 from .env import EnvBatch, StepRecords, make_cfg  # noqa: F401
-from .policy import DeviceQNet, route, select_action  # noqa: F401
+from .policy import DeviceQNet, TensorCoreRouter, route, route_tc, select_action  # noqa: F401
 from .evalkit import (EvalRun, GreedyRollout, RequestRecord, ReduceResult, reduce_eval,  # noqa: F401
                       run_eval, run_eval_batch, THRESHOLDS, WINDOW)
 

@@ -133,6 +133,10 @@ SIGNATURES = {
                                  _P, ctypes.POINTER(BeRecords), _P]),
     "be_qnet_route_f64": (_I32, [ctypes.POINTER(BeQWeights), _I32, _I32, _P, _I32, _D, _U64, _U64,
                                  _P, _P, _P]),
+    "be_qnet_route_tc_supported": (_I32, [_I32, _I32, _I32]),
+    "be_qnet_route_tc_workspace_bytes": (_SZ, [_I32]),
+    "be_qnet_route_tc": (_I32, [ctypes.POINTER(BeQWeights), _I32, _I32, _P, _I32, _D, _U64, _U64,
+                                _P, _P, _P, _P, _P]),
     "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
                               _P, _P, _P]),
     "be_reduce_selection": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _I32, _I32, _I32, _P, _P]),

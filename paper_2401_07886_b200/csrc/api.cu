@@ -326,6 +326,32 @@ int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers
                         action_out, (cudaStream_t)stream);
 }
 
+int32_t be_qnet_route_tc_supported(int32_t n_tasks, int32_t n_tiers, int32_t hidden) {
+    return route_tc_supported(n_tasks, n_tiers, hidden) ? 1 : 0;
+}
+
+size_t be_qnet_route_tc_workspace_bytes(int32_t hidden) {
+    return hidden >= 32 && hidden <= 256 ? route_tc_workspace_bytes(hidden) : 0;
+}
+
+int32_t be_qnet_route_tc(const be_qweights* W, int32_t n_tasks, int32_t n_tiers, const double* x,
+                         int32_t batch, double epsilon, uint64_t philox_seed, uint64_t philox_counter,
+                         float* q_out, uint8_t* action_out, void* workspace, int64_t* stats,
+                         void* stream) {
+    if (!W || !W->w1 || !W->b1 || !W->w2 || !W->b2 || !x || !action_out || !workspace)
+        return set_error(BE_EINVAL, "NULL argument");
+    if (n_tasks < 1 || n_tasks > BE_MAX_TASKS || n_tiers < 1 || n_tiers > BE_MAX_TIERS)
+        return set_error(BE_EINVAL, "dimensions out of range");
+    if (!route_tc_supported(n_tasks, n_tiers, W->hidden))
+        return set_error(BE_EINVAL, "route_tc needs n_tiers <= 4, n_tasks + n_tiers + 2 <= 16 and hidden a "
+                                    "multiple of 32 in [32, 256]; use be_qnet_route_f64");
+    if (((uintptr_t)workspace & 15) != 0) return set_error(BE_EINVAL, "workspace must be 16-byte aligned");
+    if (!(epsilon >= 0.0 && epsilon <= 1.0)) return set_error(BE_EINVAL, "epsilon must lie in [0, 1]");
+    if (batch < 0) return set_error(BE_EINVAL, "batch must be >= 0");
+    return launch_route_tc(W, n_tasks, n_tiers, x, batch, epsilon, philox_seed, philox_counter, q_out,
+                           action_out, workspace, stats, (cudaStream_t)stream);
+}
+
 int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const double* reward,
                        int32_t window, const double* thetas, int32_t n_theta, int32_t n_buckets,
                        int64_t* win_counts, int64_t* n_windows, int64_t* bucket_miss,

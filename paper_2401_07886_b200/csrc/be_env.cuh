@@ -20,6 +20,7 @@
 
 #include "be200.h"
 #include "be_internal.h"
+#include "be_tc.cuh"
 
 namespace be {
 
@@ -468,16 +469,6 @@ struct QsLayout {
     // floats: task rows [T][H] + values [NV][H] + A [T] + C [M+1] + b2 [M]
     __host__ __device__ static size_t floats(int T, int H) { return (size_t)(T + NV) * H + T + (M + 1) + M; }
 };
-
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-    float2 d;
-    asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-        "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-        "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-        : "=f"(d.x), "=f"(d.y)
-        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-    return d;
-}
 
 // Lane g of a group owns hidden-unit pairs (j0, j1) = (g + 2p LPE, g + 2p LPE + LPE),
 // stored at pair index P = p LPE + g so that a group's loads are consecutive.

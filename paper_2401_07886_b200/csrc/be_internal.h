@@ -66,6 +66,11 @@ int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* re
                   double* bucket_reward, cudaStream_t st);
 int launch_route(const be_qweights* W, int T, int M, const double* x, int B, double eps,
                  uint64_t seed, uint64_t counter, double* q_out, uint8_t* a_out, cudaStream_t st);
+bool route_tc_supported(int T, int M, int H);
+size_t route_tc_workspace_bytes(int H);
+int launch_route_tc(const be_qweights* W, int T, int M, const double* x, int B, double eps, uint64_t seed,
+                    uint64_t counter, float* q_out, uint8_t* a_out, void* workspace, int64_t* stats,
+                    cudaStream_t st);
 int launch_tracegen(int E, int64_t env_offset, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
                     double* arrival, uint8_t* task, cudaStream_t st);
 int launch_tracegen_general(const be_gen_cfg* cfg, int E, int64_t env_offset, int64_t ld,

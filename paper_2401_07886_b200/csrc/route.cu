@@ -8,6 +8,7 @@
 
 #include "be_internal.h"
 #include "be_philox.cuh"
+#include "be_route.cuh"
 
 namespace be {
 
@@ -31,33 +32,9 @@ __global__ void __launch_bounds__(256) route_kernel(int D, int H, const double* 
     const int warps = (gridDim.x * blockDim.x) >> 5;
     for (int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < B; row += warps) {
         double xv = lane < D ? x[(int64_t)row * D + lane] : 0.0;
-        double acc[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) acc[m] = 0.0;
-        for (int j = lane; j < H; j += 32) {
-            double pre = 0.0;
-            for (int d = 0; d < D; ++d) pre = __fma_rn(__shfl_sync(0xffffffffu, xv, d), sW1[d * H + j], pre);
-            pre = __dadd_rn(pre, sb1[j]);
-            double h = pre > 0.0 ? pre : 0.0;
-#pragma unroll
-            for (int m = 0; m < M; ++m) acc[m] = __fma_rn(h, sW2t[m * H + j], acc[m]);
-        }
-        // lanes >= H would contribute zeros; xor butterfly is bit-identical on all lanes
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-            for (int m = 0; m < M; ++m) acc[m] = __dadd_rn(acc[m], __shfl_xor_sync(0xffffffffu, acc[m], off));
         double q[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) q[m] = __dadd_rn(acc[m], sb2[m]);
-        int best = 0;
-        bool nan_seen = q[0] != q[0];
-#pragma unroll
-        for (int m = 1; m < M; ++m) {
-            if (nan_seen) break;
-            if (q[m] != q[m]) { best = m; nan_seen = true; }
-            else if (q[m] > q[best]) best = m;
-        }
+        route_row_f64<M>(xv, D, H, sW1, sb1, sW2t, 1, H, sb2, q);
+        int best = route_argmax<M>(q);
         if (eps > 0.0) {
             P4 r = philox4x32_10(counter, (uint64_t)row, seed);
             if (u01(r.x[0], r.x[1]) < eps) best = (int)below(r.x[2], (uint32_t)M);

@@ -1,0 +1,441 @@
+// route_tc.cu — batched router on the 5th-generation tensor cores:
+// QNetwork.forward + select_action (policy.py:111-132) over B encoded states,
+// be_qnet_route_tc in include/be200.h.
+//
+// Persistent CTAs of 256 threads, two per SM (each owns half of the SM's 512
+// TMEM columns); per 128-state tile:
+//   * every thread converts its state row (fp64, D <= 15 inputs + a constant-1
+//     bias input) to a 3xTF32 split (hi + lo) in shared memory, K-major
+//     no-swizzle UMMA layout;
+//   * one elected thread issues six tcgen05.mma.kind::tf32 (2 K-steps x
+//     {hi.hi, hi.lo, lo.hi}, M = 128, N = H) accumulating the layer-1
+//     pre-activations [128 x H] in fp32 in TMEM; tcgen05.commit -> mbarrier;
+//   * epilogue: two threads per state (warps w and w + 4 read the same TMEM
+//     lanes) tcgen05.ld half of the row each, relu, and the N = M (<= 4) layer-2
+//     dot products on packed FFMA2 from shared memory; halves merged in smem;
+//   * the decision is certified with an error bound (as the rollout screen,
+//     be_env.cuh) whose layer-1 term models each tensor-core accumulation step
+//     of 8 products as 9 fp32 roundings of <= 2u each; states it cannot certify
+//     are re-evaluated by a warp with route_row_f64 — the exact arithmetic of
+//     be_qnet_route_f64 — so every greedy decision equals the fp64 router's.
+// Weights are packed once per call (route_tc_pack_kernel: tf32 hi/lo UMMA
+// images of [W1; b1]^T, W2 pairs, bound tables) and staged per CTA with one
+// bulk asynchronous copy (TMA engine, mbarrier completion).  Q values out are
+// the fp32 screen values (fp64 values for fallback states), within 1e-5
+// relative of the fp64 router.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "be200.h"
+#include "be_internal.h"
+#include "be_philox.cuh"
+#include "be_route.cuh"
+#include "be_tc.cuh"
+
+namespace be {
+
+constexpr int TC_ROWS = 128;  // MMA M: states per tile = TMEM lanes
+constexpr int TC_THREADS = 256;  // two threads per state: each takes half of the hidden columns
+constexpr int TC_K = 16;      // inputs (D <= 15) + the bias input, two tf32 K-steps of 8
+constexpr int TC_MP = 4;      // layer-2 outputs padded (n_tiers <= 4)
+constexpr int TC_FLIST = 4096;  // deferred fp64 re-evaluations per CTA (shared-memory list)
+
+struct TcLayout {  // byte offsets inside the packed image (= the shared-memory image)
+    int H;
+    __host__ __device__ int b1h() const { return 0; }
+    __host__ __device__ int b1l() const { return H * TC_K * 4; }
+    __host__ __device__ int w2p() const { return 2 * H * TC_K * 4; }         // [H/2][TC_MP] float2
+    __host__ __device__ int b2() const { return w2p() + (H / 2) * TC_MP * 8; }  // [TC_MP] float
+    __host__ __device__ int bound() const { return b2() + TC_MP * 4; }         // [TC_K] float
+    __host__ __device__ int bytes() const { return bound() + TC_K * 4; }       // multiple of 16
+};
+
+// element (n, k) of a K-major no-swizzle UMMA operand with K = 16: 8 x 16-byte core
+// matrices, K-groups of 4 at 128 B (LBO), 8-row groups at 512 B (SBO); in floats
+__host__ __device__ __forceinline__ int umma_off(int n, int k) {
+    return (n >> 3) * 128 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3);
+}
+
+// error-bound constant K (units of u = 2^-24) for hidden width H: layer 1 = input /
+// weight rounding and the dropped lo.lo term (14) + 6 MMAs x 9 accumulations x 2 (108);
+// layer 2 = FFMA2 chains of <= H/16 + 1 terms per half + the half merge + 4 tree/bias
+// adds + W2 rounding (H/16 + 7); slack 16
+__host__ __device__ __forceinline__ double tc_bound_k(int H) { return (double)(122 + H / 16 + 7 + 16) * 0x1p-24; }
+
+template <int M>
+__global__ void __launch_bounds__(256) route_tc_pack_kernel(const double* w1, const double* b1, const double* w2,
+                                                            const double* b2, int D, int H, float* img) {
+    const TcLayout L{H};
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+    float* b1h = img + L.b1h() / 4;
+    float* b1l = img + L.b1l() / 4;
+    for (int e = tid; e < H * TC_K; e += nt) {
+        const int n = e / TC_K, k = e % TC_K;
+        const double w = k < D ? w1[(size_t)k * H + n] : (k == D ? b1[n] : 0.0);
+        const float f = __double2float_rn(w);
+        const float hi = tc::to_tf32(f);
+        b1h[umma_off(n, k)] = hi;
+        b1l[umma_off(n, k)] = tc::to_tf32(__fsub_rn(f, hi));
+    }
+    float2* w2p = reinterpret_cast<float2*>(img + L.w2p() / 4);
+    for (int e = tid; e < (H / 2) * TC_MP; e += nt) {
+        const int jp = e / TC_MP, m = e % TC_MP;
+        w2p[e] = m < M ? make_float2(__double2float_rn(w2[(size_t)(2 * jp) * M + m]),
+                                     __double2float_rn(w2[(size_t)(2 * jp + 1) * M + m]))
+                       : make_float2(0.f, 0.f);
+    }
+    float* fb2 = img + L.b2() / 4;
+    for (int m = tid; m < TC_MP; m += nt) fb2[m] = m < M ? __double2float_rn(b2[m]) : 0.f;
+    // bound tables: C[k] = K max_m sum_j |W2[j][m]| |W1[k][j]| (k < D), C[D] = K max_m
+    // (sum_j |W2[j][m]| |b1[j]| + |b2[m]|); one warp per row k
+    float* C = img + L.bound() / 4;
+    const double K = tc_bound_k(H);
+    const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nt >> 5;
+    for (int k = gw; k < TC_K; k += nw) {
+        double mx = 0.0;
+        bool bad = false;
+        for (int m = 0; m < M; ++m) {
+            double acc = 0.0;
+            for (int j = lane; j < H; j += 32) {
+                const double a = k < D ? w1[(size_t)k * H + j] : (k == D ? b1[j] : 0.0);
+                acc = __fma_rn(fabs(w2[(size_t)j * M + m]), fabs(a), acc);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+            if (k == D) acc = __dadd_ru(acc, fabs(b2[m]));
+            mx = fmax(mx, acc);
+            bad = bad || acc != acc;
+        }
+        if (lane == 0) C[k] = bad ? __int_as_float(0x7fc00000) : __double2float_ru(__dmul_ru(K, mx));
+    }
+}
+
+struct RouteTcParams {
+    const double* w1;
+    const double* b1;
+    const double* w2;
+    const double* b2;
+    const float* img;
+    int32_t D, H, B, ncols;
+    const double* x;
+    double eps;
+    uint64_t seed, counter;
+    float* q_out;
+    uint8_t* a_out;
+    unsigned long long* stats;  // [2] states, fp64 fallbacks (nullable)
+};
+
+// DM: compile-time bound of the input count D (8 for the shipped 4 tasks x 3 tiers)
+template <int M, int DM>
+__global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcParams p) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const TcLayout L{p.H};
+    const int img_bytes = L.bytes();
+    float* img = reinterpret_cast<float*>(smem);
+    float* Ah = reinterpret_cast<float*>(smem + ((img_bytes + 1023) & ~1023));
+    float* Al = Ah + TC_ROWS * TC_K;
+    float2* part = reinterpret_cast<float2*>(Al + TC_ROWS * TC_K);  // [4][TC_MP][TC_ROWS] upper-half sums
+    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 4 * TC_MP * TC_ROWS);  // [0] image, [1] MMA
+    uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bars + 2);
+    int* fcount = reinterpret_cast<int*>(tmem_sh + 1);
+    int* flist = fcount + 1;  // [TC_FLIST]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r = tid & (TC_ROWS - 1);      // state (= TMEM lane) of this thread
+    const bool lower = tid < TC_ROWS;       // lower threads: columns [0, c_mid) + the decision
+    const int D = p.D, H = p.H;
+    const int nch = H / 32, c_mid = (nch + 1) / 2;
+
+    if (tid == 0) {
+        tc::mbar_init(&bars[0], 1);
+        tc::mbar_init(&bars[1], 1);
+        tc::fence_mbar_init();
+        *fcount = 0;
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_sh, (uint32_t)p.ncols);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = *tmem_sh;
+    if (tid == 0) {  // weights: one bulk asynchronous copy of the packed image
+        tc::mbar_expect_tx(&bars[0], (uint32_t)img_bytes);
+        tc::bulk_g2s(img, p.img, (uint32_t)img_bytes, &bars[0]);
+    }
+    tc::mbar_wait(&bars[0], 0);
+
+    const float* B1h = img + L.b1h() / 4;
+    const float* B1l = img + L.b1l() / 4;
+    const float2* W2p = reinterpret_cast<const float2*>(img + L.w2p() / 4);
+    const float* fb2 = img + L.b2() / 4;
+    const float* C = img + L.bound() / 4;
+    const uint32_t idesc = tc::idesc_tf32(TC_ROWS, H);
+    const int ntiles = (p.B + TC_ROWS - 1) / TC_ROWS;
+    uint32_t phase = 0;
+    unsigned n_rows = 0, n_fb = 0;
+
+    // fp64 re-evaluation of the states the bound could not certify, one warp per
+    // state; deferred (CTA list in shared memory) so no tile waits for it
+    auto fallback = [&](int nf) {
+        for (int f = warp; f < nf; f += TC_THREADS / 32) {
+            const int rf = flist[f];
+            const double xv = lane < D ? __ldg(p.x + (size_t)rf * D + lane) : 0.0;
+            double q64[M];
+            route_row_f64<M>(xv, D, H, p.w1, p.b1, p.w2, M, 1, p.b2, q64);
+            int b = route_argmax<M>(q64);
+            if (p.eps > 0.0) {
+                P4 rn = philox4x32_10(p.counter, (uint64_t)rf, p.seed);
+                if (u01(rn.x[0], rn.x[1]) < p.eps) b = (int)below(rn.x[2], (uint32_t)M);
+            }
+            if (lane < M && p.q_out) {
+#pragma unroll
+                for (int m = 0; m < M; ++m)
+                    if (lane == m) p.q_out[(size_t)rf * M + m] = (float)q64[m];
+            }
+            if (lane == 0) p.a_out[rf] = (uint8_t)b;
+        }
+    };
+    // relu + layer 2 of one 32-column chunk (packed FFMA2, 4 accumulator sets)
+    float2 a[4][M];
+    auto consume = [&](const float(&u)[32], int c) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float2 h = make_float2(fmaxf(u[2 * i], 0.f), fmaxf(u[2 * i + 1], 0.f));
+            const float4* wp = reinterpret_cast<const float4*>(W2p + (size_t)(c * 16 + i) * TC_MP);
+            const float4 w01 = wp[0];
+            a[i & 3][0] = ffma2(h, make_float2(w01.x, w01.y), a[i & 3][0]);
+            if (M > 1) a[i & 3][M > 1 ? 1 : 0] = ffma2(h, make_float2(w01.z, w01.w), a[i & 3][M > 1 ? 1 : 0]);
+            if (M > 2) {
+                const float4 w23 = wp[1];
+                a[i & 3][M > 2 ? 2 : 0] = ffma2(h, make_float2(w23.x, w23.y), a[i & 3][M > 2 ? 2 : 0]);
+                if (M > 3) a[i & 3][M > 3 ? 3 : 0] = ffma2(h, make_float2(w23.z, w23.w), a[i & 3][M > 3 ? 3 : 0]);
+            }
+        }
+    };
+    auto load_row = [&](int tile, double (&xd)[DM]) {
+        const int row = tile * TC_ROWS + r;
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            xd[k] = (lower && k < D && tile < ntiles && row < p.B) ? __ldg(p.x + (size_t)row * D + k) : 0.0;
+    };
+    double xn[DM];  // next tile's state row (lower threads), loaded during this tile's epilogue
+    load_row(blockIdx.x, xn);
+
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int row = tile * TC_ROWS + r;
+        const bool valid = lower && row < p.B;
+        // ---- A operand (lower threads): the state row, 3xTF32 split (+ the bias input = 1)
+        float xf[DM];
+#pragma unroll
+        for (int k = 0; k < DM; ++k) xf[k] = __double2float_rn(xn[k]);
+        auto in = [&](int k) { return k < DM && k < D ? xf[k < DM ? k : 0] : (k == D ? 1.f : 0.f); };
+        if (lower) {
+#pragma unroll
+            for (int kg = 0; kg < TC_K / 4; ++kg) {
+                float4 h, l;
+                h.x = tc::to_tf32(in(4 * kg + 0));
+                h.y = tc::to_tf32(in(4 * kg + 1));
+                h.z = tc::to_tf32(in(4 * kg + 2));
+                h.w = tc::to_tf32(in(4 * kg + 3));
+                l.x = tc::to_tf32(__fsub_rn(in(4 * kg + 0), h.x));
+                l.y = tc::to_tf32(__fsub_rn(in(4 * kg + 1), h.y));
+                l.z = tc::to_tf32(__fsub_rn(in(4 * kg + 2), h.z));
+                l.w = tc::to_tf32(__fsub_rn(in(4 * kg + 3), h.w));
+                *reinterpret_cast<float4*>(Ah + umma_off(r, 4 * kg)) = h;
+                *reinterpret_cast<float4*>(Al + umma_off(r, 4 * kg)) = l;
+            }
+        }
+        tc::fence_proxy_async_smem();
+        tc::fence_before_sync();  // the previous tile's TMEM loads are complete
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int s = 0; s < TC_K / 8; ++s) {  // K-step s reads K-groups 2s, 2s + 1
+                const uint64_t ah = tc::smem_desc(Ah + s * 64, 128, 512), al = tc::smem_desc(Al + s * 64, 128, 512);
+                const uint64_t bh = tc::smem_desc(B1h + s * 64, 128, 512), bl = tc::smem_desc(B1l + s * 64, 128, 512);
+                tc::mma_tf32(tmem, ah, bh, idesc, s > 0);
+                tc::mma_tf32(tmem, ah, bl, idesc, true);
+                tc::mma_tf32(tmem, al, bh, idesc, true);
+            }
+            tc::mma_commit(&bars[1]);
+        }
+        load_row(tile + gridDim.x, xn);  // overlaps the MMAs and the epilogue
+        tc::mbar_wait(&bars[1], phase);
+        phase ^= 1u;
+        tc::fence_after_sync();
+
+        // ---- epilogue: lower threads take chunks [0, c_mid), upper [c_mid, nch) of the
+        // same state; the TMEM load of the next chunk is in flight while one is consumed
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int m = 0; m < M; ++m) a[s][m] = make_float2(0.f, 0.f);
+        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+        const int c0 = lower ? 0 : c_mid, c1 = lower ? c_mid : nch;
+        if (c0 < c1) {
+            float v0[32], v1[32];
+            tc::tmem_ld32_issue(lane_addr + (uint32_t)(c0 * 32), v0);
+            tc::tmem_ld_wait(v0);
+            for (int c = c0; c < c1; c += 2) {
+                if (c + 1 < c1) tc::tmem_ld32_issue(lane_addr + (uint32_t)((c + 1) * 32), v1);
+                consume(v0, c);
+                if (c + 1 < c1) {
+                    tc::tmem_ld_wait(v1);
+                    if (c + 2 < c1) tc::tmem_ld32_issue(lane_addr + (uint32_t)((c + 2) * 32), v0);
+                    consume(v1, c + 1);
+                    if (c + 2 < c1) tc::tmem_ld_wait(v0);
+                }
+            }
+        }
+        if (!lower) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+#pragma unroll
+                for (int m = 0; m < M; ++m) part[(s * TC_MP + m) * TC_ROWS + r] = a[s][m];
+        }
+        __syncthreads();
+        if (lower) {
+            float q[M];
+            int best = 0;
+            float bv = 0.f, sv = -INFINITY;
+            bool fin = true;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                float2 t[4];
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const float2 u = part[(s * TC_MP + m) * TC_ROWS + r];
+                    t[s] = make_float2(__fadd_rn(a[s][m].x, u.x), __fadd_rn(a[s][m].y, u.y));
+                }
+                const float t0 = __fadd_rn(__fadd_rn(t[0].x, t[0].y), __fadd_rn(t[1].x, t[1].y));
+                const float t1 = __fadd_rn(__fadd_rn(t[2].x, t[2].y), __fadd_rn(t[3].x, t[3].y));
+                q[m] = __fadd_rn(__fadd_rn(t0, t1), fb2[m]);
+                fin = fin && isfinite(q[m]);
+                if (m == 0 || q[m] > bv) {
+                    sv = bv;
+                    best = m;
+                    bv = q[m];
+                } else if (q[m] > sv) {
+                    sv = q[m];
+                }
+                if (m == 0) sv = -INFINITY;
+            }
+            float Bd = C[D];
+#pragma unroll
+            for (int k = 0; k < DM; ++k)
+                if (k < D) Bd = __fmaf_ru(fabsf(xf[k]), C[k], Bd);
+            // the bound is against exact arithmetic on the fp32-rounded inputs; the fp64
+            // inputs differ by <= u |x|, covered by the slack in K
+            const bool sure =
+                M == 1 || (fin && isfinite(Bd) && __dsub_rd((double)bv, (double)sv) > 2.0 * (double)Bd);
+            if (valid) {
+                ++n_rows;
+                if (!sure) {
+                    ++n_fb;
+                    flist[atomicAdd(fcount, 1)] = row;
+                } else {
+                    if (p.eps > 0.0) {
+                        P4 rn = philox4x32_10(p.counter, (uint64_t)row, p.seed);
+                        if (u01(rn.x[0], rn.x[1]) < p.eps) best = (int)below(rn.x[2], (uint32_t)M);
+                    }
+                    if (p.q_out) {
+#pragma unroll
+                        for (int m = 0; m < M; ++m) p.q_out[(size_t)row * M + m] = q[m];
+                    }
+                    p.a_out[row] = (uint8_t)best;
+                }
+            }
+        }
+        // the deferred list can take one more full tile?  else drain it now
+        __syncthreads();
+        const int nf = *fcount;
+        if (nf > TC_FLIST - TC_ROWS) {
+            fallback(nf);
+            __syncthreads();
+            if (tid == 0) *fcount = 0;
+        }
+    }
+    __syncthreads();
+    fallback(*fcount);
+    if (p.stats) {
+        const unsigned s0 = __reduce_add_sync(0xffffffffu, n_rows);
+        const unsigned s1 = __reduce_add_sync(0xffffffffu, n_fb);
+        if (lane == 0) {
+            atomicAdd(&p.stats[0], (unsigned long long)s0);
+            atomicAdd(&p.stats[1], (unsigned long long)s1);
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tmem, (uint32_t)p.ncols);
+}
+
+bool route_tc_supported(int T, int M, int H) {
+    const int D = T + M + 1;
+    return M >= 1 && M <= TC_MP && D + 1 <= TC_K && H >= 32 && H <= 256 && H % 32 == 0;
+}
+
+size_t route_tc_workspace_bytes(int H) { return (size_t)TcLayout{H}.bytes(); }
+
+static size_t route_tc_smem(int H) {
+    const size_t img = ((size_t)TcLayout{H}.bytes() + 1023) & ~size_t(1023);
+    const size_t need = img + 2 * sizeof(float) * TC_ROWS * TC_K + sizeof(float2) * 4 * TC_MP * TC_ROWS + 2 * 8 +
+                        4 + 4 + 4 * TC_FLIST;
+    // at most two CTAs per SM: each owns up to 256 of the SM's 512 TMEM columns
+    return need > 80 * 1024 ? need : 80 * 1024;
+}
+
+template <int M>
+static int launch_route_tc_m(const be_qweights* W, int T, const double* x, int B, double eps, uint64_t seed,
+                             uint64_t counter, float* q_out, uint8_t* a_out, void* workspace,
+                             unsigned long long* stats, cudaStream_t st) {
+    const int D = T + M + 1, H = W->hidden;
+    float* img = reinterpret_cast<float*>(workspace);
+    route_tc_pack_kernel<M><<<8, 256, 0, st>>>(W->w1, W->b1, W->w2, W->b2, D, H, img);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "route_tc pack launch");
+    if (B == 0) return BE_OK;
+    RouteTcParams p{};
+    p.w1 = W->w1;
+    p.b1 = W->b1;
+    p.w2 = W->w2;
+    p.b2 = W->b2;
+    p.img = img;
+    p.D = D;
+    p.H = H;
+    p.B = B;
+    p.ncols = H <= 32 ? 32 : H <= 64 ? 64 : H <= 128 ? 128 : 256;
+    p.x = x;
+    p.eps = eps;
+    p.seed = seed;
+    p.counter = counter;
+    p.q_out = q_out;
+    p.a_out = a_out;
+    p.stats = stats;
+    const size_t smem = route_tc_smem(H);
+    auto kern = D <= 8 ? route_tc_kernel<M, 8> : route_tc_kernel<M, TC_K - 1>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_cuda_error(e, "route_tc smem attribute");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ntiles = (B + TC_ROWS - 1) / TC_ROWS;
+    const int blocks = ntiles < 2 * sms ? ntiles : 2 * sms;
+    kern<<<blocks, TC_THREADS, smem, st>>>(p);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "route_tc launch");
+}
+
+int launch_route_tc(const be_qweights* W, int T, int M, const double* x, int B, double eps, uint64_t seed,
+                    uint64_t counter, float* q_out, uint8_t* a_out, void* workspace, int64_t* stats,
+                    cudaStream_t st) {
+    auto* s = reinterpret_cast<unsigned long long*>(stats);
+    switch (M) {
+        case 1: return launch_route_tc_m<1>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
+        case 2: return launch_route_tc_m<2>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
+        case 3: return launch_route_tc_m<3>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
+        case 4: return launch_route_tc_m<4>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
+        default: return set_error(BE_EINVAL, "route_tc: n_tiers must be <= 4");
+    }
+}
+
+}  // namespace be

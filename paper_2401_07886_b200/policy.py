@@ -3,6 +3,8 @@
   encode           policy.py:52-65
   QNetwork.forward policy.py:111-118   -> be_qnet_route_f64 (fp64, warp per state)
   select_action    policy.py:125-132   -> same kernel, Philox epsilon draw
+  route_tc         the batched router on the tensor cores (be_qnet_route_tc): same
+                   actions, fp32 Q values
 """
 from __future__ import annotations
 
@@ -61,6 +63,59 @@ def route(net, x: torch.Tensor, epsilon: float = 0.0, seed: int = 0, counter: in
                                    int(seed) & (2**64 - 1), int(counter) & (2**64 - 1),
                                    _lib.ptr(q), a.data_ptr(), _lib.stream_ptr()))
     return q, a
+
+
+class TensorCoreRouter:
+    """Batched select_action on the tensor cores (be_qnet_route_tc, route_tc.cu).
+
+    Layer 1 runs as tcgen05 kind::tf32 MMAs (3xTF32 split, 128 states per tile,
+    accumulators in TMEM); every greedy decision is certified by an error bound
+    or re-evaluated with the fp64 router's exact arithmetic, so the actions
+    equal `route()`'s; Q values are fp32 (within 1e-5 relative).  Owns the
+    packed-weight workspace and a (states, fp64 re-evaluations) counter."""
+
+    def __init__(self, net, device=None):
+        self.net = DeviceQNet.of(net, device)
+        dn = self.net
+        L = _lib.load()
+        if not L.be_qnet_route_tc_supported(dn.n_tasks, dn.n_tiers, dn.hidden):
+            raise _lib.InvalidParameterError(
+                "tensor-core router needs n_tiers <= 4, n_tasks + n_tiers + 2 <= 16, hidden % 32 == 0 <= 256")
+        dev = dn.w1.device
+        nbytes = int(L.be_qnet_route_tc_workspace_bytes(dn.hidden))
+        self.workspace = torch.empty((nbytes + 15) // 16 * 4, dtype=torch.float32, device=dev)
+        self.stats = torch.zeros(2, dtype=torch.int64, device=dev)
+
+    def __call__(self, x: torch.Tensor, epsilon: float = 0.0, seed: int = 0, counter: int = 0,
+                 want_q: bool = True, out: "torch.Tensor | None" = None, check: bool = True):
+        dn = self.net
+        x = x.to(dtype=torch.float64).contiguous()
+        if x.dim() != 2 or x.shape[1] != dn.n_tasks + dn.n_tiers + 1:
+            raise ValueError(f"expected input dim {dn.n_tasks + dn.n_tiers + 1}")
+        if check and not bool(torch.isfinite(x).all()):
+            raise ValueError("non-finite network input")  # policy.py:115-116
+        B = x.shape[0]
+        q = torch.empty((B, dn.n_tiers), dtype=torch.float32, device=x.device) if want_q else None
+        a = out if out is not None else torch.empty(B, dtype=torch.uint8, device=x.device)
+        w = dn.weights()
+        L = _lib.load()
+        _lib.check(L.be_qnet_route_tc(w, dn.n_tasks, dn.n_tiers, x.data_ptr(), B, float(epsilon),
+                                      int(seed) & (2**64 - 1), int(counter) & (2**64 - 1), _lib.ptr(q),
+                                      a.data_ptr(), self.workspace.data_ptr(), self.stats.data_ptr(),
+                                      _lib.stream_ptr()))
+        return q, a
+
+    def fallback_stats(self, reset: bool = False) -> tuple:
+        s = self.stats.tolist()
+        if reset:
+            self.stats.zero_()
+        return int(s[0]), int(s[1])
+
+
+def route_tc(net, x: torch.Tensor, epsilon: float = 0.0, seed: int = 0, counter: int = 0,
+             want_q: bool = True):
+    """Batched select_action on the tensor cores: (q fp32 [B, M], action u8 [B])."""
+    return TensorCoreRouter(net, x.device)(x, epsilon, seed, counter, want_q)
 
 
 def q_forward_batch(net, x) -> np.ndarray:
