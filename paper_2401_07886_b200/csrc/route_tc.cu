@@ -44,7 +44,7 @@ struct TcLayout {  // byte offsets inside the packed image (= the shared-memory 
     int H;
     __host__ __device__ int b1h() const { return 0; }
     __host__ __device__ int b1l() const { return H * TC_K * 4; }
-    __host__ __device__ int w2p() const { return 2 * H * TC_K * 4; }         // [H/2][TC_MP] float2
+    __host__ __device__ int w2p() const { return 2 * H * TC_K * 4; }         // [H/4][4] float4
     __host__ __device__ int b2() const { return w2p() + (H / 2) * TC_MP * 8; }  // [TC_MP] float
     __host__ __device__ int bound() const { return b2() + TC_MP * 4; }         // [TC_K] float
     __host__ __device__ int bytes() const { return bound() + TC_K * 4; }       // multiple of 16
@@ -77,12 +77,21 @@ __global__ void __launch_bounds__(256) route_tc_pack_kernel(const double* w1, co
         b1h[umma_off(n, k)] = hi;
         b1l[umma_off(n, k)] = tc::to_tf32(__fsub_rn(f, hi));
     }
-    float2* w2p = reinterpret_cast<float2*>(img + L.w2p() / 4);
-    for (int e = tid; e < (H / 2) * TC_MP; e += nt) {
-        const int jp = e / TC_MP, m = e % TC_MP;
-        w2p[e] = m < M ? make_float2(__double2float_rn(w2[(size_t)(2 * jp) * M + m]),
-                                     __double2float_rn(w2[(size_t)(2 * jp + 1) * M + m]))
-                       : make_float2(0.f, 0.f);
+    // W2 in groups of four hidden units j..j+3 (two FFMA2 pairs), four float4 each:
+    // (w[j][0], w[j+1][0], w[j][1], w[j+1][1]), the same for j+2, j+3, then
+    // (w[j..j+3][2]) and (w[j..j+3][3]) — M = 3 needs 3 loads per 4 units, not 4
+    float* w2q = img + L.w2p() / 4;
+    for (int e = tid; e < (H / 4) * 16; e += nt) {
+        const int g = e / 16, f = e % 16, v = f / 4, c = f % 4;
+        int j, m;
+        if (v < 2) {
+            j = 4 * g + 2 * v + (c & 1);
+            m = c >> 1;
+        } else {
+            j = 4 * g + c;
+            m = v;
+        }
+        w2q[e] = m < M ? __double2float_rn(w2[(size_t)j * M + m]) : 0.f;
     }
     float* fb2 = img + L.b2() / 4;
     for (int m = tid; m < TC_MP; m += nt) fb2[m] = m < M ? __double2float_rn(b2[m]) : 0.f;
@@ -164,7 +173,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
 
     const float* B1h = img + L.b1h() / 4;
     const float* B1l = img + L.b1l() / 4;
-    const float2* W2p = reinterpret_cast<const float2*>(img + L.w2p() / 4);
+    const float4* W2q = reinterpret_cast<const float4*>(img + L.w2p() / 4);
     const float* fb2 = img + L.b2() / 4;
     const float* C = img + L.bound() / 4;
     const uint32_t idesc = tc::idesc_tf32(TC_ROWS, H);
@@ -197,16 +206,26 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     float2 a[4][M];
     auto consume = [&](const float(&u)[32], int c) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const float2 h = make_float2(fmaxf(u[2 * i], 0.f), fmaxf(u[2 * i + 1], 0.f));
-            const float4* wp = reinterpret_cast<const float4*>(W2p + (size_t)(c * 16 + i) * TC_MP);
-            const float4 w01 = wp[0];
-            a[i & 3][0] = ffma2(h, make_float2(w01.x, w01.y), a[i & 3][0]);
-            if (M > 1) a[i & 3][M > 1 ? 1 : 0] = ffma2(h, make_float2(w01.z, w01.w), a[i & 3][M > 1 ? 1 : 0]);
+        for (int i = 0; i < 16; i += 2) {
+            const float2 h0 = make_float2(fmaxf(u[2 * i], 0.f), fmaxf(u[2 * i + 1], 0.f));
+            const float2 h1 = make_float2(fmaxf(u[2 * i + 2], 0.f), fmaxf(u[2 * i + 3], 0.f));
+            const float4* g = W2q + (size_t)(c * 8 + i / 2) * 4;
+            const float4 g0 = g[0], g1 = g[1];
+            a[i & 3][0] = ffma2(h0, make_float2(g0.x, g0.y), a[i & 3][0]);
+            a[(i + 1) & 3][0] = ffma2(h1, make_float2(g1.x, g1.y), a[(i + 1) & 3][0]);
+            if (M > 1) {
+                a[i & 3][M > 1 ? 1 : 0] = ffma2(h0, make_float2(g0.z, g0.w), a[i & 3][M > 1 ? 1 : 0]);
+                a[(i + 1) & 3][M > 1 ? 1 : 0] = ffma2(h1, make_float2(g1.z, g1.w), a[(i + 1) & 3][M > 1 ? 1 : 0]);
+            }
             if (M > 2) {
-                const float4 w23 = wp[1];
-                a[i & 3][M > 2 ? 2 : 0] = ffma2(h, make_float2(w23.x, w23.y), a[i & 3][M > 2 ? 2 : 0]);
-                if (M > 3) a[i & 3][M > 3 ? 3 : 0] = ffma2(h, make_float2(w23.z, w23.w), a[i & 3][M > 3 ? 3 : 0]);
+                const float4 g2 = g[2];
+                a[i & 3][M > 2 ? 2 : 0] = ffma2(h0, make_float2(g2.x, g2.y), a[i & 3][M > 2 ? 2 : 0]);
+                a[(i + 1) & 3][M > 2 ? 2 : 0] = ffma2(h1, make_float2(g2.z, g2.w), a[(i + 1) & 3][M > 2 ? 2 : 0]);
+            }
+            if (M > 3) {
+                const float4 g3 = g[3];
+                a[i & 3][M > 3 ? 3 : 0] = ffma2(h0, make_float2(g3.x, g3.y), a[i & 3][M > 3 ? 3 : 0]);
+                a[(i + 1) & 3][M > 3 ? 3 : 0] = ffma2(h1, make_float2(g3.z, g3.w), a[(i + 1) & 3][M > 3 ? 3 : 0]);
             }
         }
     };
