@@ -213,6 +213,56 @@ def training_probe(dev, world):
 
 
 
+def router_probe(dev):
+    """The batched router (north star: Q-network forward + argmax over the whole
+    environment batch) on 4,194,304 encoded states of the trained policy: the
+    tensor-core router (be_qnet_route_tc) beside the fp64 router; device time,
+    inputs resident.  Reported beside the headline (not part of `value`)."""
+    import torch
+    from paper_2401_07886_b200 import TensorCoreRouter, load_checkpoint, route
+    B, reps = 1 << 22, 10
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.zeros((B, N_TASKS + 4), dtype=torch.float64, device=dev)
+    x[torch.arange(B, device=dev), torch.randint(0, N_TASKS, (B,), device=dev, generator=g)] = 1.0
+    for m, sc in enumerate((128.0, 32.0, 8.0)):
+        x[:, N_TASKS + m] = torch.randint(0, int(2 * sc), (B,), device=dev, generator=g).double() / sc
+    x[:, -1] = torch.rand(B, device=dev, generator=g, dtype=torch.float64) * (30.0 / 48.0)
+    net = load_checkpoint(POLICY)
+    tc = TensorCoreRouter(net, dev)
+    a_tc = torch.empty(B, dtype=torch.uint8, device=dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize(dev)
+        return s.elapsed_time(e) / reps
+
+    ms64 = timed(lambda: route(net, x, want_q=False))
+    ms_tc = timed(lambda: tc(x, want_q=False, out=a_tc, check=False))
+    tc.fallback_stats(reset=True)
+    _, a1 = tc(x, want_q=False)
+    n, fb = tc.fallback_stats()
+    _, a0 = route(net, x, want_q=False)
+    out = dict(states=B, tc_states_per_s=B / ms_tc * 1e3, fp64_states_per_s=B / ms64 * 1e3,
+               tc_ms=ms_tc, fp64_ms=ms64, fp64_reevaluated_frac=fb / max(n, 1),
+               actions_identical_to_fp64=bool(torch.equal(a0, a1)),
+               kernel="route_tc_kernel<3, 8>: tcgen05.mma.kind::tf32 (3xTF32) layer 1, FFMA2 layer 2, "
+                      "certified decisions + fp64 re-evaluation")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        k = json.load(open(prof)).get("kernels", {}).get("route_tc")
+        if k:
+            out["tensor_pipe_pct"] = k.get("tensor_pipe_pct")
+            out["issue_active_pct"] = k.get("issue_active_pct")
+            out["ncu_source"] = k.get("source")
+    return out
+
+
 class ClockSampler:
     def __init__(self, index):
         self.index = index
@@ -391,6 +441,7 @@ def main():
     red_gbs = ALG_BYTES_REDUCE * E * N / (red_ms / 1e3) / 1e9
 
     train = None if a.no_training else training_probe(dev, world)
+    router = None if a.no_training else router_probe(dev)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -423,7 +474,7 @@ def main():
                                   frac=red_gbs / hbm_peak, ms=red_ms,
                                   algorithmic_bytes_per_request=ALG_BYTES_REDUCE),
             kernel_ms=dict(rollout=r_ms, reduce=red_ms),
-            issue_roofline=issue, training=train,
+            issue_roofline=issue, training=train, router=router,
             q_screen=dict(decisions=n_screened, fp64_fallbacks=n_fallback,
                           fallback_frac=n_fallback / max(n_screened, 1),
                           note="certified fp32 decision screen (FFMA2) with exact fp64 fallback; "

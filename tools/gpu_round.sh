@@ -22,4 +22,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:roll
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:reduce_kernel -s 1 -c 1 \
     -o gpurun_out/prof_reduce_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-training \
     > /dev/null 2> gpurun_out/prof_reduce_$tag.err
+timeout 300 python tools/probe_route.py > gpurun_out/route_$tag.json 2> gpurun_out/route_$tag.err
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:route_tc_kernel -s 1 -c 1 \
+    -o gpurun_out/prof_route_tc_$tag -f python tools/probe_route.py 4194304 2 > /dev/null 2> gpurun_out/prof_route_tc_$tag.err
 ls -la gpurun_out

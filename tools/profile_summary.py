@@ -20,7 +20,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 import ncu_summary  # noqa: E402
 
-KERNELS = {"rollout": ("rollout.o", "rollout_kernelILi3ELi16"), "reduce": ("reduce.o", "reduce_kernelILi5")}
+KERNELS = {"rollout": ("rollout.o", "rollout_kernelILi3ELi16"), "reduce": ("reduce.o", "reduce_kernelILi5"),
+           "route_tc": ("route_tc.o", "route_tc_kernelILi3ELi8")}
 
 
 def metric(d, k):
@@ -47,6 +48,8 @@ def main():
             return None if v is None else float(v[0].replace(",", "")) * unit.get(v[1], 1.0)
         rd, wr = nbytes("dram__bytes_read.sum"), nbytes("dram__bytes_write.sum")
         t_ms = metric(d, "gpu__time_duration.sum")
+        if t_ms is not None and d["gpu__time_duration.sum"][1] == "us":
+            t_ms *= 1e-3
         summ["kernels"][name] = dict(
             tag=tag, kernel=d["kernel"], envs=envs, requests=reqs, time_ms=t_ms,
             dram_read_bytes=rd, dram_write_bytes=wr, dram_bytes=(rd or 0) + (wr or 0),
