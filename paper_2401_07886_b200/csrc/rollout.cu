@@ -52,6 +52,7 @@ struct RolloutParams {
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
     unsigned long long* screen_stats;  // [2] decisions screened, fp64 fallbacks (nullable)
+    int32_t pack_obs;    // 1: per-tier queue sums fit 10-bit fields (observe with one REDUX)
     const double* qpack;  // screen on: the fp64 fallback's packed weights (QLayout) in global
                           // memory (L1/L2-resident), so shared memory holds only the screen
 };
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(256, BE_ROLLOUT_MINB) rollout_kernel(const Rol
         }
         const double U = __shfl_sync(FULL, pf_arr, g0 + sub);
         int task = __shfl_sync(FULL, pf_task, g0 + sub);
-        const int ftier = __shfl_sync(FULL, pf_forced, g0 + sub);
+        const int ftier = p.forced ? __shfl_sync(FULL, pf_forced, g0 + sub) : 0;
         if (!live) task = 0;  // keep idle groups' shared-memory reads in range
         double rate = 0.0;
         if (live) {
@@ -198,9 +199,17 @@ __global__ void __launch_bounds__(256, BE_ROLLOUT_MINB) rollout_kernel(const Rol
             rate = true_rate ? cur_rate : estimator_observe(est, U, false, cur_rate, p.cfg.prior_rate);
         }
         int obs[M];
+        if (M <= 3 && p.pack_obs) {
+            // one REDUX per group: tier m's replica counts in bits [10m, 10m + 10) (the host
+            // checked replicas x ring capacity < 1024 for every tier, so no field overflows)
+            const unsigned s = group_sum<LPE>(live && active_lane ? (unsigned)r.count << (10 * tc.tier) : 0u, grp);
 #pragma unroll
-        for (int m = 0; m < M; ++m)
-            obs[m] = (int)group_sum<LPE>((live && tc.tier == m) ? (unsigned)r.count : 0u, grp);
+            for (int m = 0; m < M; ++m) obs[m] = (int)((s >> (10 * m)) & 1023u);
+        } else {
+#pragma unroll
+            for (int m = 0; m < M; ++m)
+                obs[m] = (int)group_sum<LPE>((live && tc.tier == m) ? (unsigned)r.count : 0u, grp);
+        }
         int tier;
         if (p.forced) {
             tier = ftier;
@@ -250,8 +259,9 @@ __global__ void __launch_bounds__(256, BE_ROLLOUT_MINB) rollout_kernel(const Rol
             ++i;
         }
         // ---- group bookkeeping: failure or end of trace -> drain, next env
-        const bool gfail = (__ballot_sync(FULL, live && (!ok || bad)) & gmask) != 0;
-        const bool gbad = (__ballot_sync(FULL, live && bad) & gmask) != 0;
+        const unsigned fb = __ballot_sync(FULL, live && (!ok || bad));
+        const bool gfail = (fb & gmask) != 0;
+        const bool gbad = fb != 0 && (__ballot_sync(FULL, live && bad) & gmask) != 0;  // fb: warp-uniform
         if (!dead && (gfail || i >= n)) {
             if (!gfail && active_lane) ok &= advance_lane(r, tc, INF, ring, mask, sc, out);
             const bool drain_fail = (__ballot_sync(gmask, !ok) & gmask) != 0;
@@ -352,6 +362,12 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
                rollout_smem_bytes(T, M, p.H, true, 0, true) <= 200 * 1024;
     p.screen_stats = p.screen ? env->d_screen : nullptr;
     p.qpack = env->d_qpack;
+    {
+        int ok_pack = M <= 3;
+        for (int m = 0; m < M; ++m)
+            if ((long long)env->cfg.tiers[m].replicas << env->cap_log2 >= 1024) ok_pack = 0;
+        p.pack_obs = ok_pack;
+    }
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
     // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)

@@ -350,6 +350,11 @@ class StreamingEvaluator:
         self._k = 0
         self.h2d_bytes = 0
         self.d2h_bytes = 0
+        # pinned host buffers for the statistics, allocated up front (pinned allocation
+        # synchronises the device): up to `max_outstanding` submits may await result()
+        self._stat_pool = []
+        self._stat_shapes = None
+        self.max_outstanding = 8
 
     def _device_buf(self, slot: int, host: TraceBatch) -> TraceBatch:
         b = self._bufs[slot]
@@ -383,11 +388,7 @@ class StreamingEvaluator:
             o = self.ro.launch(dev, self.net, self.static_tier, stream=ks)
             red = reduce_eval(dev, o.flags, o.reward, self.thresholds, self.n_buckets, stream=ks)
             self._freed[slot].record(ks)
-            host_stats = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-                          for k, v in (("win_counts", red.win_counts), ("n_windows", red.n_windows),
-                                       ("bucket_miss", red.bucket_miss),
-                                       ("bucket_req", red.bucket_req),
-                                       ("bucket_reward", red.bucket_reward))}
+            host_stats = self._stats_buffer(red)
             for k, t in host_stats.items():
                 t.copy_(getattr(red, k), non_blocking=True)
             done = torch.cuda.Event()
@@ -396,12 +397,26 @@ class StreamingEvaluator:
         self._k += 1
         return done, host_stats
 
+    _STATS = ("win_counts", "n_windows", "bucket_miss", "bucket_req", "bucket_reward")
+
+    def _stats_buffer(self, red) -> dict:
+        shapes = tuple((tuple(getattr(red, k).shape), getattr(red, k).dtype) for k in self._STATS)
+        if shapes != self._stat_shapes:
+            self._stat_shapes = shapes
+            self._stat_pool = [{k: torch.empty(sh, dtype=dt, pin_memory=True)
+                                for k, (sh, dt) in zip(self._STATS, shapes)}
+                               for _ in range(self.max_outstanding)]
+        if not self._stat_pool:
+            raise RuntimeError(f"more than {self.max_outstanding} submits await result()")
+        return self._stat_pool.pop()
+
     def result(self, handle) -> ReduceResult:
         done, hs = handle
         done.synchronize()
         self.ro.env.check(self.compute_stream)
-        return ReduceResult(self.thresholds, hs["win_counts"], hs["n_windows"], hs["bucket_miss"],
-                            hs["bucket_req"], hs["bucket_reward"])
+        out = ReduceResult(self.thresholds, *(hs[k].clone() for k in self._STATS))
+        self._stat_pool.append(hs)
+        return out
 
 
 def pin_trace(tb: TraceBatch) -> TraceBatch:

@@ -275,3 +275,12 @@ def test_screen_falls_back_on_exact_ties(cuda):
                                  batch_scales=m["enc"]["batch_scales"],
                                  estimator_mode=m["estimator_mode"], reset=m["reset"])
     assert np.array_equal(res[0][0], ref["tier"])
+
+
+@pytest.mark.parametrize("name", ["unpredictable-1_trained", "stable_mixed1", "hellaswag-copa-soft_mixed0"])
+def test_wide_rings_use_unpacked_observe(cuda, name):
+    """Ring capacity 1024 x 4 replicas per tier exceeds the 10-bit packed observe
+    fields, so the kernel sums each tier with its own REDUX: same results."""
+    g = goldens.load(name)
+    o, _ = gpu_run(g, ring_capacity=1024)
+    assert_env_equal(o, 0, g)

@@ -1,0 +1,41 @@
+"""End-to-end StreamingEvaluator (pinned host traces -> copy stream -> fused
+rollout + reducer -> pinned statistics) against the device-resident path."""
+import os
+
+import pytest
+import torch
+
+import goldens
+from paper_2401_07886_b200 import (GreedyRollout, RewardSpec, StateEncoding, TraceBatch,
+                                   default_tiers, load_checkpoint, reduce_eval)
+from paper_2401_07886_b200.evalkit import StreamingEvaluator, pin_trace
+
+pytestmark = pytest.mark.gpu
+
+
+def test_streaming_matches_device_path(cuda):
+    E, N, K = 512, 2000, 10
+    tiers, rw = default_tiers(), RewardSpec.default()
+    enc = StateEncoding(4, tuple(float(t.max_batch) for t in tiers))
+    net = load_checkpoint(os.path.join(goldens.GOLDEN, "trained_seed7.beqn"))
+    batches = []
+    for seed in (3, 4, 5):
+        rates = [3.0 * (1 + (e % K)) for e in range(E)]
+        batches.append(TraceBatch.generate_stable(rates, N, 4, seed, device=cuda,
+                                                  buckets=[e % K for e in range(E)]))
+    ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False)
+    want = []
+    for tb in batches:
+        o = ro.run(tb, net)
+        want.append(reduce_eval(tb, o.flags, o.reward, n_buckets=K).totals())
+    se = StreamingEvaluator(net, tiers, rw, E, N, enc, estimator_mode="true-rate", n_buckets=K,
+                            ring_capacity=ro.ring_capacity, device=cuda)
+    hosts = [pin_trace(tb) for tb in batches]
+    for rnd in range(3):  # several outstanding submits, buffers and stat slots recycled
+        handles = [se.submit(h) for h in hosts]
+        got = [se.result(h).totals() for h in handles]
+        for g, w in zip(got, want):
+            assert g.keys() == w.keys()
+            for k in w:
+                assert str(g[k]) == str(w[k]), (rnd, k)
+    assert se.h2d_bytes > E * N * 9 and se.d2h_bytes > 0

@@ -108,9 +108,9 @@ def config3():
                       log_every=5000, seed=11)
     run_training(default_tiers(), RewardSpec.default(),
                  TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=50,
-                             log_every=50, seed=11), n_envs=4096)
+                             log_every=50, seed=11), n_envs=4096, mode="graph")
     t = {}
-    res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=4096, timing=t)
+    res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=4096, timing=t, mode="graph")
     s = t["loop_ms"] / 1e3
     return dict(iterations_per_s=5000 / s, updates_per_s=res.updates / s, env_steps_per_s=4096 * 5000 / s,
                 final_loss=res.log[-1].loss, transitions=res.transitions)
