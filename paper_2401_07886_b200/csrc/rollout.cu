@@ -20,6 +20,12 @@
 #ifndef BE_ROLLOUT_MINB
 #define BE_ROLLOUT_MINB 2  // resident CTAs per SM the register allocation is capped for
 #endif
+#ifndef BE_ROLLOUT_THREADS
+#define BE_ROLLOUT_THREADS 256
+#endif
+#ifndef BE_SKIP_SMEM_MAX
+#define BE_SKIP_SMEM_MAX (100 * 1024)  // stage the skip table if the CTA's shared memory stays below
+#endif
 
 namespace be {
 
@@ -79,7 +85,7 @@ __device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
 }
 
 template <int M, int LPE>
-__global__ void __launch_bounds__(256, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
+__global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
@@ -297,7 +303,7 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     }
-    const int threads = 256;
+    const int threads = BE_ROLLOUT_THREADS;
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (e != cudaSuccess) return set_cuda_error(e, "occupancy");
@@ -371,7 +377,7 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
     // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
-    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <= 100 * 1024;
+    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <= BE_SKIP_SMEM_MAX;
     size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0, p.screen);
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
