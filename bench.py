@@ -464,7 +464,7 @@ def main():
                         envs_per_gpu=E, requests_per_env=N, total_envs=world * E,
                         parallelism=f"env-sharded dp{world}", l2="inputs larger than L2 (5.9 GB traces/GPU)",
                         step="fused rollout kernel + evaluation reducer"),
-            gpu_launches=2 * a.steps,
+            gpu_launches=3 * a.steps,  # per step: stage_qpack_kernel, rollout_kernel, reduce_kernel
             roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
                           frac=achieved / hbm_peak, traffic=traffic, peak_source=peak_src,
                           kernel="rollout_kernel<3>", algorithmic_bytes_per_env_step=ALG_BYTES_STEP,
