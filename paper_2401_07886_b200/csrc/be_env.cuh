@@ -612,6 +612,23 @@ __device__ __forceinline__ bool qnet_screen(const float* __restrict__ sf, int T,
     return M == 1 || (fin && isfinite(B) && __dsub_rd((double)bv, (double)sv) > 2.0 * (double)B);
 }
 
+// Sum / min over the lanes of this lane's group (REDUX over the warp with the
+// other group masked out; all 32 lanes must call).
+template <int LPE>
+__device__ __forceinline__ unsigned group_sum(unsigned v, int grp) {
+    if (LPE == 32) return __reduce_add_sync(FULL, v);
+    const unsigned s0 = __reduce_add_sync(FULL, grp == 0 ? v : 0u);
+    const unsigned s1 = __reduce_add_sync(FULL, grp == 1 ? v : 0u);
+    return grp ? s1 : s0;
+}
+template <int LPE>
+__device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
+    if (LPE == 32) return __reduce_min_sync(FULL, v);
+    const unsigned s0 = __reduce_min_sync(FULL, grp == 0 ? v : 0xffffffffu);
+    const unsigned s1 = __reduce_min_sync(FULL, grp == 1 ? v : 0xffffffffu);
+    return grp ? s1 : s0;
+}
+
 // np.argmax semantics: first NaN if any, else first maximum.
 template <int M>
 __device__ __forceinline__ int argmax_first(const double (&q)[M]) {

@@ -13,6 +13,7 @@
 // sums and the replica argmin are REDUX ops.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 #include "be_env.cuh"
 #include "be_internal.h"
@@ -67,23 +68,6 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code, int env)
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
 }
 
-// Sum / min over the lanes of this lane's group (REDUX over the warp with the
-// other group masked out; all 32 lanes must call).
-template <int LPE>
-__device__ __forceinline__ unsigned group_sum(unsigned v, int grp) {
-    if (LPE == 32) return __reduce_add_sync(FULL, v);
-    const unsigned s0 = __reduce_add_sync(FULL, grp == 0 ? v : 0u);
-    const unsigned s1 = __reduce_add_sync(FULL, grp == 1 ? v : 0u);
-    return grp ? s1 : s0;
-}
-template <int LPE>
-__device__ __forceinline__ unsigned group_min(unsigned v, int grp) {
-    if (LPE == 32) return __reduce_min_sync(FULL, v);
-    const unsigned s0 = __reduce_min_sync(FULL, grp == 0 ? v : 0xffffffffu);
-    const unsigned s1 = __reduce_min_sync(FULL, grp == 1 ? v : 0xffffffffu);
-    return grp ? s1 : s0;
-}
-
 template <int M, int LPE>
 __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -132,7 +116,10 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
     // per-group ("group-uniform") env state
     int env = -1;
     bool need = true, dead = false;
-    int64_t base = 0, n = 0, i = 0, seg = 0, seg_end = 0, next_seg = INT64_MAX;
+    // request indices are 32-bit (ld <= 2^24, checked at the API); segment CSR offsets 64-bit
+    int64_t base = 0, seg = 0, seg_end = 0;
+    int n = 0, i = 0, next_seg = INT_MAX;
+    auto seg_mark = [&](int64_t k) { return k < seg_end ? (int)min(p.seg_start[k], (int64_t)INT_MAX) : INT_MAX; };
     double cur_rate = 0.0;
     Slot* ring = p.rings;
     Rep r;
@@ -156,11 +143,11 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
             } else {
                 env = got;
                 base = (int64_t)env * p.ld;
-                n = p.n_events ? p.n_events[env] : p.ld;
+                n = (int)(p.n_events ? p.n_events[env] : p.ld);
                 i = 0;
                 seg = p.seg_off[env];
                 seg_end = p.seg_off[env + 1];
-                next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
+                next_seg = seg_mark(seg);
                 cur_rate = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
                 ring = p.rings + ((size_t)env * p.R + (active_lane ? gl : 0)) * ((size_t)mask + 1);
                 rep_reset(r);
@@ -177,7 +164,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
         // ---- one request for every live group (evalkit.py:185-205)
         const int sub = (int)(i & (LPE - 1));
         if (live && sub == 0) {  // coalesced LPE-request prefetch
-            const int64_t ii = i + gl;
+            const int ii = i + gl;
             if (ii < n) {
                 pf_arr = __ldg(p.arrival + base + ii);
                 pf_task = __ldg(p.task + base + ii);
@@ -198,7 +185,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
                 }
                 cur_rate = p.seg_rate[seg];
                 ++seg;
-                next_seg = seg < seg_end ? p.seg_start[seg] : INT64_MAX;
+                next_seg = seg_mark(seg);
             }
             if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out);
             // true-rate mode never reads the arrival window (workload.py:241-242)

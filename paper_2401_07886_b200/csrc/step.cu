@@ -90,11 +90,13 @@ __device__ __forceinline__ double epsilon_at(int64_t it, double start, double en
     return __dadd_rn(start, __dmul_rn(__dsub_rn(end, start), frac));
 }
 
-template <int M>
-__device__ __forceinline__ void step_env(const StepParams& p, int e, const Score& sc, const double* sw,
+template <int M, int LPE>
+__device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
                                          bool policy, int T, int H, int D);
 
-template <int M>
+// LPE lanes per env: 16 (two envs per warp) when the cluster has <= 16 replicas and
+// the encoded state fits 16 lanes, else 32
+template <int M, int LPE>
 __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
@@ -105,21 +107,29 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     __syncthreads();
     // persistent grid (one wave): the weights are staged once per CTA, then every
     // warp steps envs warp_id, warp_id + n_warps, ...
+    constexpr int G = 32 / LPE;  // envs per warp
     const int n_warps = (gridDim.x * blockDim.x) >> 5;
-    for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < p.E; e += n_warps)
-        step_env<M>(p, e, sc, p.qpack, policy, T, H, D);
+    const int grp = (threadIdx.x & 31) / LPE;
+    for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w * G < p.E; w += n_warps) {
+        const int e = w * G + grp;
+        step_env<M, LPE>(p, e < p.E ? e : p.E - 1, e < p.E, sc, p.qpack, policy, T, H, D);
+    }
 }
 
-template <int M>
-__device__ __forceinline__ void step_env(const StepParams& p, int e, const Score& sc, const double* sw,
+// One env per LPE-lane group (all 32 lanes of the warp call it: the group
+// reductions are warp-wide); `live` = false for a padding group past the last env.
+template <int M, int LPE>
+__device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
                                          bool policy, int T, int H, int D) {
     const int lane = threadIdx.x & 31;
-    const TierC tc = lane_tier(p.cfg, lane, p.skip);  // skip table read through L1
-    const bool al = tc.tier >= 0;
+    const int gl = lane & (LPE - 1), grp = LPE == 32 ? 0 : lane / LPE;
+    const unsigned gmask = LPE == 32 ? FULL : (0xffffu << (grp * LPE));
+    const TierC tc = lane_tier(p.cfg, gl, p.skip);  // skip table read through L1
+    const bool al = live && tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
-    Slot* ring = p.rings + ((size_t)e * p.R + (al ? lane : 0)) * ((size_t)mask + 1);
+    Slot* ring = p.rings + ((size_t)e * p.R + (al ? gl : 0)) * ((size_t)mask + 1);
     Rep r;
-    if (al) r = reps_of(p.state, e, p.R)[lane];
+    if (al) r = reps_of(p.state, e, p.R)[gl];
     else rep_reset(r);
     EnvState* es = state_of(p.state, e, p.E, p.R);
     // records are indexed by request id modulo rec_ld (a ring for long runs)
@@ -128,13 +138,13 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, const Score
     bool ok = true;
     if (p.drain) {
         if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out);
-        if (al) reps_of(p.state, e, p.R)[lane] = r;
-        const bool all_ok = __all_sync(FULL, ok);
-        if (!all_ok && lane == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
+        if (al) reps_of(p.state, e, p.R)[gl] = r;
+        const bool all_ok = (__ballot_sync(FULL, !ok) & gmask) == 0;
+        if (live && !all_ok && gl == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
         return;
     }
     const double U = p.arrival[e];
-    const int task = p.task[e];
+    const int task = live ? p.task[e] : 0;
     if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out);
     Estimator est;
 #pragma unroll
@@ -145,7 +155,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, const Score
     const double rate = estimator_observe(est, U, p.cfg.estimator_true_rate != 0, cur, p.cfg.prior_rate);
     int obs[M];
 #pragma unroll
-    for (int m = 0; m < M; ++m) obs[m] = (int)__reduce_add_sync(FULL, (tc.tier == m) ? (unsigned)r.count : 0u);
+    for (int m = 0; m < M; ++m) obs[m] = (int)group_sum<LPE>((al && tc.tier == m) ? (unsigned)r.count : 0u, grp);
     double xt[M], q[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) {
@@ -175,13 +185,13 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, const Score
                 tier = (int)below(rnd.x[2], (uint32_t)M);
             }
         }
-        qnet_group<M, 32>(sw, T, H, task, xt, xr, q);
+        qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
         if (!explore) tier = argmax_first<M>(q);
     }
-    if (lane < M) {
+    if (live && gl < M) {
 #pragma unroll
         for (int m = 0; m < M; ++m) {
-            if (lane == m) {
+            if (gl == m) {
                 if (p.obs_out) p.obs_out[(size_t)e * M + m] = obs[m];
                 if (p.q_out) p.q_out[(size_t)e * M + m] = q[m];
             }
@@ -194,26 +204,26 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, const Score
         if (x_out) x_out += slot * (size_t)p.E * D;
         if (action_out) action_out += slot * (size_t)p.E;
     }
-    if (x_out && lane < D) {
+    if (live && x_out && gl < D) {
         // encode (policy.py:52-65): [onehot(task), obs/scale, rate/rate_scale]
         double v = 0.0;
-        if (lane < T) v = lane == task ? 1.0 : 0.0;
+        if (gl < T) v = gl == task ? 1.0 : 0.0;
 #pragma unroll
         for (int m = 0; m < M; ++m)
-            if (lane == T + m) v = xt[m];
-        if (lane == T + M) v = xr;
-        x_out[(size_t)e * D + lane] = v;
+            if (gl == T + m) v = xt[m];
+        if (gl == T + M) v = xr;
+        x_out[(size_t)e * D + gl] = v;
     }
-    unsigned key = (tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)lane) : 0xffffffffu;
-    unsigned best = __reduce_min_sync(FULL, key);
+    unsigned key = (al && tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)gl) : 0xffffffffu;
+    unsigned best = group_min<LPE>(key, grp);
     bool bad = best == 0xffffffffu;
-    if (!bad && (int)(best & 31u) == lane) {
+    if (live && !bad && (int)(best & 31u) == gl) {
         uint32_t rid = (uint32_t)(id % p.rec_ld);
         p.rec.flags[(int64_t)e * p.rec_ld + rid] = 0;  // record slot now "in flight"
         ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
     }
-    if (al) reps_of(p.state, e, p.R)[lane] = r;
-    if (lane == 0) {
+    if (al) reps_of(p.state, e, p.R)[gl] = r;
+    if (live && gl == 0) {
         if (p.rate_out) p.rate_out[e] = rate;
         if (action_out) action_out[e] = (uint8_t)tier;
 #pragma unroll
@@ -221,8 +231,8 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, const Score
         es->n = est.n;
         es->next_id = id + 1;
     }
-    const bool all_ok = __all_sync(FULL, ok);
-    if (lane == 0 && (bad || !all_ok)) {
+    const bool all_ok = (__ballot_sync(FULL, !ok) & gmask) == 0;
+    if (live && gl == 0 && (bad || !all_ok)) {
         if (atomicCAS(&p.status[0], 0, bad ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
     }
 }
@@ -237,7 +247,8 @@ int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st) {
 
 template <int M>
 static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
-    auto kern = env_step_kernel<M>;
+    const bool two = p.R <= 16 && p.cfg.n_tasks + M + 1 <= 16;
+    auto kern = two ? env_step_kernel<M, 16> : env_step_kernel<M, 32>;
     if (p.qpack) {  // pack the (possibly just updated) weights for this step
         stage_qpack_kernel<M><<<QPACK_CTAS, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
                                                           const_cast<double*>(p.qpack));
@@ -249,7 +260,8 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
     }
     int threads = 256;
-    long long blocks = ((long long)p.E * 32 + threads - 1) / threads;
+    const long long warps = two ? ((long long)p.E + 1) / 2 : (long long)p.E;
+    long long blocks = (warps * 32 + threads - 1) / threads;
     int per_sm = 0, dev = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
