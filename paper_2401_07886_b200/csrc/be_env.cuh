@@ -76,11 +76,15 @@ struct Score {
 
 
 
+// This env's record rows (element id at [id]): row pointers are formed once per
+// env so every completion indexes with the 24-bit request id alone.
 struct RecOut {
     uint8_t* flags;
     double* reward;
-    double* realized;
-    int64_t base;  // e * ld
+    double* realized;  // nullable
+    __device__ __forceinline__ static RecOut row(const be_records& rec, int64_t base) {
+        return RecOut{rec.flags + base, rec.reward + base, rec.realized ? rec.realized + base : nullptr};
+    }
 };
 
 __device__ __forceinline__ void load_score(Score& s, const be_cfg& c, const ScoreAux& aux) {
@@ -137,14 +141,14 @@ __device__ __forceinline__ TierC lane_tier(const be_cfg& c, int lane, const doub
 __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Score& sc,
                                          const RecOut& o, double t_end) {
     int task = (int)(r.h_idtask >> 24);
-    int64_t id = (int64_t)(r.h_idtask & 0xffffffu);
+    const uint32_t id = r.h_idtask & 0xffffffu;
     const double span = __dsub_rn(t_end, r.h_arr);
     if (!sc.soft[task] && !o.realized) {
         // hard deadline, realized not requested: weight_hard (reward.py:94-96) via the
         // exact division-free threshold
         const bool hit = span <= sc.hit_tau[task * BE_MAX_TIERS + tc.tier];
-        o.reward[o.base + id] = hit ? sc.matrix[task * BE_MAX_TIERS + tc.tier] : 0.0;
-        o.flags[o.base + id] = (uint8_t)(tc.tier | 0x40 | (hit ? 0 : 0x80));
+        o.reward[id] = hit ? sc.matrix[task * BE_MAX_TIERS + tc.tier] : 0.0;
+        o.flags[id] = (uint8_t)(tc.tier | 0x40 | (hit ? 0 : 0x80));
         return;
     }
     double realized = __ddiv_rn(span, (double)tc.tokens);
@@ -166,9 +170,9 @@ __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Sc
     double reward = __dmul_rn(w, sc.matrix[task * BE_MAX_TIERS + tc.tier]);
     // flags: tier (bits 0-5) | completed (0x40) | deadline miss (0x80)
     uint8_t flag = (uint8_t)(tc.tier | 0x40 | ((realized > dl) ? 0x80 : 0));
-    o.reward[o.base + id] = reward;
-    o.flags[o.base + id] = flag;
-    if (o.realized) o.realized[o.base + id] = realized;
+    o.reward[id] = reward;
+    o.flags[id] = flag;
+    if (o.realized) o.realized[id] = realized;
 }
 
 // ---------------------------------------------------------------------------

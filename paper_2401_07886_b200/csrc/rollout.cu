@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
     bool need = true, dead = false;
     // request indices are 32-bit (ld <= 2^24, checked at the API); segment CSR offsets 64-bit
     int64_t base = 0, seg = 0, seg_end = 0;
+
     int n = 0, i = 0, next_seg = INT_MAX;
     auto seg_mark = [&](int64_t k) { return k < seg_end ? (int)min(p.seg_start[k], (int64_t)INT_MAX) : INT_MAX; };
     double cur_rate = 0.0;
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
             } else {
                 env = got;
                 base = (int64_t)env * p.ld;
+
                 n = (int)(p.n_events ? p.n_events[env] : p.ld);
                 i = 0;
                 seg = p.seg_off[env];
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
         }
         if (__all_sync(FULL, dead)) break;
         const bool live = !dead && i < n;
-        RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, base};
+        const RecOut out = RecOut::row(p.rec, base);
 
         // ---- one request for every live group (evalkit.py:185-205)
         const int sub = (int)(i & (LPE - 1));

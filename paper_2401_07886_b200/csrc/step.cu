@@ -134,7 +134,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     EnvState* es = state_of(p.state, e, p.E, p.R);
     // records are indexed by request id modulo rec_ld (a ring for long runs)
     // complete() writes at base + id; id is the 24-bit slot id.
-    RecOut out{p.rec.flags, p.rec.reward, p.rec.realized, (int64_t)e * p.rec_ld};
+    const RecOut out = RecOut::row(p.rec, (int64_t)e * p.rec_ld);
     bool ok = true;
     if (p.drain) {
         if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out);
