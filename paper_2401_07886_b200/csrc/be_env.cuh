@@ -393,6 +393,8 @@ __device__ __forceinline__ void stage_qnet(const double* __restrict__ w1, const 
 template <int M>
 __global__ void __launch_bounds__(256) stage_qpack_kernel(const double* w1, const double* b1, const double* w2,
                                                           const double* b2, int T, int H, double* out) {
+    pdl_trigger();
+    pdl_wait();  // the weights may have been updated by the previous kernel
     stage_qnet<M>(w1, b1, w2, b2, T, H, out, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 constexpr int QPACK_CTAS = 16;

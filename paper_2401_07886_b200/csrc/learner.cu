@@ -37,6 +37,8 @@ __global__ void train_workload_kernel(int E, double* state, double log_lo, doubl
                                       int equal_time, double mean_seconds, double mean_requests,
                                       int n_tasks, uint64_t seed, uint64_t step, double* arrival,
                                       uint8_t* task, double* rate_out, const int64_t* step_dev) {
+    pdl_trigger();  // the next kernel of the stream may be scheduled now
+    pdl_wait();     // the previous one has completed and its writes are visible
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     if (step_dev) step = (uint64_t)*step_dev;  // be_train_iteration: iteration index on device
@@ -154,6 +156,8 @@ __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane
 }
 
 __global__ void __launch_bounds__(CENVS * 32) commit_fused_kernel(const CommitParams p) {
+    pdl_trigger();  // the next kernel of the stream may be scheduled now
+    pdl_wait();     // the previous one has completed and its writes are visible
     __shared__ int vb_sh, cnt[CENVS];
     __shared__ long long wpre[CENVS];
     __shared__ long long excl_sh, cursor_sh;
@@ -382,6 +386,8 @@ struct UpdateParams {
 };
 
 __global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdateParams u) {
+    pdl_trigger();  // the next kernel of the stream may be scheduled now
+    pdl_wait();     // the previous one has completed and its writes are visible
     const ApplyParams& p = u.ap;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int k = blockIdx.x * 32 + lane;
@@ -437,6 +443,8 @@ __global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdatePa
 
 template <int DM>
 __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
+    pdl_trigger();  // the next kernel of the stream may be scheduled now
+    pdl_wait();     // the previous one has completed and its writes are visible
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
     double* xs = lsm;                    // [LROWS][D]
@@ -724,10 +732,9 @@ int32_t be_learner_workload(be_learner* L, uint64_t seed, int64_t step, double* 
     const be_learner_cfg& c = L->cfg;
     if (!(c.rate_low > 0) || c.rate_high < c.rate_low) return set_error(BE_EINVAL, "need 0 < rate_low <= rate_high");
     const int E = c.n_envs;
-    train_workload_kernel<<<(E + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+    cudaError_t e = launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream,
         E, L->wl_state, log(c.rate_low), log(c.rate_high), c.regime_equal_time, c.regime_mean_seconds,
         c.regime_mean_requests, c.n_tasks, seed, (uint64_t)step, arrival_ms, task, true_rate, nullptr);
-    cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "workload launch");
 }
 
@@ -753,8 +760,7 @@ static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cud
     p.status = L->status;
     p.scan = L->scan;
     p.ticket = L->ticket;
-    commit_fused_kernel<<<(p.E + CENVS - 1) / CENVS, CENVS * 32, 0, st>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(commit_fused_kernel, dim3((p.E + CENVS - 1) / CENVS), dim3(CENVS * 32), 0, st, p);
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "commit launch");
 }
 
@@ -777,8 +783,7 @@ static int launch_update(be_learner* L, int reduce, int apply, ApplyParams ap, c
     ap.gate = gate;
     u.ap = ap;
     const int blocks = (reduce || apply) ? (L->nparam + 32) / 32 : 1;  // 32 parameters (+ the loss) per CTA
-    learner_update_kernel<<<blocks, UTHREADS, 0, st>>>(u);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(learner_update_kernel, dim3(blocks), dim3(UTHREADS), 0, st, u);
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner update launch");
 }
 
@@ -898,7 +903,7 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
     const int64_t* gate = c->use_gate ? L->gate : nullptr;
     if (c->phase == 0 || c->phase == 3) {
         // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156)
-        train_workload_kernel<<<(E + 255) / 256, 256, 0, st>>>(
+        launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, st,
             E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
             cf.regime_mean_seconds, cf.regime_mean_requests, cf.n_tasks, c->workload_seed, 0,
             L->it_arrival, L->it_task, L->it_rate, it);

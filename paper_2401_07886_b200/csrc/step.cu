@@ -98,6 +98,8 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
 // the encoded state fits 16 lanes, else 32
 template <int M, int LPE>
 __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
+    pdl_trigger();  // the next kernel of the stream may be scheduled now
+    pdl_wait();     // the previous one has completed and its writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     const int T = p.cfg.n_tasks;
@@ -250,9 +252,8 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
     const bool two = p.R <= 16 && p.cfg.n_tasks + M + 1 <= 16;
     auto kern = two ? env_step_kernel<M, 16> : env_step_kernel<M, 32>;
     if (p.qpack) {  // pack the (possibly just updated) weights for this step
-        stage_qpack_kernel<M><<<QPACK_CTAS, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
-                                                          const_cast<double*>(p.qpack));
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(stage_qpack_kernel<M>, dim3(QPACK_CTAS), dim3(256), 0, st, p.w1, p.b1, p.w2, p.b2,
+                                   p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack));
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
     }
     if (smem > 48 * 1024) {
@@ -268,8 +269,7 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm < 1) per_sm = 1;
     if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
-    kern<<<(unsigned)blocks, threads, smem, st>>>(p);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(kern, dim3((unsigned)blocks), dim3(threads), smem, st, p);
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step launch");
 }
 
