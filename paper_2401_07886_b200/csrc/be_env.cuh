@@ -49,6 +49,7 @@ struct Rep {
     int n_running;   // FIFO prefix that has joined an iteration
     int h_join;
     uint32_t h_idtask;
+    int n_assigned;  // FIFO prefix whose join iteration is known (<= max_batch; see submit_lane)
 };
 
 struct TierC {
@@ -236,9 +237,12 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
             int n_active = min(r.count, tc.max_batch);
             if (r.n_running < n_active) {  // newly admitted requests join (simcore.py:143-145)
                 if (r.n_running == 0) r.h_join = r.iters;
-                for (int k = max(r.n_running, 1); k < n_active; ++k)
+                // requests admitted straight into `active` got their join at submit; only
+                // those admitted from the queue at the last END still need it
+                for (int k = max(max(r.n_running, r.n_assigned), 1); k < n_active; ++k)
                     ring[(r.head + (uint32_t)k) & mask].join = r.iters;
                 r.n_running = n_active;
+                r.n_assigned = max(r.n_assigned, n_active);
             }
             double c = __dmul_rn(tc.beta, (double)n_active);
             if (tc.skip) {
@@ -263,6 +267,7 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
                 r.head++;
                 r.count--;
                 r.n_running--;
+                r.n_assigned--;  // >= n_running >= 1 before the pop
                 if (r.count > 0) {
                     Slot s = ring[r.head & mask];
                     r.h_arr = s.arrival;
@@ -282,17 +287,25 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
 __device__ __forceinline__ bool submit_lane(Rep& r, const TierC& tc, double clock, uint32_t idtask,
                                             Slot* ring, uint32_t mask) {
     if ((uint32_t)r.count > mask) return false;
+    // A request that enters `active` directly (len(active) < max_batch, simcore.py:101-104)
+    // joins the running batch at the next START: now if the replica is idle or a START
+    // is pending, after the pending END otherwise (END increments the iteration counter
+    // first).  Recording it here saves the START-time write for the common case; a
+    // queued request gets its join when a later START admits it.
+    const bool direct = r.count < tc.max_batch;
+    const int join = direct ? r.iters + (r.kind == K_END ? 1 : 0) : -1;
     if (r.count == 0) {
         r.h_arr = clock;
         r.h_idtask = idtask;
-        r.h_join = -1;
+        r.h_join = join;
     } else {
         Slot s;
         s.arrival = clock;
         s.idtask = idtask;
-        s.join = -1;
+        s.join = join;
         ring[(r.head + (uint32_t)r.count) & mask] = s;
     }
+    if (direct && r.n_assigned == r.count) r.n_assigned++;
     r.count++;
     if (r.kind == K_NONE) {  // idle replica: START at the current clock
         r.kind = K_START;
@@ -310,6 +323,7 @@ __device__ __forceinline__ void rep_reset(Rep& r) {
     r.n_running = 0;
     r.h_join = -1;
     r.h_idtask = 0;
+    r.n_assigned = 0;
 }
 
 // Rate estimator (workload.py:212-255), warp-uniform.
