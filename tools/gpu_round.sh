@@ -26,3 +26,4 @@ timeout 300 python tools/probe_route.py > gpurun_out/route_$tag.json 2> gpurun_o
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:route_tc_kernel -s 1 -c 1 \
     -o gpurun_out/prof_route_tc_$tag -f python tools/probe_route.py 4194304 2 > /dev/null 2> gpurun_out/prof_route_tc_$tag.err
 ls -la gpurun_out
+timeout 1200 python tools/configs_bench.py > gpurun_out/configs_$tag.log 2>&1 && cp gpurun_out/configs.json gpurun_out/configs_$tag.json
