@@ -265,7 +265,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     as "device": readiness is all-reduced so every rank updates in the same
     iterations, and the collectives stay outside any graph).
     `timing`: optional dict, receives the device time of the iteration loop
-    ("loop_ms", CUDA events on the launching stream; setup excluded)."""
+    ("loop_ms", CUDA events on the launching stream; setup and the one-time graph
+    capture excluded, intermediate log rows included, the final one excluded)."""
     n_tasks, n_tiers = len(reward_spec.tasks), len(reward_spec.matrix[0])
     if len(tiers) != n_tiers:
         raise ValueError("tier count must match reward matrix width")
@@ -313,7 +314,7 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         size = learner.size
         k = min(size, 1000)
         cur = int(learner.ring_state[0])
-        idx = [(cur - 1 - j) % cfg.buffer_capacity for j in range(k)]
+        idx = (cur - 1 - torch.arange(k, device=learner.ring_rewards.device)) % cfg.buffer_capacity
         mean_recent = float(learner.ring_rewards[idx].mean()) if k else math.nan
         gs = int(learner.counters[1])
         loss = float(learner.loss[1]) if gs > 0 else math.nan
@@ -365,27 +366,36 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         graph = None
         if mode == "graph":
             G = graph_chunk or max(d for d in range(1, 65) if log_every % d == 0)
+            if G > 1 and total >= G:
+                # capture (host-side, like compiling) before the timed loop starts: the
+                # graph records G iterations, each replay runs them on the device
+                graph = torch.cuda.CUDAGraph()
+                side = torch.cuda.Stream(device=dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.graph(graph, stream=side):
+                    for _ in range(G):
+                        iteration()
+                torch.cuda.current_stream(dev).wait_stream(side)
+        t_begin = torch.cuda.Event(enable_timing=True)
+        t_begin.record()
         it = 0
         while it < total:
             seg_end = min(total, (it // log_every + 1) * log_every)
-            if mode == "graph" and G > 1:
+            if graph is not None:
                 while seg_end - it >= G:
-                    if graph is None:
-                        graph = torch.cuda.CUDAGraph()
-                        side = torch.cuda.Stream(device=dev)
-                        side.wait_stream(torch.cuda.current_stream(dev))
-                        with torch.cuda.graph(graph, stream=side):
-                            for _ in range(G):
-                                iteration()
                     graph.replay()
                     it += G
             while it < seg_end:
                 iteration()
                 it += 1
+            if it == total:  # device work of the loop ends here (the last log row is host-side)
+                t_end = torch.cuda.Event(enable_timing=True)
+                t_end.record()
             if it % log_every == 0:
                 log_row(it - 1)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_end.record()
+    if total == 0 or mode == "host":
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_end.record()
     learner.check()
     env.check()
     if timing is not None:
