@@ -339,6 +339,22 @@ int32_t be_learner_backward_batch(be_learner* learner, const double* states,
 int32_t be_learner_apply(be_learner* learner, int32_t explicit_batch, void* stream);
 int32_t be_learner_check(be_learner* learner, void* stream);
 
+/* Data-parallel learner without a collective library (be_train_iteration
+ * phase 4): every rank's update kernel publishes its tile-reduced gradients in
+ * an exchange buffer, waits for every rank's publication of the same update
+ * (release/acquire at system scope over NVLink peer memory, bounded wait), sums
+ * all ranks' gradients in rank order, scales by 1/W and applies Adam — the
+ * replicas stay bit-identical and no NCCL launch sits on the update path.
+ *   be_learner_exchange_buffer: this learner's exchange allocation (device);
+ *   be_learner_ipc_handle:      its cudaIpcMemHandle_t (64 bytes) for other processes;
+ *   be_learner_set_peers:       the device pointers (valid in this process) of every
+ *                               rank's exchange allocation, xmems[rank] = own;
+ *   be_learner_open_peers_ipc:  the same from world x 64-byte IPC handles. */
+int32_t be_learner_exchange_buffer(be_learner* learner, void** xmem, size_t* bytes);
+int32_t be_learner_ipc_handle(be_learner* learner, void* handle_out);
+int32_t be_learner_set_peers(be_learner* learner, int32_t world, int32_t rank, const uint64_t* xmems);
+int32_t be_learner_open_peers_ipc(be_learner* learner, int32_t world, int32_t rank, const void* handles);
+
 /* One iteration of run_training's loop (trainer.py:374-401) for all E envs,
  * with EVERY per-iteration value read from device memory — the iteration index
  * `it` (views.counters[3]), epsilon_at(it) (trainer.py:85-90), the Philox
@@ -347,8 +363,10 @@ int32_t be_learner_check(be_learner* learner, void* stream);
  *   pending slot it % P) -> commit(it) -> update(s) -> it += 1.
  * Bit-identical to driving be_learner_workload / be_env_step / be_learner_commit
  * / be_learner_backward / be_learner_apply from the host with the same seeds.
- * phase 0: whole iteration; each update is ONE fused kernel (Double-Q targets,
- *          Huber backward, tile reduction and Adam in the last CTA to finish).
+ * phase 0: whole iteration; each update = the row-tile kernel (Double-Q targets,
+ *          Huber backward) + one tile-reduction/Adam kernel.
+ * phase 4: whole iteration with the peer-memory gradient exchange (data-parallel,
+ *          be_learner_set_peers first): no host round trip, graph-capturable.
  * phase 3: the env part only (workload, env step, commits);
  * phase 1: the gradients of update `update_index` into views.grad — all-reduce
  *          them here (DP learner);

@@ -155,6 +155,10 @@ SIGNATURES = {
     "be_learner_apply": (_I32, [_P, _I32, _P]),
     "be_learner_check": (_I32, [_P, _P]),
     "be_train_iteration": (_I32, [_P, _P, ctypes.POINTER(BeTrainIterCfg), _P]),
+    "be_learner_exchange_buffer": (_I32, [_P, ctypes.POINTER(_P), ctypes.POINTER(_SZ)]),
+    "be_learner_ipc_handle": (_I32, [_P, _P]),
+    "be_learner_set_peers": (_I32, [_P, _I32, _I32, _P]),
+    "be_learner_open_peers_ipc": (_I32, [_P, _I32, _I32, _P]),
 }
 
 _lib = None

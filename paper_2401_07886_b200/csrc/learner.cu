@@ -19,6 +19,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
+#include <stdio.h>
 
 #include "be200.h"
 #include "be_internal.h"
@@ -441,6 +442,133 @@ __global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdatePa
     }
 }
 
+// ------------------------------------------- data-parallel update over peer memory
+// The DP learner without a collective library: each rank's update kernel reduces
+// its own row tiles into an exchange buffer, publishes it with a release store of
+// the update's epoch, waits (acquire, system scope) until every rank published the
+// same epoch, then sums all ranks' gradients in rank order straight out of their
+// exchange buffers (NVLink peer memory, or the same GPU), scales by 1/W and applies
+// Adam — the same arithmetic as "all-reduce (sum) then x 1/W" for every rank, so
+// the replicas stay bit-identical, with no NCCL launch on the update path.
+// Readiness ("replay holds max(batch, warmup)") travels in the same buffer: the
+// update runs iff every rank is ready (the NCCL path's MIN all-reduce of the gate).
+// Exchange buffers are double-buffered by epoch parity: a rank can be at most one
+// epoch ahead of the slowest (it waits for everyone's flag), so it never overwrites
+// a buffer a peer may still be reading.
+constexpr int XMAX_RANKS = 16;
+constexpr unsigned long long XWAIT_NS = 2000000000ull;  // 2 s without a peer: fail loudly, never hang
+
+struct XParams {
+    int32_t world, rank;
+    double* xbuf_self;                            // [2][nparam + 2]
+    unsigned long long* flag_self;                // [1] last published epoch
+    const double* xbuf[XMAX_RANKS];               // every rank's exchange buffer (own included)
+    const unsigned long long* flag[XMAX_RANKS];
+    unsigned* done;                               // [2] CTA tickets (publish, finish)
+    int32_t* status;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateParams u, const XParams x) {
+    pdl_trigger();
+    pdl_wait();
+    const ApplyParams& p = u.ap;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int k = blockIdx.x * 32 + lane;
+    const int ld = p.nparam + 2;
+    // epoch of this update: counters[4] advances only in the last CTA of the finish ticket
+    const unsigned long long epoch = (unsigned long long)p.counters[4] + 1ull;
+    const int par = (int)(epoch & 1ull);
+    double* mine = x.xbuf_self + (size_t)par * ld;
+    const bool ready = !(p.sampling && p.ring_state[1] < p.min_size);  // local replay readiness
+    // ---- publish: this rank's tile sums (same fixed tree as learner_update_kernel)
+    __shared__ double slice[UTHREADS / 32][32];
+    __shared__ int all_ready;
+    if (ready) {
+        constexpr int NS = UTHREADS / 32;
+        const int per = (u.n_tiles + NS - 1) / NS;
+        const int t0 = warp * per, t1 = min(u.n_tiles, t0 + per);
+        double sum = 0.0;
+        if (k <= p.nparam) {
+            const double* src = u.partial + k;
+            const size_t pld = (size_t)p.nparam + 1;
+#pragma unroll 8
+            for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __ldcg(src + (size_t)t * pld));
+        }
+        slice[warp][lane] = sum;
+        __syncthreads();
+        if (warp == 0 && k <= p.nparam) {
+            double s = slice[0][lane];
+#pragma unroll
+            for (int w = 1; w < NS; ++w) s = __dadd_rn(s, slice[w][lane]);
+            mine[k] = s;  // k == nparam: the local loss sum
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) mine[p.nparam + 1] = ready ? 1.0 : 0.0;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&x.done[0], 1u) == gridDim.x - 1) {
+        x.done[0] = 0u;
+        __threadfence_system();
+        st_release_sys(x.flag_self, epoch);
+    }
+    // ---- wait for every rank's epoch (bounded: a missing peer is an error, not a hang)
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (int r = 0; r < x.world; ++r) {
+            while (ld_acquire_sys(x.flag[r]) < epoch) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (now - t0 > XWAIT_NS) {
+                    ok = 0;
+                    if (atomicCAS(&x.status[0], 0, BE_ECUDA) == 0) x.status[1] = r;
+                    break;
+                }
+                __nanosleep(64);
+            }
+        }
+        int rd = ok;
+        for (int r = 0; r < x.world && rd; ++r) rd = ld_relaxed_sys(x.xbuf[r] + (size_t)par * ld + p.nparam + 1) != 0.0;
+        all_ready = rd;
+    }
+    __syncthreads();
+    if (all_ready && warp == 0) {
+        if (k < p.nparam) {
+            double s = 0.0;
+            for (int r = 0; r < x.world; ++r) s = __dadd_rn(s, ld_relaxed_sys(x.xbuf[r] + (size_t)par * ld + k));
+            const double g = __dmul_rn(s, __ddiv_rn(1.0, (double)x.world));
+            p.grad[k] = g;
+            apply_elem(p, adam_coef(p), k, g);
+        } else if (k == p.nparam) {
+            *p.loss = __ddiv_rn(mine[k], (double)u.B);  // local loss, as the NCCL path logs it
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&x.done[1], 1u) == gridDim.x - 1) {
+        __threadfence();
+        if (all_ready) apply_finish(p);
+        if (p.advance) p.counters[3] += 1;
+        p.counters[4] = (long long)epoch;
+        x.done[1] = 0u;
+    }
+}
+
 template <int DM>
 __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
     pdl_trigger();  // the next kernel of the stream may be scheduled now
@@ -598,6 +726,12 @@ struct be_learner {
     unsigned* done;    // fused-update CTA arrival counter
     unsigned long long* scan;  // commit look-back state [(E + 7) / 8]
     unsigned* ticket;          // commit ticket / epoch
+    // peer exchange (phase 4): one allocation = [2][nparam + 2] doubles + the epoch flag
+    void* xmem;
+    int32_t x_world, x_rank;
+    const double* x_buf[XMAX_RANKS];
+    const unsigned long long* x_flag[XMAX_RANKS];
+    void* x_opened[XMAX_RANKS];  // peer allocations opened through CUDA IPC (closed at destroy)
     int64_t* gate;     // DP update gate (be_train_iteration use_gate)
 };
 
@@ -607,7 +741,17 @@ static void learner_free(be_learner* L) {
                     L->preward, L->low, L->status, L->wl_state,
                     L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket};
     for (void* p : ptrs) cudaFree(p);
+    for (int r = 0; r < XMAX_RANKS; ++r)
+        if (L->x_opened[r]) cudaIpcCloseMemHandle(L->x_opened[r]);
+    cudaFree(L->xmem);
     delete L;
+}
+
+static size_t xmem_bytes(const be_learner* L) { return (size_t)2 * (L->nparam + 2) * sizeof(double) + 64; }
+static double* x_buf_self(const be_learner* L) { return reinterpret_cast<double*>(L->xmem); }
+static unsigned long long* x_flag_self(const be_learner* L) {
+    return reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(L->xmem) +
+                                                 (size_t)2 * (L->nparam + 2) * sizeof(double));
 }
 
 extern "C" {
@@ -655,6 +799,12 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         }
         cudaMemset(*a.p, 0, a.n);
     }
+    e = cudaMalloc(&L->xmem, xmem_bytes(L));
+    if (e != cudaSuccess) {
+        learner_free(L);
+        return set_cuda_error(e, "be_learner_create: exchange buffer");
+    }
+    cudaMemset(L->xmem, 0, xmem_bytes(L));
     // configured here, not at launch time: launches may be captured in a CUDA graph
     cudaFuncSetAttribute(learner_partial_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(learner_partial_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -689,6 +839,7 @@ int32_t be_learner_set_params(be_learner* L, const double* w1, const double* b1,
     cudaMemsetAsync(L->m, 0, (size_t)L->nparam * 8, st);
     cudaMemsetAsync(L->v, 0, (size_t)L->nparam * 8, st);
     cudaMemsetAsync(L->counters, 0, 64, st);
+    cudaMemsetAsync(L->xmem, 0, xmem_bytes(L), st);  // peer-exchange epochs restart with the counters
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "set_params");
 }
@@ -787,12 +938,37 @@ static int launch_update(be_learner* L, int reduce, int apply, ApplyParams ap, c
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner update launch");
 }
 
+static int launch_xupdate(be_learner* L, int32_t advance, cudaStream_t st) {
+    UpdateParams u{};
+    u.n_tiles = L->n_tiles;
+    u.B = L->cfg.batch;
+    u.reduce = 1;
+    u.apply = 1;
+    u.partial = L->partial;
+    u.done = L->done;
+    u.ap = apply_params(L, 0, advance);
+    XParams x{};
+    x.world = L->x_world;
+    x.rank = L->x_rank;
+    x.xbuf_self = x_buf_self(L);
+    x.flag_self = x_flag_self(L);
+    for (int r = 0; r < L->x_world; ++r) {
+        x.xbuf[r] = L->x_buf[r];
+        x.flag[r] = L->x_flag[r];
+    }
+    x.done = L->done + 1;
+    x.status = L->status;
+    const int blocks = (L->nparam + 32) / 32;
+    cudaError_t e = launch_pdl(learner_xupdate_kernel, dim3(blocks), dim3(UTHREADS), 0, st, u, x);
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner peer-exchange update launch");
+}
+
 static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* a, const double* r,
                                  const double* s2, const double* c, int32_t B, uint64_t seed,
                                  uint64_t counter, int64_t* sample_idx, cudaStream_t st,
                                  const int64_t* iter_dev = nullptr, int32_t ups = 1, int32_t uidx = 0,
                                  int32_t fused = 0, int32_t advance = 0,
-                                 const int64_t* gate = nullptr) {
+                                 const int64_t* gate = nullptr, int32_t partials_only = 0) {
     const be_learner_cfg& cf = L->cfg;
     if (B != cf.batch) return set_error(BE_EINVAL, "batch size differs from the learner config");
     LearnParams p{};
@@ -837,6 +1013,7 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "learner launch");
+    if (partials_only) return BE_OK;
     return launch_update(L, 1, fused, apply_params(L, sampling ? 0 : 1, fused ? advance : 0), gate, st);
 }
 
@@ -886,13 +1063,71 @@ int32_t be_learner_apply(be_learner* L, int32_t explicit_batch, void* stream) {
     return launch_update(L, 0, 1, apply_params(L, explicit_batch, 0), nullptr, (cudaStream_t)stream);
 }
 
+int32_t be_learner_exchange_buffer(be_learner* L, void** xmem, size_t* bytes) {
+    if (!L || !xmem) return set_error(BE_EINVAL, "NULL argument");
+    *xmem = L->xmem;
+    if (bytes) *bytes = xmem_bytes(L);
+    return BE_OK;
+}
+
+int32_t be_learner_ipc_handle(be_learner* L, void* handle_out) {
+    if (!L || !handle_out) return set_error(BE_EINVAL, "NULL argument");
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, L->xmem);
+    if (e != cudaSuccess) return set_cuda_error(e, "be_learner_ipc_handle");
+    memcpy(handle_out, &h, sizeof(h));
+    return BE_OK;
+}
+
+int32_t be_learner_set_peers(be_learner* L, int32_t world, int32_t rank, const uint64_t* xmems) {
+    if (!L || !xmems) return set_error(BE_EINVAL, "NULL argument");
+    if (world < 1 || world > XMAX_RANKS || rank < 0 || rank >= world)
+        return set_error(BE_EINVAL, "world must be in [1, 16] and 0 <= rank < world");
+    if ((void*)(uintptr_t)xmems[rank] != L->xmem) return set_error(BE_EINVAL, "xmems[rank] is not this learner's buffer");
+    const size_t off = (size_t)2 * (L->nparam + 2) * sizeof(double);
+    for (int r = 0; r < world; ++r) {
+        if (!xmems[r]) return set_error(BE_EINVAL, "missing peer buffer");
+        L->x_buf[r] = reinterpret_cast<const double*>((uintptr_t)xmems[r]);
+        L->x_flag[r] = reinterpret_cast<const unsigned long long*>((uintptr_t)xmems[r] + off);
+    }
+    L->x_world = world;
+    L->x_rank = rank;
+    return BE_OK;
+}
+
+int32_t be_learner_open_peers_ipc(be_learner* L, int32_t world, int32_t rank, const void* handles) {
+    if (!L || !handles) return set_error(BE_EINVAL, "NULL argument");
+    if (world < 1 || world > XMAX_RANKS || rank < 0 || rank >= world)
+        return set_error(BE_EINVAL, "world must be in [1, 16] and 0 <= rank < world");
+    uint64_t ptrs[XMAX_RANKS] = {0};
+    for (int r = 0; r < world; ++r) {
+        if (r == rank) {
+            ptrs[r] = (uint64_t)(uintptr_t)L->xmem;
+            continue;
+        }
+        if (L->x_opened[r]) {
+            cudaIpcCloseMemHandle(L->x_opened[r]);
+            L->x_opened[r] = nullptr;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, reinterpret_cast<const char*>(handles) + (size_t)r * sizeof(h), sizeof(h));
+        void* ptr = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) return set_cuda_error(e, "be_learner_open_peers_ipc");
+        L->x_opened[r] = ptr;
+        ptrs[r] = (uint64_t)(uintptr_t)ptr;
+    }
+    return be_learner_set_peers(L, world, rank, ptrs);
+}
+
 int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* c, void* stream) {
     if (!L || !env || !c) return set_error(BE_EINVAL, "NULL argument");
     const be_learner_cfg& cf = L->cfg;
     cudaStream_t st = (cudaStream_t)stream;
     if (env->E != cf.n_envs || env->cfg.n_tiers != cf.n_tiers || env->cfg.n_tasks != cf.n_tasks)
         return set_error(BE_EINVAL, "env and learner shapes differ");
-    if (c->updates_per_step < 0 || c->phase < 0 || c->phase > 3 || c->update_index < 0 ||
+    if (c->phase == 4 && L->x_world < 1) return set_error(BE_EINVAL, "phase 4 needs be_learner_set_peers first");
+    if (c->updates_per_step < 0 || c->phase < 0 || c->phase > 4 || c->update_index < 0 ||
         ((c->phase == 1 || c->phase == 2) && c->update_index >= c->updates_per_step))
         return set_error(BE_EINVAL, "bad phase / update index");
     if (!(cf.rate_low > 0) || cf.rate_high < cf.rate_low)
@@ -901,7 +1136,7 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
     const int E = cf.n_envs, D = L->D, H = cf.hidden, M = cf.n_tiers;
     int rc;
     const int64_t* gate = c->use_gate ? L->gate : nullptr;
-    if (c->phase == 0 || c->phase == 3) {
+    if (c->phase == 0 || c->phase == 3 || c->phase == 4) {
         // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156)
         launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, st,
             E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
@@ -939,6 +1174,19 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                    c->sample_seed, 0, nullptr, st, it, ups, c->update_index, 0, 0,
                                    gate);
         if (rc) return rc;
+    } else if (c->phase == 4) {
+        // updates with the peer-memory gradient exchange (no collective library)
+        for (int u = 0; u < ups; ++u) {
+            rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch, c->sample_seed,
+                                       0, nullptr, st, it, ups, u, 0, 0, nullptr, /*partials_only=*/1);
+            if (rc) return rc;
+            rc = launch_xupdate(L, u == ups - 1, st);
+            if (rc) return rc;
+        }
+        if (ups == 0) {
+            rc = launch_update(L, 0, 0, apply_params(L, 1, 1), nullptr, st);
+            if (rc) return rc;
+        }
     } else if (c->phase == 2) {
         rc = launch_update(L, 0, 1, apply_params(L, 0, c->update_index == ups - 1), gate, st);
         if (rc) return rc;
@@ -955,6 +1203,11 @@ int32_t be_learner_check(be_learner* L, void* stream) {
     cudaMemcpy(st, L->status, sizeof(st), cudaMemcpyDeviceToHost);
     if (st[0] == 0) return BE_OK;
     cudaMemset(L->status, 0, 64);
+    if (st[0] == BE_ECUDA) {
+        char msg[160];
+        snprintf(msg, sizeof(msg), "peer gradient exchange: rank %d never published its update (timed out)", st[1]);
+        return set_error(BE_ECUDA, msg);
+    }
     return set_error(st[0], "pending-transition ring overflow: a request stayed in flight longer "
                             "than pending_capacity decisions; raise pending_capacity");
 }

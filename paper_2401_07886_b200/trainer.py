@@ -219,6 +219,27 @@ class DeviceLearner:
     def check(self) -> None:
         _lib.check(self._L.be_learner_check(self._h, _lib.stream_ptr()))
 
+    # ------------------------------------------------------------ peer exchange (DP)
+    def exchange_buffer(self) -> int:
+        p = ctypes.c_void_p()
+        _lib.check(self._L.be_learner_exchange_buffer(self._h, ctypes.byref(p), None))
+        return int(p.value)
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _lib.check(self._L.be_learner_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def set_peers(self, rank: int, xmems) -> None:
+        """In-process peers: every rank's exchange_buffer() (xmems[rank] = own)."""
+        arr = (ctypes.c_uint64 * len(xmems))(*[int(x) for x in xmems])
+        _lib.check(self._L.be_learner_set_peers(self._h, len(xmems), int(rank), arr))
+
+    def open_peers_ipc(self, rank: int, handles) -> None:
+        """Peers in other processes: every rank's ipc_handle(), in rank order."""
+        blob = b"".join(handles)
+        _lib.check(self._L.be_learner_open_peers_ipc(self._h, len(handles), int(rank), blob))
+
     @property
     def size(self) -> int:
         return int(self.ring_state[1])
@@ -244,7 +265,7 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                  completion_log=None, *, n_envs: int = 1, updates_per_step: int = 1,
                  pending_capacity: int = 4096, ring_capacity: int = 1024, device=None,
                  world=None, mode: str = "device", graph_chunk: int = 0,
-                 timing: Optional[dict] = None) -> TrainResult:
+                 timing: Optional[dict] = None, exchange: str = "nccl") -> TrainResult:
     """trainer.py:333-406 on the GPU for `n_envs` lockstep environments.
 
     Every iteration: TrainingWorkload arrivals (Philox), one env step with
@@ -264,6 +285,11 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     between backward and the optimizer step (data-parallel learner; always runs
     as "device": readiness is all-reduced so every rank updates in the same
     iterations, and the collectives stay outside any graph).
+    `exchange` (with `world`): "nccl" — gradients all-reduced by NCCL between the
+    backward and the optimizer launches (readiness all-reduced too); "peer" — one
+    update kernel per rank exchanges the gradients through the ranks' exchange
+    buffers in peer memory (CUDA IPC handles swapped once over `world`), no
+    collective on the update path, graph-capturable (be_train_iteration phase 4).
     `timing`: optional dict, receives the device time of the iteration loop
     ("loop_ms", CUDA events on the launching stream; setup and the one-time graph
     capture excluded, intermediate log rows included, the final one excluded)."""
@@ -272,6 +298,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         raise ValueError("tier count must match reward matrix width")
     if mode not in ("graph", "device", "host"):
         raise ValueError("mode must be 'graph', 'device' or 'host'")
+    if exchange not in ("nccl", "peer"):
+        raise ValueError("exchange must be 'nccl' or 'peer'")
     if encoding is None:
         encoding = StateEncoding(n_tasks=n_tasks, batch_scales=tuple(float(t.max_batch) for t in tiers))
     dev = _lib.require_cuda(device)
@@ -289,9 +317,18 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         import torch.distributed as dist
         dist.broadcast(learner.params, 0)
         dist.broadcast(learner.target, 0)
-        # the DP update gate (all ranks update in the same iterations) lives in the
-        # device-resident iteration; the collective stays outside any graph
-        mode = "device"
+        if exchange == "peer":
+            handles = [None] * dist.get_world_size()
+            dist.all_gather_object(handles, learner.ipc_handle())
+            learner.open_peers_ipc(dist.get_rank(), handles)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            if mode == "host":
+                mode = "device"
+        else:
+            # the DP update gate (all ranks update in the same iterations) lives in the
+            # device-resident iteration; the collective stays outside any graph
+            mode = "device"
     env = EnvBatch(tiers, reward_spec, E, encoding, estimator_mode=cfg.estimator_mode,
                    prior_rate=cfg.prior_rate, ring_capacity=ring_capacity, device=dev)
     # SeedSequence(seed).spawn(4) -> init, env, policy, sample (trainer.py:351-353); a
@@ -335,6 +372,11 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         gate_b = torch.empty(1, dtype=torch.bool, device=dev)
 
         def iteration():
+            if world is not None and exchange == "peer":
+                tic.phase, tic.update_index, tic.use_gate = 4, 0, 0
+                _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
+                                                         _lib.stream_ptr()))
+                return
             if world is None:
                 tic.phase, tic.update_index = 0, 0
                 _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),

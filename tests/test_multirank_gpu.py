@@ -3,6 +3,8 @@ ranks on one GPU, so these use the gloo backend with CUDA tensors — the
 collectives are the same torch.distributed calls the NCCL path makes):
   * data-parallel learner (run_training(world=...)): gradients all-reduced
     between backward and Adam -> replicas stay bit-identical, shards differ;
+  * the same learner with exchange="peer" (gradients read from the peers'
+    exchange buffers through CUDA IPC, no collective per update);
   * bench.py under torchrun with 2 ranks: env-sharded rollout, max-over-ranks
     timing, end-of-run statistics all-reduce, one JSON line from rank 0."""
 import json
@@ -29,7 +31,7 @@ def _port():
     return p
 
 
-def _dp_worker(rank, world, port, out):
+def _dp_worker(rank, world, port, out, exchange="nccl"):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
@@ -39,7 +41,7 @@ def _dp_worker(rank, world, port, out):
     cfg = TrainConfig(batch_size=64, buffer_capacity=20_000, warmup=500, total_iterations=120,
                       log_every=60, seed=4)
     res = run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=16, updates_per_step=1,
-                       world=dist.group.WORLD)
+                       world=dist.group.WORLD, exchange=exchange)
     out[rank] = ([p.copy() for p in res.net.params()], res.updates, res.transitions,
                  [(r.loss, r.mean_recent_reward) for r in res.log])
     dist.destroy_process_group()
@@ -55,6 +57,29 @@ def test_data_parallel_learner_replicas_identical(cuda):
         assert np.array_equal(a, b)
     assert len(l0) == len(l1) == 2
     assert t0 != t1 or l0 != l1  # the env shards (and their batches) are independent
+
+
+def test_peer_exchange_two_processes_matches_allreduce(cuda):
+    """exchange="peer": the ranks swap CUDA IPC handles of their exchange buffers
+    once and every update reads the peers' gradients from their memory (two
+    processes on one GPU here; NVLink peer memory across GPUs).  Same replicas,
+    bit for bit, as the all-reduce path on the same seeds."""
+    world = 2
+    res = {}
+    for exchange in ("nccl", "peer"):
+        out = mp.Manager().dict()
+        mp.spawn(_dp_worker, args=(world, _port(), out, exchange), nprocs=world, join=True)
+        res[exchange] = (out[0], out[1])
+    (p0, u0, t0, l0), (p1, u1, t1, l1) = res["peer"]
+    assert u0 == u1 > 0
+    for a, b in zip(p0, p1):
+        assert np.array_equal(a, b)
+    for r in range(world):
+        pa, ua, ta, la = res["peer"][r]
+        pb, ub, tb, lb = res["nccl"][r]
+        assert (ua, ta, la) == (ub, tb, lb)
+        for a, b in zip(pa, pb):
+            assert np.array_equal(a, b)
 
 
 def test_bench_two_ranks_one_gpu(cuda, tmp_path):
