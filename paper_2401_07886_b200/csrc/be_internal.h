@@ -38,6 +38,9 @@ namespace be {
 // before touching anything the predecessor wrote, and pdl_trigger() lets its own
 // successor be scheduled early.  Hides the kernel-boundary latency of the
 // launch-bound training iteration (six dependent kernels per iteration).
+#ifndef BE_PDL_IN_GRAPHS
+#define BE_PDL_IN_GRAPHS 1
+#endif
 #ifdef __CUDACC__
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -54,11 +57,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    // eager launches only: replaying a captured chain with programmatic edges measured
-    // slower on B200 than the plain graph (12.2k vs 14.3k training iterations/s)
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(st, &cs);
-    cfg.numAttrs = cs == cudaStreamCaptureStatusNone ? 1 : 0;
+    cfg.numAttrs = BE_PDL_IN_GRAPHS ? 1 : 0;
+    if (!BE_PDL_IN_GRAPHS) {  // programmatic edges only for eager launches
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        cfg.numAttrs = cs == cudaStreamCaptureStatusNone ? 1 : 0;
+    }
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 #endif

@@ -157,7 +157,6 @@ __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane
 }
 
 __global__ void __launch_bounds__(CENVS * 32) commit_fused_kernel(const CommitParams p) {
-    pdl_trigger();  // the next kernel of the stream may be scheduled now
     pdl_wait();     // the previous one has completed and its writes are visible
     __shared__ int vb_sh, cnt[CENVS];
     __shared__ long long wpre[CENVS];
@@ -230,6 +229,7 @@ __global__ void __launch_bounds__(CENVS * 32) commit_fused_kernel(const CommitPa
     }
     __syncthreads();
     if (e < p.E) commit_env(p, e, lane, excl_sh + wpre[warp], cursor_sh, true);
+    pdl_trigger();
 }
 
 // --------------------------------------------------------------- learner
@@ -387,7 +387,6 @@ struct UpdateParams {
 };
 
 __global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdateParams u) {
-    pdl_trigger();  // the next kernel of the stream may be scheduled now
     pdl_wait();     // the previous one has completed and its writes are visible
     const ApplyParams& p = u.ap;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -483,7 +482,6 @@ __device__ __forceinline__ double ld_relaxed_sys(const double* p) {
 }
 
 __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateParams u, const XParams x) {
-    pdl_trigger();
     pdl_wait();
     const ApplyParams& p = u.ap;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -571,7 +569,6 @@ __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateP
 
 template <int DM>
 __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
-    pdl_trigger();  // the next kernel of the stream may be scheduled now
     pdl_wait();     // the previous one has completed and its writes are visible
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
@@ -689,6 +686,7 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, lrow[row]);
         out[nparam] = s;
     }
+    pdl_trigger();
 }
 
 }  // namespace be

@@ -98,8 +98,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
 // the encoded state fits 16 lanes, else 32
 template <int M, int LPE>
 __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
-    pdl_trigger();  // the next kernel of the stream may be scheduled now
-    pdl_wait();     // the previous one has completed and its writes are visible
+    pdl_wait();  // the previous kernel has completed and its writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     const int T = p.cfg.n_tasks;
@@ -116,6 +115,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
         const int e = w * G + grp;
         step_env<M, LPE>(p, e < p.E ? e : p.E - 1, e < p.E, sc, p.qpack, policy, T, H, D);
     }
+    pdl_trigger();  // this CTA is done: the next kernel may start filling the SM
 }
 
 // One env per LPE-lane group (all 32 lanes of the warp call it: the group

@@ -275,9 +275,9 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
       "device" (default) be_train_iteration — every per-iteration value lives on
                the device and each update is one fused kernel; launched eagerly;
       "graph"  the same iterations captured once (`graph_chunk` at a time) in a
-               CUDA graph and replayed (B200, E = 4096, batch 512: 14.2k it/s vs
-               13.6k eager — 6 dependent launches per iteration, ~47 us of kernels;
-               eager launches use programmatic dependent launch, PDL);
+               CUDA graph and replayed (B200, E = 4096, batch 512: ~15k it/s vs
+               ~14k eager — 6 dependent launches per iteration, ~47 us of kernels;
+               launches use programmatic dependent launch, PDL);
       "host"   the step-by-step C ABI (workload / env step / commit / backward /
                apply) driven from Python — the reference loop's structure.
     All three give bit-identical results for the same seed.
