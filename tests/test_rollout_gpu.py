@@ -8,7 +8,7 @@ import torch
 
 import goldens
 from helpers import enc_of, first_diff, oracle_run, reward_of, tiers_of
-from paper_2401_07886_b200 import (CapacityError, GreedyRollout, QNetwork, TraceBatch,
+from paper_2401_07886_b200 import (CapacityError, GreedyRollout, QNetwork, StateEncoding, TraceBatch,
                                    reduce_eval, run_eval)
 from oracle import oracle
 
@@ -284,3 +284,49 @@ def test_wide_rings_use_unpacked_observe(cuda, name):
     g = goldens.load(name)
     o, _ = gpu_run(g, ring_capacity=1024)
     assert_env_equal(o, 0, g)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_screen_random_configs_equal_fp64(cuda, seed):
+    """Certified screen vs fp64 decisions on random clusters and networks: 1-8
+    tiers (packed and unpacked observe), up to 24 replicas (32-lane groups),
+    hidden 32-512, weights scaled up to make near-ties and large bounds common,
+    estimated rates on bursty traces (huge rate inputs).  Flags and rewards must
+    be identical bit for bit, whatever the fallback rate."""
+    rng = np.random.default_rng(500 + seed)
+    M = int(rng.choice([1, 2, 3, 4, 5, 8]))
+    T = int(rng.integers(1, 5))
+    H = int(rng.choice([32, 64, 128, 256, 512]))
+    tiers = []
+    for m in range(M):
+        tiers.append(dict(replicas=int(rng.integers(1, 25 // M + 1)), alpha_ms=float(rng.uniform(0.5, 30.0)),
+                          beta_ms=float(rng.uniform(0.05, 4.0)), max_batch=int(rng.integers(1, 64)),
+                          tokens_per_request=int(rng.integers(5, 120))))
+    reward = dict(tasks=[dict(name=f"t{t}", deadline=float(rng.uniform(5, 60)), kind=["hard", "soft"][t % 2])
+                         for t in range(T)],
+                  matrix=[[float(x) for x in rng.uniform(0, 1, M)] for _ in range(T)], decay=0.01, cutoff=0.1)
+    meta = dict(tiers=tiers, reward=reward)
+    net = QNetwork.init_random(T, M, H, rng)
+    scale = float(rng.choice([1.0, 30.0, 300.0]))
+    net.w2 = net.w2 * scale
+    net.b1 = rng.normal(0, 0.3, H)
+    net.b2 = rng.normal(0, 0.01 * scale, M)
+    E, n = 96, 1500
+    gaps = rng.exponential(1.0, size=(E, n)) * np.where(rng.random((E, n)) < 0.1, 0.05, 60.0)
+    arr = np.cumsum(gaps, axis=1)
+    tsk = rng.integers(0, T, size=(E, n)).astype(np.uint8)
+    tb = TraceBatch.from_arrays(arr, tsk, [[0]] * E, [[1.0]] * E)
+    enc = StateEncoding(T, tuple(float(t["max_batch"]) for t in tiers))
+    outs = []
+    for screen in (True, False):
+        ro = GreedyRollout(tiers_of(meta), reward_of(meta), E, n, enc, estimator_mode="estimated",
+                           q_screen=screen, ring_capacity=4096)
+        ro.env.screen_stats(reset=True)
+        o = ro.run(tb, net)
+        outs.append((o.flags.clone(), o.reward.clone(), ro.env.screen_stats()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    screened, fallback = outs[0][2]
+    lpe = 16 if sum(t["replicas"] for t in tiers) <= 16 else 32
+    assert screened == (E * n if H % (2 * lpe) == 0 else 0)  # the screen needs H % (2 LPE) == 0
+    assert 0 <= fallback <= screened
