@@ -18,14 +18,19 @@
 #include "be_env.cuh"
 #include "be_internal.h"
 
+// Occupancy (A/B on B200, config-4 bench, rollout ms): 256 threads x 3 CTAs per SM
+// (80 registers, small spills) with the skip table read through L1 373; 128 x 6 377;
+// 256 x 2 (128 registers) 393; 256 x 3 with the skip table staged in shared memory
+// 433 (the staging shrinks L1, which caches the skip table and the FIFO rings);
+// 128 x 7 / x 8 420 / 416 (spills).
 #ifndef BE_ROLLOUT_MINB
-#define BE_ROLLOUT_MINB 2  // resident CTAs per SM the register allocation is capped for
+#define BE_ROLLOUT_MINB 3  // resident CTAs per SM the register allocation is capped for
 #endif
 #ifndef BE_ROLLOUT_THREADS
 #define BE_ROLLOUT_THREADS 256
 #endif
 #ifndef BE_SKIP_SMEM_MAX
-#define BE_SKIP_SMEM_MAX (100 * 1024)  // stage the skip table if the CTA's shared memory stays below
+#define BE_SKIP_SMEM_MAX 0  // stage the skip table if the CTA's shared memory stays below (0: never)
 #endif
 
 namespace be {
@@ -68,7 +73,9 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code, int env)
     if (atomicCAS(&status[0], 0, code) == 0) status[1] = env;
 }
 
-template <int M, int LPE>
+// TR: 1 = true-rate estimator (the arrival window is never read, so its registers
+// are not allocated), 0 = estimated rate (workload.py:234-247)
+template <int M, int LPE, int TR>
 __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_k
     const TierC tc = lane_tier(p.cfg, gl, skip_tab);
     const bool active_lane = tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
-    const bool true_rate = p.cfg.estimator_true_rate != 0;
+    constexpr bool true_rate = TR != 0;
     const bool reset_segs = p.cfg.reset_between_segments != 0;
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
     // encode (policy.py:63-64) divides by the scales; multiplying by the
@@ -287,7 +294,7 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
 
 template <int M, int LPE>
 static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
-    auto kern = rollout_kernel<M, LPE>;
+    auto kern = p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 1> : rollout_kernel<M, LPE, 0>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
