@@ -23,14 +23,25 @@
 // 256 x 2 (128 registers) 393; 256 x 3 with the skip table staged in shared memory
 // 433 (the staging shrinks L1, which caches the skip table and the FIFO rings);
 // 128 x 7 / x 8 420 / 416 (spills).
+// The estimated-rate variant keeps the 5-arrival window live and spills at 80
+// registers (config 2, 4096 unpredictable-1 envs: 1.21e9 at 2 CTAs/SM with the skip
+// table in shared memory, 0.84e9 at 3 CTAs/SM), so it keeps 2 CTAs/SM and stages the
+// skip table; the true-rate variant runs 3 CTAs/SM and reads it through L1 when the
+// batch fills them (config 4), else 2 CTAs/SM (config 1: 18 envs, latency-bound).
 #ifndef BE_ROLLOUT_MINB
-#define BE_ROLLOUT_MINB 3  // resident CTAs per SM the register allocation is capped for
+#define BE_ROLLOUT_MINB 3  // resident CTAs per SM the register allocation is capped for (true rate)
+#endif
+#ifndef BE_ROLLOUT_MINB_EST
+#define BE_ROLLOUT_MINB_EST 2  // the same for the estimated-rate variant
 #endif
 #ifndef BE_ROLLOUT_THREADS
 #define BE_ROLLOUT_THREADS 256
 #endif
 #ifndef BE_SKIP_SMEM_MAX
-#define BE_SKIP_SMEM_MAX 0  // stage the skip table if the CTA's shared memory stays below (0: never)
+#define BE_SKIP_SMEM_MAX 0  // true rate: stage the skip table if the CTA's shared memory stays below (0: never)
+#endif
+#ifndef BE_SKIP_SMEM_MAX_EST
+#define BE_SKIP_SMEM_MAX_EST (100 * 1024)  // estimated rate: the same bound
 #endif
 
 namespace be {
@@ -74,9 +85,13 @@ __device__ __forceinline__ void raise_status(int32_t* status, int code, int env)
 }
 
 // TR: 1 = true-rate estimator (the arrival window is never read, so its registers
-// are not allocated), 0 = estimated rate (workload.py:234-247)
-template <int M, int LPE, int TR>
-__global__ void __launch_bounds__(BE_ROLLOUT_THREADS, BE_ROLLOUT_MINB) rollout_kernel(const RolloutParams p) {
+// are not allocated), 0 = estimated rate (workload.py:234-247).
+// OCC: 1 = the throughput variant (BE_ROLLOUT_MINB CTAs/SM, fewer registers), for
+// batches with enough envs to fill them; 0 = the latency variant (2 CTAs/SM, 128
+// registers, no spills) — a small batch is bound by its slowest env's serial chain.
+template <int M, int LPE, int TR, int OCC>
+__global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE_ROLLOUT_MINB_EST)
+    rollout_kernel(const RolloutParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     double* sw = reinterpret_cast<double*>(smem_raw + ((sizeof(Score) + 15) & ~size_t(15)));
@@ -294,7 +309,11 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
 
 template <int M, int LPE>
 static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
-    auto kern = p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 1> : rollout_kernel<M, LPE, 0>;
+    // the throughput variant once the batch fills BE_ROLLOUT_MINB CTAs on every SM
+    const bool many = (long long)p.E >= (long long)sms * BE_ROLLOUT_MINB * (BE_ROLLOUT_THREADS / LPE);
+    auto kern = !p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 0, 0>
+                : many                     ? rollout_kernel<M, LPE, 1, 1>
+                                           : rollout_kernel<M, LPE, 1, 0>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
@@ -373,7 +392,10 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
     // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
-    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <= BE_SKIP_SMEM_MAX;
+    const bool many = (long long)p.E >= (long long)env->sms * BE_ROLLOUT_MINB *
+                                           (BE_ROLLOUT_THREADS / (env->R <= 16 ? 16 : 32));
+    p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <=
+                              (size_t)(env->cfg.estimator_true_rate && many ? BE_SKIP_SMEM_MAX : BE_SKIP_SMEM_MAX_EST);
     size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0, p.screen);
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
