@@ -105,6 +105,14 @@ typedef struct {
     const int64_t* seg_start;    /* SegmentMark.start_index */
     const double* seg_rate;      /* SegmentMark.rate */
     const int32_t* seg_bucket;   /* per segment reducer bucket id, or NULL */
+    /* Streamed upload (optional, be_rollout_greedy): env e's arrival/task rows are
+     * read only after env_ready[e / envs_per_ready] >= ready_value — the caller's
+     * copy stream writes that flag after the rows' copy (e.g. a 4-byte
+     * cudaMemcpyAsync), so the rollout starts on the first envs while the rest of
+     * the batch is still in flight.  NULL: the rows are resident. */
+    const int32_t* env_ready;
+    int32_t envs_per_ready;
+    int32_t ready_value;
 } be_trace_soa;
 
 /* QNetwork parameters (policy.py:68-118), fp64, BEQN1 order/layout. */

@@ -56,7 +56,8 @@ class BeTraceSoa(ctypes.Structure):
                 ("arrival_ms", ctypes.c_void_p), ("task", ctypes.c_void_p),
                 ("n_events", ctypes.c_void_p), ("seg_offsets", ctypes.c_void_p),
                 ("seg_start", ctypes.c_void_p), ("seg_rate", ctypes.c_void_p),
-                ("seg_bucket", ctypes.c_void_p)]
+                ("seg_bucket", ctypes.c_void_p), ("env_ready", ctypes.c_void_p),
+                ("envs_per_ready", ctypes.c_int32), ("ready_value", ctypes.c_int32)]
 
 
 class BeQWeights(ctypes.Structure):

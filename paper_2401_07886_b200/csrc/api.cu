@@ -243,6 +243,8 @@ int32_t be_env_check(be_env* env, void* stream) {
         snprintf(msg, sizeof(msg), "env %d: action / tier out of range", st[1]);
     else if (st[0] == BE_ENONFINITE)
         snprintf(msg, sizeof(msg), "env %d: non-finite network input", st[1]);
+    else if (st[0] == BE_ECUDA)
+        snprintf(msg, sizeof(msg), "env %d: streamed trace rows never became ready (env_ready flag)", st[1]);
     else
         snprintf(msg, sizeof(msg), "env %d: device error %d", st[1], st[0]);
     return set_error(st[0], msg);

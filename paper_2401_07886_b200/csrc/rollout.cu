@@ -58,6 +58,8 @@ struct RolloutParams {
     const int64_t* seg_start;
     const double* seg_rate;
     const uint8_t* forced;
+    const int32_t* env_ready;  // streamed upload: wait for env_ready[env / envs_per_ready] >= ready_value
+    int32_t envs_per_ready, ready_value;
     int32_t static_tier;
     int32_t H;
     const double* w1;
@@ -158,6 +160,23 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
     for (;;) {
         // ---- (re)fill groups that finished their env
         int got = (need && gl == 0) ? atomicAdd(p.env_counter, 1) : 0;
+        if (p.env_ready && need && gl == 0 && got < p.E) {
+            // streamed upload: this env's rows are readable once its chunk's flag is set
+            const int32_t* f = p.env_ready + got / p.envs_per_ready;
+            unsigned long long t0, now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            for (;;) {
+                int v;
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                if (v >= p.ready_value) break;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (now - t0 > 10000000000ull) {  // 10 s: the upload never arrived
+                    raise_status(p.status, BE_ECUDA, got);
+                    break;
+                }
+                __nanosleep(256);
+            }
+        }
         got = __shfl_sync(FULL, got, g0);
         if (need) {
             need = false;
@@ -190,8 +209,11 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         if (live && sub == 0) {  // coalesced LPE-request prefetch
             const int ii = i + gl;
             if (ii < n) {
-                pf_arr = __ldg(p.arrival + base + ii);
-                pf_task = __ldg(p.task + base + ii);
+                // through L2 only (ld.global.cg): rows that arrive during the kernel
+                // (streamed upload) are never served from a stale L1 line; read-once
+                // rows gain nothing from L1 anyway (A/B: 1% faster than a branch)
+                pf_arr = __ldcg(p.arrival + base + ii);
+                pf_task = __ldcg(p.task + base + ii);
                 if (p.forced) pf_forced = __ldg(p.forced + base + ii);
             }
         }
@@ -360,6 +382,9 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     p.seg_start = tr->seg_start;
     p.seg_rate = tr->seg_rate;
     p.forced = forced;
+    p.env_ready = tr->env_ready;
+    p.envs_per_ready = tr->envs_per_ready > 0 ? tr->envs_per_ready : 1;
+    p.ready_value = tr->ready_value;
     p.static_tier = static_tier;
     p.rec = *rec;
     p.rings = reinterpret_cast<Slot*>(env->rings);

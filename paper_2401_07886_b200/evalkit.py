@@ -199,7 +199,7 @@ class GreedyRollout:
         return True
 
     def launch(self, trace: TraceBatch, policy=None, static_tier: int = -1,
-               forced: Optional[torch.Tensor] = None, stream=None) -> RolloutOutputs:
+               forced: Optional[torch.Tensor] = None, stream=None, ready=None) -> RolloutOutputs:
         """Asynchronous: enqueue the fused rollout on `stream` (no sync)."""
         if trace.n_envs > self.n_envs or trace.ld != self.ld:
             raise ValueError("trace batch does not match the rollout shape")
@@ -216,6 +216,9 @@ class GreedyRollout:
             self._dn = DeviceQNet.of(policy, self.device)
             w = self._dn.weights()
         soa = trace.soa()
+        if ready is not None:  # streamed upload (StreamingEvaluator): per-chunk ready flags
+            flags, per, value = ready
+            soa.env_ready, soa.envs_per_ready, soa.ready_value = flags.data_ptr(), int(per), int(value)
         _lib.check(self.env._L.be_rollout_greedy(self.env.handle, soa, w, int(static_tier),
                                                  _lib.ptr(forced), rec, _lib.stream_ptr(stream)))
         return o
@@ -355,6 +358,7 @@ class StreamingEvaluator:
         self._stat_pool = []
         self._stat_shapes = None
         self.max_outstanding = 8
+        self._flags = None
 
     def _device_buf(self, slot: int, host: TraceBatch) -> TraceBatch:
         b = self._bufs[slot]
@@ -367,25 +371,48 @@ class StreamingEvaluator:
             self._bufs[slot] = b
         return b
 
+    CHUNKS = 16  # streamed upload: the rollout starts once the first 1/16 of the envs arrived
+
     def submit(self, host: TraceBatch):
-        """host: a TraceBatch whose tensors live in pinned host memory."""
+        """host: a TraceBatch whose tensors live in pinned host memory.
+
+        The small per-env / per-segment arrays are copied first; the arrival and
+        task rows follow in CHUNKS env ranges, each followed by a 4-byte copy that
+        sets its ready flag, and the rollout (launched right after the metadata)
+        waits per env for its chunk's flag (be_trace_soa.env_ready) — so the
+        rollout of the first envs overlaps the upload of the rest."""
         slot = self._k & 1
         dev = self._device_buf(slot, host)
         cs, ks = self.copy_stream, self.compute_stream
+        E = host.n_envs
+        per = max(1, -(-E // self.CHUNKS))
+        n_chunks = -(-E // per)
+        if self._flags is None:
+            self._flags = [torch.zeros(self.CHUNKS, dtype=torch.int32, device=self.device) for _ in range(2)]
+            self._flag_vals = torch.arange(1, 1 << 16, dtype=torch.int32).pin_memory()
+        value = self._k // 2 + 1  # per slot: 1, 2, 3, ... (monotone, so flags never need a reset)
+        flags = self._flags[slot]
         with torch.cuda.stream(cs):
             cs.wait_event(self._freed[slot])  # previous use of this buffer finished
             nbytes = 0
-            for name in ("arrival", "task", "n_events", "seg_offsets", "seg_start", "seg_rate",
-                         "seg_bucket"):
+            for name in ("n_events", "seg_offsets", "seg_start", "seg_rate", "seg_bucket"):
                 src, dst = getattr(host, name), getattr(dev, name)
                 if src is not None:
                     dst.copy_(src, non_blocking=True)
                     nbytes += src.numel() * src.element_size()
             self._copied[slot].record(cs)
+            for c in range(n_chunks):
+                lo, hi = c * per, min(E, (c + 1) * per)
+                for name in ("arrival", "task"):
+                    src, dst = getattr(host, name), getattr(dev, name)
+                    dst[lo:hi].copy_(src[lo:hi], non_blocking=True)
+                    nbytes += src[lo:hi].numel() * src.element_size()
+                flags[c:c + 1].copy_(self._flag_vals[value - 1:value], non_blocking=True)
         self.h2d_bytes = nbytes
         with torch.cuda.stream(ks):
             ks.wait_event(self._copied[slot])
-            o = self.ro.launch(dev, self.net, self.static_tier, stream=ks)
+            o = self.ro.launch(dev, self.net, self.static_tier, stream=ks,
+                               ready=(flags, per, value))
             red = reduce_eval(dev, o.flags, o.reward, self.thresholds, self.n_buckets, stream=ks)
             self._freed[slot].record(ks)
             host_stats = self._stats_buffer(red)

@@ -26,7 +26,7 @@ def test_struct_sizes_match_c():
     from paper_2401_07886_b200 import _lib
     # be_tier 32 B; be_cfg layout checked against offsets in the header
     assert ctypes.sizeof(_lib.BeTier) == 32
-    assert ctypes.sizeof(_lib.BeTraceSoa) == 16 + 7 * 8
+    assert ctypes.sizeof(_lib.BeTraceSoa) == 16 + 8 * 8 + 2 * 4  # + env_ready, envs_per_ready, ready_value
     assert ctypes.sizeof(_lib.BeQWeights) == 8 + 4 * 8
     assert ctypes.sizeof(_lib.BeRecords) == 6 * 8
     assert ctypes.sizeof(_lib.BeGenCfg) == 128
