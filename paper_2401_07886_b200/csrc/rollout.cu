@@ -169,8 +169,9 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                 int v;
                 asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
                 if (v >= p.ready_value) break;
+                if (*(volatile int32_t*)p.status != 0) break;  // already failed: do not wait again
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                if (now - t0 > 10000000000ull) {  // 10 s: the upload never arrived
+                if (now - t0 > 5000000000ull) {  // 5 s: the upload never arrived
                     raise_status(p.status, BE_ECUDA, got);
                     break;
                 }

@@ -39,3 +39,21 @@ def test_streaming_matches_device_path(cuda):
             for k in w:
                 assert str(g[k]) == str(w[k]), (rnd, k)
     assert se.h2d_bytes > E * N * 9 and se.d2h_bytes > 0
+
+
+def test_streamed_rows_that_never_arrive_fail_loudly(cuda):
+    """A chunk flag that is never written makes the rollout report an error after
+    the bounded wait (5 s) instead of hanging or reading garbage silently."""
+    from paper_2401_07886_b200 import CudaError
+    E, N = 64, 500
+    tiers, rw = default_tiers(), RewardSpec.default()
+    enc = StateEncoding(4, tuple(float(t.max_batch) for t in tiers))
+    net = load_checkpoint(os.path.join(goldens.GOLDEN, "trained_seed7.beqn"))
+    tb = TraceBatch.generate_stable([3.0] * E, N, 4, 1, device=cuda)
+    ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False,
+                       ring_capacity=4096)
+    flags = torch.zeros(4, dtype=torch.int32, device=cuda)
+    flags[:2] = 7  # chunks 0-1 ready, 2-3 never
+    ro.launch(tb, net, ready=(flags, 16, 7))
+    with pytest.raises(CudaError, match="never became ready"):
+        ro.env.check()
