@@ -390,10 +390,12 @@ class StreamingEvaluator:
         if self._flags is None:
             self._flags = [torch.zeros(self.CHUNKS, dtype=torch.int32, device=self.device) for _ in range(2)]
             self._flag_vals = torch.arange(1, 1 << 16, dtype=torch.int32).pin_memory()
-        value = self._k // 2 + 1  # per slot: 1, 2, 3, ... (monotone, so flags never need a reset)
+        value = (self._k // 2) % (self._flag_vals.numel()) + 1  # per slot: 1, 2, 3, ... then wraps
         flags = self._flags[slot]
         with torch.cuda.stream(cs):
             cs.wait_event(self._freed[slot])  # previous use of this buffer finished
+            if value == 1:
+                flags.zero_()  # first use of the slot, or the value wrapped: flags below 1 again
             nbytes = 0
             for name in ("n_events", "seg_offsets", "seg_start", "seg_rate", "seg_bucket"):
                 src, dst = getattr(host, name), getattr(dev, name)
