@@ -22,6 +22,7 @@ collective), int64/f64 statistics all-reduced once at the end; weak scaling.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -414,11 +415,16 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    # the host side is a short Python loop: a cyclic-GC pass landing inside it (it walks
+    # every live Python object, ~0.1 s here) would be charged to the GPU pipeline
+    gc.collect()
+    gc.disable()
     t0 = time.perf_counter()
     hs = [se.submit(host) for _ in range(a.steps)]
     for h in hs:
         se.result(h)
     e2e_s = time.perf_counter() - t0
+    gc.enable()
     e2e_s = sharding.max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
     e2e = dict(value=world * E * N * a.steps / e2e_s, unit="env-steps/s",
                h2d_bytes_per_step=se.h2d_bytes, d2h_bytes_per_step=se.d2h_bytes,
