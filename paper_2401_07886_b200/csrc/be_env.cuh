@@ -351,7 +351,12 @@ __device__ __forceinline__ double estimator_observe(Estimator& est, double t, bo
     if (true_rate) return cur_rate;
     if (est.n < 2) return prior;
     double last = t;
-    double gap = __ddiv_rn(__ddiv_rn(__dsub_rn(last, est.w[0]), (double)(est.n - 1)), 1000.0);
+    // (last - w0) / (n - 1): for n - 1 in {1, 2, 4} (4 in steady state) the quotient is an
+    // exact power-of-two scaling, so the multiply gives the same bits as the division
+    const double span = __dsub_rn(last, est.w[0]);
+    const int d = est.n - 1;
+    const double mean = d == 3 ? __ddiv_rn(span, 3.0) : __dmul_rn(span, d == 4 ? 0.25 : d == 2 ? 0.5 : 1.0);
+    double gap = __ddiv_rn(mean, 1000.0);
     return __ddiv_rn(1.0, gap > 1e-6 ? gap : 1e-6);
 }
 
