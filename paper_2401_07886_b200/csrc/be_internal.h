@@ -92,7 +92,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st);
+                        double* x_base, cudaStream_t st, const struct WorkloadArgs* wl = nullptr);
 size_t env_state_bytes_per_env(int R);
 int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* reward, int window,
                   const double* thetas, int n_theta, int n_buckets, int64_t* win_counts,

@@ -24,6 +24,7 @@
 #include "be200.h"
 #include "be_internal.h"
 #include "be_philox.cuh"
+#include "be_workload.cuh"
 
 namespace be {
 
@@ -32,37 +33,13 @@ constexpr int UTHREADS = 256;  // learner_update_kernel: 32 parameters x 8 tile 
 constexpr int LTHREADS = 256;  // one thread per hidden unit (looping for H > 256)
 
 // --------------------------------------------------------------- workload
-// TrainingWorkload.next_arrival (trainer.py:304-316) per env; state [E][3] =
-// (time_ms, rate, segment_left).  Philox counter (step, env), key seed.
-__global__ void train_workload_kernel(int E, double* state, double log_lo, double log_hi,
-                                      int equal_time, double mean_seconds, double mean_requests,
-                                      int n_tasks, uint64_t seed, uint64_t step, double* arrival,
-                                      uint8_t* task, double* rate_out, const int64_t* step_dev) {
+// TrainingWorkload.next_arrival per env: be_workload.cuh (shared with the fused
+// weight-packing + workload launch of be_train_iteration, step.cu).
+__global__ void train_workload_kernel(WorkloadArgs w) {
     pdl_trigger();  // the next kernel of the stream may be scheduled now
     pdl_wait();     // the previous one has completed and its writes are visible
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= E) return;
-    if (step_dev) step = (uint64_t)*step_dev;  // be_train_iteration: iteration index on device
-    double t = state[3 * e], rate = state[3 * e + 1], left = state[3 * e + 2];
-    P4 a = philox4x32_10(step * 2, (uint64_t)e, seed);
-    if (left <= 0.0) {
-        rate = exp(log_lo + (log_hi - log_lo) * u01(a.x[0], a.x[1]));
-        double mean = equal_time ? fmax(1.0, mean_seconds * rate) : mean_requests;
-        double p = 1.0 / mean;
-        // numpy geometric(p): trials to the first success, >= 1 (inversion)
-        double u = u01(a.x[2], a.x[3]);
-        left = p >= 1.0 ? 1.0 : fmax(1.0, ceil(log1p(-u) / log1p(-p)));
-    }
-    left -= 1.0;
-    P4 b = philox4x32_10(step * 2 + 1, (uint64_t)e, seed);
-    const double gap = -log1p(-u01(b.x[0], b.x[1])) * (1000.0 / rate);
-    t = t + gap;
-    state[3 * e] = t;
-    state[3 * e + 1] = rate;
-    state[3 * e + 2] = left;
-    arrival[e] = t;
-    task[e] = (uint8_t)below(b.x[2], (uint32_t)n_tasks);
-    rate_out[e] = rate;
+    if (e < w.E) train_workload_env(w, e);
 }
 
 // --------------------------------------------------------------- commits
@@ -881,9 +858,9 @@ int32_t be_learner_workload(be_learner* L, uint64_t seed, int64_t step, double* 
     const be_learner_cfg& c = L->cfg;
     if (!(c.rate_low > 0) || c.rate_high < c.rate_low) return set_error(BE_EINVAL, "need 0 < rate_low <= rate_high");
     const int E = c.n_envs;
-    cudaError_t e = launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream,
-        E, L->wl_state, log(c.rate_low), log(c.rate_high), c.regime_equal_time, c.regime_mean_seconds,
-        c.regime_mean_requests, c.n_tasks, seed, (uint64_t)step, arrival_ms, task, true_rate, nullptr);
+    WorkloadArgs w{E, L->wl_state, log(c.rate_low), log(c.rate_high), c.regime_equal_time, c.regime_mean_seconds,
+                   c.regime_mean_requests, c.n_tasks, seed, (uint64_t)step, arrival_ms, task, true_rate, nullptr};
+    cudaError_t e = launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, (cudaStream_t)stream, w);
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "workload launch");
 }
 
@@ -1135,11 +1112,11 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
     int rc;
     const int64_t* gate = c->use_gate ? L->gate : nullptr;
     if (c->phase == 0 || c->phase == 3 || c->phase == 4) {
-        // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156)
-        launch_pdl(train_workload_kernel, dim3((E + 255) / 256), dim3(256), 0, st,
-            E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
-            cf.regime_mean_seconds, cf.regime_mean_requests, cf.n_tasks, c->workload_seed, 0,
-            L->it_arrival, L->it_task, L->it_rate, it);
+        // workload (trainer.py:375) -> env step (:376-395) -> commits (:143-156); the
+        // workload rides in the env step's weight-packing launch
+        const WorkloadArgs wl{E, L->wl_state, log(cf.rate_low), log(cf.rate_high), cf.regime_equal_time,
+                              cf.regime_mean_seconds, cf.regime_mean_requests, cf.n_tasks, c->workload_seed, 0,
+                              L->it_arrival, L->it_task, L->it_rate, it};
         be_qweights W;
         W.hidden = H;
         W.w1 = L->params;
@@ -1151,7 +1128,7 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         rec.reward = L->preward;
         rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                  c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
-                                 cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st);
+                                 cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl);
         if (rc) return rc;
         rc = commit_impl(L, 0, it, st);
         if (rc) return rc;

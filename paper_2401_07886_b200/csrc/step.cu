@@ -9,6 +9,7 @@
 #include "be_env.cuh"
 #include "be_internal.h"
 #include "be_philox.cuh"
+#include "be_workload.cuh"
 
 namespace be {
 
@@ -247,11 +248,30 @@ int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st) {
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env reset");
 }
 
+// Weight packing for the env step, fused with the next training arrival of every env
+// (be_train_iteration): CTAs [0, QPACK_CTAS) pack, the rest run the workload.
 template <int M>
-static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
+__global__ void __launch_bounds__(256) prep_kernel(const double* w1, const double* b1, const double* w2,
+                                                   const double* b2, int T, int H, double* out, WorkloadArgs wl) {
+    pdl_wait();  // the weights were updated by the previous kernel
+    if (blockIdx.x < QPACK_CTAS) {
+        stage_qnet<M>(w1, b1, w2, b2, T, H, out, blockIdx.x * blockDim.x + threadIdx.x, QPACK_CTAS * blockDim.x);
+    } else {
+        const int e = (blockIdx.x - QPACK_CTAS) * blockDim.x + threadIdx.x;
+        if (e < wl.E) train_workload_env(wl, e);
+    }
+    pdl_trigger();
+}
+
+template <int M>
+static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, const WorkloadArgs* wl) {
     const bool two = p.R <= 16 && p.cfg.n_tasks + M + 1 <= 16;
     auto kern = two ? env_step_kernel<M, 16> : env_step_kernel<M, 32>;
-    if (p.qpack) {  // pack the (possibly just updated) weights for this step
+    if (p.qpack && wl) {  // pack the weights + the training workload, one launch
+        cudaError_t e = launch_pdl(prep_kernel<M>, dim3(QPACK_CTAS + (wl->E + 255) / 256), dim3(256), 0, st, p.w1,
+                                   p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack), *wl);
+        if (e != cudaSuccess) return set_cuda_error(e, "prep launch");
+    } else if (p.qpack) {  // pack the (possibly just updated) weights for this step
         cudaError_t e = launch_pdl(stage_qpack_kernel<M>, dim3(QPACK_CTAS), dim3(256), 0, st, p.w1, p.b1, p.w2, p.b2,
                                    p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack));
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
@@ -275,16 +295,16 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st) {
 
 static size_t step_smem_bytes() { return (sizeof(Score) + 15) & ~size_t(15); }
 
-static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st) {
+static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st, const WorkloadArgs* wl = nullptr) {
     switch (p.cfg.n_tiers) {
-        case 1: return launch_step_m<1>(p, smem, st);
-        case 2: return launch_step_m<2>(p, smem, st);
-        case 3: return launch_step_m<3>(p, smem, st);
-        case 4: return launch_step_m<4>(p, smem, st);
-        case 5: return launch_step_m<5>(p, smem, st);
-        case 6: return launch_step_m<6>(p, smem, st);
-        case 7: return launch_step_m<7>(p, smem, st);
-        case 8: return launch_step_m<8>(p, smem, st);
+        case 1: return launch_step_m<1>(p, smem, st, wl);
+        case 2: return launch_step_m<2>(p, smem, st, wl);
+        case 3: return launch_step_m<3>(p, smem, st, wl);
+        case 4: return launch_step_m<4>(p, smem, st, wl);
+        case 5: return launch_step_m<5>(p, smem, st, wl);
+        case 6: return launch_step_m<6>(p, smem, st, wl);
+        case 7: return launch_step_m<7>(p, smem, st, wl);
+        case 8: return launch_step_m<8>(p, smem, st, wl);
         default: return set_error(BE_EINVAL, "n_tiers out of range");
     }
 }
@@ -341,7 +361,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st) {
+                        double* x_base, cudaStream_t st, const WorkloadArgs* wl) {
     StepParams p = base_params(env, rec_ld, rec);
     p.arrival = arrival;
     p.task = task;
@@ -360,7 +380,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     p.w2 = W->w2;
     p.b2 = W->b2;
     p.qpack = env->d_qpack;
-    return dispatch_step(p, step_smem_bytes(), st);
+    return dispatch_step(p, step_smem_bytes(), st, wl);
 }
 
 int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st) {
