@@ -199,19 +199,30 @@ def training_probe(dev, world):
     exchange_err = None
     if world > 1:
         # data-parallel learner (config 5): per-rank env shard and replay, gradients
-        # exchanged through peer memory inside the update kernel (graph-capturable)
+        # exchanged through peer memory inside the update kernel (graph-capturable) if
+        # every rank can map every peer's buffer (decided collectively), else NCCL
+        import torch
         import torch.distributed as dist
-        kw.update(world=dist.group.WORLD, exchange="peer")
+        from paper_2401_07886_b200.trainer import DeviceLearner
+        ok = 1
+        try:
+            probe = DeviceLearner(N_TASKS, 3, TrainConfig(batch_size=8, buffer_capacity=64), 1, 16, dev)
+            handles = [None] * world
+            dist.all_gather_object(handles, probe.ipc_handle())
+            probe.open_peers_ipc(dist.get_rank(), handles)
+        except Exception as e:  # e.g. CUDA IPC not permitted in this container
+            ok, exchange_err = 0, f"{type(e).__name__}: {e}"[:200]
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        dist.barrier()
+        if int(flag.item()):
+            kw.update(world=dist.group.WORLD, exchange="peer")
+        else:
+            kw.update(world=dist.group.WORLD, exchange="nccl", mode="device")
+            exchange_err = exchange_err or "a peer rank could not map the exchange buffers"
     warm = TrainConfig(batch_size=512, buffer_capacity=1 << 20, warmup=10_000, total_iterations=50,
                        log_every=50, seed=11)
-    try:
-        run_training(default_tiers(), RewardSpec.default(), warm, **kw)  # warm
-    except Exception as e:  # e.g. CUDA IPC not permitted in this container: NCCL all-reduce path
-        if world == 1:
-            raise
-        exchange_err = f"{type(e).__name__}: {e}"[:200]
-        kw.update(exchange="nccl", mode="device")
-        run_training(default_tiers(), RewardSpec.default(), warm, **kw)
+    run_training(default_tiers(), RewardSpec.default(), warm, **kw)  # warm
     t = {}
     res = run_training(default_tiers(), RewardSpec.default(), cfg, timing=t, **kw)
     s = t["loop_ms"] / 1e3
