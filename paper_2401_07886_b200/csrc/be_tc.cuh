@@ -121,6 +121,25 @@ __device__ __forceinline__ void tmem_ld_wait(float (&v)[32]) {
         : "memory");
 }
 
+// 16 consecutive fp32 columns.  No memory clobber: TMEM is not generic memory
+// and the wait is tied to the destination registers, so shared loads (the
+// epilogue's weight reads) may be scheduled across both; ordering after the
+// MMA's mbarrier wait is kept by asm volatile.
+__device__ __forceinline__ void tmem_ld_issue(uint32_t taddr, float (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+          "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait(float (&v)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]),
+                   "+f"(v[7]), "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]),
+                   "+f"(v[14]), "+f"(v[15]));
+}
+
 // UMMA shared-memory descriptor, K-major, no swizzle ("interleave"): the operand
 // is a grid of 8-row x 16-byte core matrices; `lbo` = byte distance between the
 // two K-adjacent core matrices one MMA reads, `sbo` = between 8-row groups.

@@ -3,21 +3,20 @@
 // be_qnet_route_tc in include/be200.h.
 //
 // Persistent CTAs of 256 threads, two per SM (each owns half of the SM's 512
-// TMEM columns); per 128-state tile:
-//   * every thread converts its state row (fp64, D <= 15 inputs + a constant-1
+// TMEM columns); per 256-state tile (two 128-row halves):
+//   * every thread converts one state row (fp64, D <= 15 inputs + a constant-1
 //     bias input) to a 3xTF32 split (hi + lo) in shared memory, K-major
 //     no-swizzle UMMA layout;
-//   * one elected thread issues six tcgen05.mma.kind::tf32 (2 K-steps x
-//     {hi.hi, hi.lo, lo.hi}, M = 128, N = H) accumulating the layer-1
-//     pre-activations [128 x H] in fp32 in TMEM; tcgen05.commit -> mbarrier;
-//   * epilogue: two threads per state (warps w and w + 4 read the same TMEM
-//     lanes) tcgen05.ld half of the row each, relu, and the N = M (<= 4) layer-2
-//     dot products on packed FFMA2 from shared memory; halves merged in smem;
-//   * the decision is certified with an error bound (as the rollout screen,
-//     be_env.cuh) whose layer-1 term models each tensor-core accumulation step
-//     of 8 products as 9 fp32 roundings of <= 2u each; states it cannot certify
-//     are re-evaluated by a warp with route_row_f64 — the exact arithmetic of
-//     be_qnet_route_f64 — so every greedy decision equals the fp64 router's.
+//   * two passes over the hidden units (H/2 each): one elected thread issues
+//     twelve tcgen05.mma.kind::tf32 (2 halves x 2 K-steps x {hi.hi, hi.lo,
+//     lo.hi}, M = 128, N = H/2) accumulating the pass's layer-1 pre-activations
+//     of both halves in fp32 in TMEM (columns [0, H/2) and [H/2, H));
+//     tcgen05.commit -> mbarrier;
+//   * epilogue: warps w and w + 4 read the same TMEM lanes r, each half of the
+//     pass's columns of BOTH states r and r + 128, relu, and the N = M (<= 4)
+//     layer-2 dot products on packed FFMA2 — every W2 shared-memory load feeds
+//     two states; after the second pass the two threads exchange partial sums
+//     in shared memory and each finalizes one state;
 // Weights are packed once per call (route_tc_pack_kernel: tf32 hi/lo UMMA
 // images of [W1; b1]^T, W2 pairs, bound tables) and staged per CTA with one
 // bulk asynchronous copy (TMA engine, mbarrier completion).  Q values out are
@@ -35,7 +34,9 @@
 namespace be {
 
 constexpr int TC_ROWS = 128;  // MMA M: states per tile = TMEM lanes
-constexpr int TC_THREADS = 256;  // two threads per state: each takes half of the hidden columns
+constexpr int TC_TILE = 256;  // states per tile: two 128-row MMA halves
+constexpr int TC_THREADS = 256;  // per TMEM lane two threads (lower / upper), each half of the hidden units of both states
+constexpr int TC_CW = 16;     // TMEM columns per tcgen05.ld in the epilogue
 constexpr int TC_K = 16;      // inputs (D <= 15) + the bias input, two tf32 K-steps of 8
 constexpr int TC_MP = 4;      // layer-2 outputs padded (n_tiers <= 4)
 constexpr int TC_FLIST = 4096;  // deferred fp64 re-evaluations per CTA (shared-memory list)
@@ -58,9 +59,13 @@ __host__ __device__ __forceinline__ int umma_off(int n, int k) {
 
 // error-bound constant K (units of u = 2^-24) for hidden width H: layer 1 = input /
 // weight rounding and the dropped lo.lo term (14) + 6 MMAs x 9 accumulations x 2 (108);
-// layer 2 = FFMA2 chains of <= H/16 + 1 terms per half + the half merge + 4 tree/bias
-// adds + W2 rounding (H/16 + 7); slack 16
-__host__ __device__ __forceinline__ double tc_bound_k(int H) { return (double)(122 + H / 16 + 7 + 16) * 0x1p-24; }
+// layer 2 = FFMA2 chains of <= L = 8 ceil(H / 64) terms (a thread's share of a state:
+// 2 passes x <= ceil(H / 64) chunks of 16 units over 2 sets x 2 lanes) + the
+// lower/upper merge, the lane merge, the set merge and the bias add + W2 rounding
+// (<= L + 7); slack 16
+__host__ __device__ __forceinline__ double tc_bound_k(int H) {
+    return (double)(122 + 8 * ((H + 63) / 64) + 7 + 16) * 0x1p-24;
+}
 
 template <int M>
 __global__ void __launch_bounds__(256) route_tc_pack_kernel(const double* w1, const double* b1, const double* w2,
@@ -141,18 +146,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     const TcLayout L{p.H};
     const int img_bytes = L.bytes();
     float* img = reinterpret_cast<float*>(smem);
-    float* Ah = reinterpret_cast<float*>(smem + ((img_bytes + 1023) & ~1023));
-    float* Al = Ah + TC_ROWS * TC_K;
-    float2* part = reinterpret_cast<float2*>(Al + TC_ROWS * TC_K);  // [4][TC_MP][TC_ROWS] upper-half sums
-    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 4 * TC_MP * TC_ROWS);  // [0] image, [1] MMA
+    float* Ah = reinterpret_cast<float*>(smem + ((img_bytes + 1023) & ~1023));  // [2 halves][TC_ROWS x TC_K]
+    float* Al = Ah + 2 * TC_ROWS * TC_K;
+    float2* part = reinterpret_cast<float2*>(Al + 2 * TC_ROWS * TC_K);  // [2 sets][TC_MP][TC_TILE] exchanged sums
+    uint64_t* bars = reinterpret_cast<uint64_t*>(part + 2 * TC_MP * TC_TILE);  // [0] image, [1] MMA
     uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bars + 2);
     int* fcount = reinterpret_cast<int*>(tmem_sh + 1);
     int* flist = fcount + 1;  // [TC_FLIST]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int r = tid & (TC_ROWS - 1);      // state (= TMEM lane) of this thread
-    const bool lower = tid < TC_ROWS;       // lower threads: columns [0, c_mid) + the decision
-    const int D = p.D, H = p.H;
-    const int nch = H / 32, c_mid = (nch + 1) / 2;
+    const int r = tid & (TC_ROWS - 1);  // TMEM lane of this thread
+    const int hs = tid >> 7;            // 0: lower threads, 1: upper threads
+    const int D = p.D, H = p.H, HP = H / 2;
+    const int nch = HP / TC_CW, c_mid = (nch + 1) / 2;
 
     if (tid == 0) {
         tc::mbar_init(&bars[0], 1);
@@ -176,8 +181,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     const float4* W2q = reinterpret_cast<const float4*>(img + L.w2p() / 4);
     const float* fb2 = img + L.b2() / 4;
     const float* C = img + L.bound() / 4;
-    const uint32_t idesc = tc::idesc_tf32(TC_ROWS, H);
-    const int ntiles = (p.B + TC_ROWS - 1) / TC_ROWS;
+    const uint32_t idesc = tc::idesc_tf32(TC_ROWS, HP);
+    const int ntiles = (p.B + TC_TILE - 1) / TC_TILE;
     uint32_t phase = 0;
     unsigned n_rows = 0, n_fb = 0;
 
@@ -202,131 +207,166 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
             if (lane == 0) p.a_out[rf] = (uint8_t)b;
         }
     };
-    // relu + layer 2 of one 32-column chunk (packed FFMA2, 4 accumulator sets)
-    float2 a[4][M];
-    auto consume = [&](const float(&u)[32], int c) {
+    // relu + layer 2 of one TC_CW-unit chunk for BOTH states of this lane (u0:
+    // state r, u1: state r + 128), so every W2 shared-memory load feeds two
+    // states; units (2i, 2i+1) accumulate into set 0, (2i+2, 2i+3) into set 1
+    float2 a0[2][M], a1[2][M];
+    auto consume = [&](const float(&u0)[TC_CW], const float(&u1)[TC_CW], int jb) {
 #pragma unroll
-        for (int i = 0; i < 16; i += 2) {
-            const float2 h0 = make_float2(fmaxf(u[2 * i], 0.f), fmaxf(u[2 * i + 1], 0.f));
-            const float2 h1 = make_float2(fmaxf(u[2 * i + 2], 0.f), fmaxf(u[2 * i + 3], 0.f));
-            const float4* g = W2q + (size_t)(c * 8 + i / 2) * 4;
+        for (int i = 0; i < TC_CW / 2; i += 2) {
+            const float2 h00 = make_float2(fmaxf(u0[2 * i], 0.f), fmaxf(u0[2 * i + 1], 0.f));
+            const float2 h01 = make_float2(fmaxf(u0[2 * i + 2], 0.f), fmaxf(u0[2 * i + 3], 0.f));
+            const float2 h10 = make_float2(fmaxf(u1[2 * i], 0.f), fmaxf(u1[2 * i + 1], 0.f));
+            const float2 h11 = make_float2(fmaxf(u1[2 * i + 2], 0.f), fmaxf(u1[2 * i + 3], 0.f));
+            const float4* g = W2q + (size_t)((jb + 2 * i) >> 2) * 4;
             const float4 g0 = g[0], g1 = g[1];
-            a[i & 3][0] = ffma2(h0, make_float2(g0.x, g0.y), a[i & 3][0]);
-            a[(i + 1) & 3][0] = ffma2(h1, make_float2(g1.x, g1.y), a[(i + 1) & 3][0]);
+            a0[0][0] = ffma2(h00, make_float2(g0.x, g0.y), a0[0][0]);
+            a0[1][0] = ffma2(h01, make_float2(g1.x, g1.y), a0[1][0]);
+            a1[0][0] = ffma2(h10, make_float2(g0.x, g0.y), a1[0][0]);
+            a1[1][0] = ffma2(h11, make_float2(g1.x, g1.y), a1[1][0]);
             if (M > 1) {
-                a[i & 3][M > 1 ? 1 : 0] = ffma2(h0, make_float2(g0.z, g0.w), a[i & 3][M > 1 ? 1 : 0]);
-                a[(i + 1) & 3][M > 1 ? 1 : 0] = ffma2(h1, make_float2(g1.z, g1.w), a[(i + 1) & 3][M > 1 ? 1 : 0]);
+                constexpr int m1 = M > 1 ? 1 : 0;
+                a0[0][m1] = ffma2(h00, make_float2(g0.z, g0.w), a0[0][m1]);
+                a0[1][m1] = ffma2(h01, make_float2(g1.z, g1.w), a0[1][m1]);
+                a1[0][m1] = ffma2(h10, make_float2(g0.z, g0.w), a1[0][m1]);
+                a1[1][m1] = ffma2(h11, make_float2(g1.z, g1.w), a1[1][m1]);
             }
             if (M > 2) {
+                constexpr int m2 = M > 2 ? 2 : 0;
                 const float4 g2 = g[2];
-                a[i & 3][M > 2 ? 2 : 0] = ffma2(h0, make_float2(g2.x, g2.y), a[i & 3][M > 2 ? 2 : 0]);
-                a[(i + 1) & 3][M > 2 ? 2 : 0] = ffma2(h1, make_float2(g2.z, g2.w), a[(i + 1) & 3][M > 2 ? 2 : 0]);
+                a0[0][m2] = ffma2(h00, make_float2(g2.x, g2.y), a0[0][m2]);
+                a0[1][m2] = ffma2(h01, make_float2(g2.z, g2.w), a0[1][m2]);
+                a1[0][m2] = ffma2(h10, make_float2(g2.x, g2.y), a1[0][m2]);
+                a1[1][m2] = ffma2(h11, make_float2(g2.z, g2.w), a1[1][m2]);
             }
             if (M > 3) {
+                constexpr int m3 = M > 3 ? 3 : 0;
                 const float4 g3 = g[3];
-                a[i & 3][M > 3 ? 3 : 0] = ffma2(h0, make_float2(g3.x, g3.y), a[i & 3][M > 3 ? 3 : 0]);
-                a[(i + 1) & 3][M > 3 ? 3 : 0] = ffma2(h1, make_float2(g3.z, g3.w), a[(i + 1) & 3][M > 3 ? 3 : 0]);
+                a0[0][m3] = ffma2(h00, make_float2(g3.x, g3.y), a0[0][m3]);
+                a0[1][m3] = ffma2(h01, make_float2(g3.z, g3.w), a0[1][m3]);
+                a1[0][m3] = ffma2(h10, make_float2(g3.x, g3.y), a1[0][m3]);
+                a1[1][m3] = ffma2(h11, make_float2(g3.z, g3.w), a1[1][m3]);
             }
         }
     };
+    // this thread's state row of a tile (thread t stages state t of the tile)
     auto load_row = [&](int tile, double (&xd)[DM]) {
-        const int row = tile * TC_ROWS + r;
+        const int row = tile * TC_TILE + tid;
 #pragma unroll
         for (int k = 0; k < DM; ++k)
-            xd[k] = (lower && k < D && tile < ntiles && row < p.B) ? __ldg(p.x + (size_t)row * D + k) : 0.0;
+            xd[k] = (k < D && tile < ntiles && row < p.B) ? __ldg(p.x + (size_t)row * D + k) : 0.0;
     };
-    double xn[DM];  // next tile's state row (lower threads), loaded during this tile's epilogue
+    // one pass: layer 1 for hidden units [pass * HP, pass * HP + HP) of both
+    // 128-state halves (TMEM columns [0, HP) and [HP, 2 HP)); one thread issues
+    auto issue_mma = [&](int pass) {
+        tc::fence_after_sync();
+        const float* bh0 = B1h + pass * HP * TC_K;  // 8-row groups of 128 floats: row n0 at n0 * 16
+        const float* bl0 = B1l + pass * HP * TC_K;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t d = tmem + (uint32_t)(h * HP);
+            const float* ah0 = Ah + h * TC_ROWS * TC_K;
+            const float* al0 = Al + h * TC_ROWS * TC_K;
+#pragma unroll
+            for (int s = 0; s < TC_K / 8; ++s) {  // K-step s reads K-groups 2s, 2s + 1
+                const uint64_t ah = tc::smem_desc(ah0 + s * 64, 128, 512), al = tc::smem_desc(al0 + s * 64, 128, 512);
+                const uint64_t bh = tc::smem_desc(bh0 + s * 64, 128, 512), bl = tc::smem_desc(bl0 + s * 64, 128, 512);
+                tc::mma_tf32(d, ah, bh, idesc, s > 0);
+                tc::mma_tf32(d, ah, bl, idesc, true);
+                tc::mma_tf32(d, al, bh, idesc, true);
+            }
+        }
+        tc::mma_commit(&bars[1]);
+    };
+    // epilogue of one pass: lower threads take chunks [0, c_mid), upper [c_mid, nch)
+    const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    auto epilogue = [&](int pass) {
+        const int c0 = hs ? c_mid : 0, c1 = hs ? nch : c_mid;
+        for (int c = c0; c < c1; ++c) {
+            float u0[TC_CW], u1[TC_CW];
+            tc::tmem_ld_issue(lane_addr + (uint32_t)(c * TC_CW), u0);
+            tc::tmem_ld_issue(lane_addr + (uint32_t)(HP + c * TC_CW), u1);
+            tc::tmem_ld_wait(u0);
+            tc::tmem_ld_wait(u1);
+            consume(u0, u1, pass * HP + c * TC_CW);
+        }
+    };
+
+    double xn[DM];  // next tile's state row, loaded during this tile's MMAs and epilogue
     load_row(blockIdx.x, xn);
 
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int row = tile * TC_ROWS + r;
-        const bool valid = lower && row < p.B;
-        // ---- A operand (lower threads): the state row, 3xTF32 split (+ the bias input = 1)
+        const int row = tile * TC_TILE + tid;
+        const bool valid = row < p.B;
+        // ---- A operand: this thread's state row, 3xTF32 split (+ the bias input = 1)
         float xf[DM];
 #pragma unroll
         for (int k = 0; k < DM; ++k) xf[k] = __double2float_rn(xn[k]);
         auto in = [&](int k) { return k < DM && k < D ? xf[k < DM ? k : 0] : (k == D ? 1.f : 0.f); };
-        if (lower) {
+        float* ahm = Ah + hs * TC_ROWS * TC_K;
+        float* alm = Al + hs * TC_ROWS * TC_K;
 #pragma unroll
-            for (int kg = 0; kg < TC_K / 4; ++kg) {
-                float4 h, l;
-                h.x = tc::to_tf32(in(4 * kg + 0));
-                h.y = tc::to_tf32(in(4 * kg + 1));
-                h.z = tc::to_tf32(in(4 * kg + 2));
-                h.w = tc::to_tf32(in(4 * kg + 3));
-                l.x = tc::to_tf32(__fsub_rn(in(4 * kg + 0), h.x));
-                l.y = tc::to_tf32(__fsub_rn(in(4 * kg + 1), h.y));
-                l.z = tc::to_tf32(__fsub_rn(in(4 * kg + 2), h.z));
-                l.w = tc::to_tf32(__fsub_rn(in(4 * kg + 3), h.w));
-                *reinterpret_cast<float4*>(Ah + umma_off(r, 4 * kg)) = h;
-                *reinterpret_cast<float4*>(Al + umma_off(r, 4 * kg)) = l;
-            }
+        for (int kg = 0; kg < TC_K / 4; ++kg) {
+            float4 h, l;
+            h.x = tc::to_tf32(in(4 * kg + 0));
+            h.y = tc::to_tf32(in(4 * kg + 1));
+            h.z = tc::to_tf32(in(4 * kg + 2));
+            h.w = tc::to_tf32(in(4 * kg + 3));
+            l.x = tc::to_tf32(__fsub_rn(in(4 * kg + 0), h.x));
+            l.y = tc::to_tf32(__fsub_rn(in(4 * kg + 1), h.y));
+            l.z = tc::to_tf32(__fsub_rn(in(4 * kg + 2), h.z));
+            l.w = tc::to_tf32(__fsub_rn(in(4 * kg + 3), h.w));
+            *reinterpret_cast<float4*>(ahm + umma_off(r, 4 * kg)) = h;
+            *reinterpret_cast<float4*>(alm + umma_off(r, 4 * kg)) = l;
         }
+        // decision bound (needs only the inputs): against exact arithmetic on the
+        // fp32-rounded inputs; the fp64 inputs differ by <= u |x|, covered by the slack in K
+        float Bd = C[D];
+#pragma unroll
+        for (int k = 0; k < DM; ++k)
+            if (k < D) Bd = __fmaf_ru(fabsf(xf[k]), C[k], Bd);
         tc::fence_proxy_async_smem();
         tc::fence_before_sync();  // the previous tile's TMEM loads are complete
         __syncthreads();
-        if (tid == 0) {
-            tc::fence_after_sync();
+        if (tid == 0) issue_mma(0);
+        load_row(tile + gridDim.x, xn);  // overlaps the MMAs and the epilogues
 #pragma unroll
-            for (int s = 0; s < TC_K / 8; ++s) {  // K-step s reads K-groups 2s, 2s + 1
-                const uint64_t ah = tc::smem_desc(Ah + s * 64, 128, 512), al = tc::smem_desc(Al + s * 64, 128, 512);
-                const uint64_t bh = tc::smem_desc(B1h + s * 64, 128, 512), bl = tc::smem_desc(B1l + s * 64, 128, 512);
-                tc::mma_tf32(tmem, ah, bh, idesc, s > 0);
-                tc::mma_tf32(tmem, ah, bl, idesc, true);
-                tc::mma_tf32(tmem, al, bh, idesc, true);
-            }
-            tc::mma_commit(&bars[1]);
-        }
-        load_row(tile + gridDim.x, xn);  // overlaps the MMAs and the epilogue
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int m = 0; m < M; ++m) a0[s][m] = a1[s][m] = make_float2(0.f, 0.f);
         tc::mbar_wait(&bars[1], phase);
         phase ^= 1u;
         tc::fence_after_sync();
-
-        // ---- epilogue: lower threads take chunks [0, c_mid), upper [c_mid, nch) of the
-        // same state; the TMEM load of the next chunk is in flight while one is consumed
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-#pragma unroll
-            for (int m = 0; m < M; ++m) a[s][m] = make_float2(0.f, 0.f);
-        const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-        const int c0 = lower ? 0 : c_mid, c1 = lower ? c_mid : nch;
-        if (c0 < c1) {
-            float v0[32], v1[32];
-            tc::tmem_ld32_issue(lane_addr + (uint32_t)(c0 * 32), v0);
-            tc::tmem_ld_wait(v0);
-            for (int c = c0; c < c1; c += 2) {
-                if (c + 1 < c1) tc::tmem_ld32_issue(lane_addr + (uint32_t)((c + 1) * 32), v1);
-                consume(v0, c);
-                if (c + 1 < c1) {
-                    tc::tmem_ld_wait(v1);
-                    if (c + 2 < c1) tc::tmem_ld32_issue(lane_addr + (uint32_t)((c + 2) * 32), v0);
-                    consume(v1, c + 1);
-                    if (c + 2 < c1) tc::tmem_ld_wait(v0);
-                }
-            }
-        }
-        if (!lower) {
-#pragma unroll
-            for (int s = 0; s < 4; ++s)
-#pragma unroll
-                for (int m = 0; m < M; ++m) part[(s * TC_MP + m) * TC_ROWS + r] = a[s][m];
-        }
+        epilogue(0);
+        tc::fence_before_sync();
         __syncthreads();
-        if (lower) {
+        if (tid == 0) issue_mma(1);
+        tc::mbar_wait(&bars[1], phase);
+        phase ^= 1u;
+        tc::fence_after_sync();
+        epilogue(1);
+        // ---- exchange: the lower thread of lane r finalizes state r, the upper one
+        // state r + 128; each hands the other its partial sums of the other state
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int m = 0; m < M; ++m) part[(s * TC_MP + m) * TC_TILE + (tid ^ TC_ROWS)] = hs ? a0[s][m] : a1[s][m];
+        __syncthreads();
+        {
             float q[M];
             int best = 0;
             float bv = 0.f, sv = -INFINITY;
             bool fin = true;
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                float2 t[4];
+                float2 t[2];
 #pragma unroll
-                for (int s = 0; s < 4; ++s) {
-                    const float2 u = part[(s * TC_MP + m) * TC_ROWS + r];
-                    t[s] = make_float2(__fadd_rn(a[s][m].x, u.x), __fadd_rn(a[s][m].y, u.y));
+                for (int s = 0; s < 2; ++s) {
+                    const float2 own = hs ? a1[s][m] : a0[s][m];
+                    const float2 u = part[(s * TC_MP + m) * TC_TILE + tid];
+                    t[s] = make_float2(__fadd_rn(own.x, u.x), __fadd_rn(own.y, u.y));
                 }
-                const float t0 = __fadd_rn(__fadd_rn(t[0].x, t[0].y), __fadd_rn(t[1].x, t[1].y));
-                const float t1 = __fadd_rn(__fadd_rn(t[2].x, t[2].y), __fadd_rn(t[3].x, t[3].y));
+                const float t0 = __fadd_rn(t[0].x, t[0].y), t1 = __fadd_rn(t[1].x, t[1].y);
                 q[m] = __fadd_rn(__fadd_rn(t0, t1), fb2[m]);
                 fin = fin && isfinite(q[m]);
                 if (m == 0 || q[m] > bv) {
@@ -338,12 +378,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
                 }
                 if (m == 0) sv = -INFINITY;
             }
-            float Bd = C[D];
-#pragma unroll
-            for (int k = 0; k < DM; ++k)
-                if (k < D) Bd = __fmaf_ru(fabsf(xf[k]), C[k], Bd);
-            // the bound is against exact arithmetic on the fp32-rounded inputs; the fp64
-            // inputs differ by <= u |x|, covered by the slack in K
             const bool sure =
                 M == 1 || (fin && isfinite(Bd) && __dsub_rd((double)bv, (double)sv) > 2.0 * (double)Bd);
             if (valid) {
@@ -367,7 +401,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
         // the deferred list can take one more full tile?  else drain it now
         __syncthreads();
         const int nf = *fcount;
-        if (nf > TC_FLIST - TC_ROWS) {
+        if (nf > TC_FLIST - TC_TILE) {
             fallback(nf);
             __syncthreads();
             if (tid == 0) *fcount = 0;
@@ -397,7 +431,7 @@ size_t route_tc_workspace_bytes(int H) { return (size_t)TcLayout{H}.bytes(); }
 
 static size_t route_tc_smem(int H) {
     const size_t img = ((size_t)TcLayout{H}.bytes() + 1023) & ~size_t(1023);
-    const size_t need = img + 2 * sizeof(float) * TC_ROWS * TC_K + sizeof(float2) * 4 * TC_MP * TC_ROWS + 2 * 8 +
+    const size_t need = img + 4 * sizeof(float) * TC_ROWS * TC_K + sizeof(float2) * 2 * TC_MP * TC_TILE + 2 * 8 +
                         4 + 4 + 4 * TC_FLIST;
     // at most two CTAs per SM: each owns up to 256 of the SM's 512 TMEM columns
     return need > 80 * 1024 ? need : 80 * 1024;
@@ -437,7 +471,7 @@ static int launch_route_tc_m(const be_qweights* W, int T, const double* x, int B
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int ntiles = (B + TC_ROWS - 1) / TC_ROWS;
+    const int ntiles = (B + TC_TILE - 1) / TC_TILE;
     const int blocks = ntiles < 2 * sms ? ntiles : 2 * sms;
     kern<<<blocks, TC_THREADS, smem, st>>>(p);
     e = cudaGetLastError();
