@@ -39,6 +39,8 @@ constexpr int TC_THREADS = 256;  // per TMEM lane two threads (lower / upper), e
 constexpr int TC_CW = 16;     // TMEM columns per tcgen05.ld in the epilogue
 constexpr int TC_K = 16;      // inputs (D <= 15) + the bias input, two tf32 K-steps of 8
 constexpr int TC_MP = 4;      // layer-2 outputs padded (n_tiers <= 4)
+constexpr int TC_FBS = 4;     // fp64 fallback: states per warp
+constexpr int TC_FBKB = 4;    // fp64 fallback: hidden units per lane per block
 constexpr int TC_FLIST = 4096;  // deferred fp64 re-evaluations per CTA (shared-memory list)
 
 struct TcLayout {  // byte offsets inside the packed image (= the shared-memory image)
@@ -186,25 +188,35 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     uint32_t phase = 0;
     unsigned n_rows = 0, n_fb = 0;
 
-    // fp64 re-evaluation of the states the bound could not certify, one warp per
-    // state; deferred (CTA list in shared memory) so no tile waits for it
+    // fp64 re-evaluation of the states the bound could not certify, TC_FBS states
+    // per warp (each weight load feeds all of them); deferred (CTA list in shared
+    // memory) so no tile waits for it
     auto fallback = [&](int nf) {
-        for (int f = warp; f < nf; f += TC_THREADS / 32) {
-            const int rf = flist[f];
-            const double xv = lane < D ? __ldg(p.x + (size_t)rf * D + lane) : 0.0;
-            double q64[M];
-            route_row_f64<M>(xv, D, H, p.w1, p.b1, p.w2, M, 1, p.b2, q64);
-            int b = route_argmax<M>(q64);
-            if (p.eps > 0.0) {
-                P4 rn = philox4x32_10(p.counter, (uint64_t)rf, p.seed);
-                if (u01(rn.x[0], rn.x[1]) < p.eps) b = (int)below(rn.x[2], (uint32_t)M);
-            }
-            if (lane < M && p.q_out) {
+        for (int f0 = warp * TC_FBS; f0 < nf; f0 += TC_THREADS / 32 * TC_FBS) {
+            int rf[TC_FBS];
+            double xv[TC_FBS];
 #pragma unroll
-                for (int m = 0; m < M; ++m)
-                    if (lane == m) p.q_out[(size_t)rf * M + m] = (float)q64[m];
+            for (int s = 0; s < TC_FBS; ++s) {
+                rf[s] = flist[f0 + s < nf ? f0 + s : f0];  // past the end: repeat the first, no output
+                xv[s] = lane < D ? __ldg(p.x + (size_t)rf[s] * D + lane) : 0.0;
             }
-            if (lane == 0) p.a_out[rf] = (uint8_t)b;
+            double q64[TC_FBS][M];
+            route_rows_f64<M, TC_FBS, TC_FBKB, 1>(xv, D, H, p.w1, p.b1, p.w2, M, 1, p.b2, q64);
+#pragma unroll
+            for (int s = 0; s < TC_FBS; ++s) {
+                if (f0 + s >= nf) break;
+                int b = route_argmax<M>(q64[s]);
+                if (p.eps > 0.0) {
+                    P4 rn = philox4x32_10(p.counter, (uint64_t)rf[s], p.seed);
+                    if (u01(rn.x[0], rn.x[1]) < p.eps) b = (int)below(rn.x[2], (uint32_t)M);
+                }
+                if (lane < M && p.q_out) {
+#pragma unroll
+                    for (int m = 0; m < M; ++m)
+                        if (lane == m) p.q_out[(size_t)rf[s] * M + m] = (float)q64[s][m];
+                }
+                if (lane == 0) p.a_out[rf[s]] = (uint8_t)b;
+            }
         }
     };
     // relu + layer 2 of one TC_CW-unit chunk for BOTH states of this lane (u0:
