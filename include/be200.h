@@ -184,7 +184,7 @@ int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers
                           void* stream);
 
 /* The same router on the tensor cores (route_tc.cu): layer 1 as
- * tcgen05.mma.kind::tf32 with a 3xTF32 split over 128-state tiles (TMEM
+ * tcgen05.mma.kind::tf32 with a 3xTF32 split over 256-state tiles (TMEM
  * accumulators, weights staged in shared memory by one bulk async copy),
  * relu + layer 2 in fp32; each greedy decision is certified by an error bound
  * or re-evaluated with the exact arithmetic of be_qnet_route_f64, so actions

@@ -68,7 +68,7 @@ def route(net, x: torch.Tensor, epsilon: float = 0.0, seed: int = 0, counter: in
 class TensorCoreRouter:
     """Batched select_action on the tensor cores (be_qnet_route_tc, route_tc.cu).
 
-    Layer 1 runs as tcgen05 kind::tf32 MMAs (3xTF32 split, 128 states per tile,
+    Layer 1 runs as tcgen05 kind::tf32 MMAs (3xTF32 split, 256 states per tile,
     accumulators in TMEM); every greedy decision is certified by an error bound
     or re-evaluated with the fp64 router's exact arithmetic, so the actions
     equal `route()`'s; Q values are fp32 (within 1e-5 relative).  Owns the
