@@ -491,8 +491,12 @@ template <int M>
 struct QsLayout {
     static constexpr int NV = 2 * M + 1;  // per-hidden-unit values besides the task row
     static constexpr int NQ4 = NV / 2;    // float4 arrays (two values x two units)
-    // floats: task rows [T][H] + values [NV][H] + A [T] + C [M+1] + b2 [M]
-    __host__ __device__ static size_t floats(int T, int H) { return (size_t)(T + NV) * H + T + (M + 1) + M; }
+    // floats: per task [T][H/2] float4 (task-row pair, last-value pair) + the other
+    // values [NQ4][H/2] float4 + A [T] + C [M+1] + b2 [M]; the task row and the last
+    // value share one 16-byte load per unit pair
+    __host__ __device__ static size_t q4_off(int T, int H) { return (size_t)2 * T * H; }
+    __host__ __device__ static size_t bA_off(int T, int H) { return (size_t)(2 * T + 2 * NQ4) * H; }
+    __host__ __device__ static size_t floats(int T, int H) { return bA_off(T, H) + T + (M + 1) + M; }
 };
 
 // Lane g of a group owns hidden-unit pairs (j0, j1) = (g + 2p LPE, g + 2p LPE + LPE),
@@ -514,27 +518,24 @@ __device__ __forceinline__ void stage_qscreen(const double* __restrict__ w1, con
     auto val = [&](int v, int j) -> double {  // v < M: tier inputs, v == M: rate, v > M: W2[j][v-M-1]
         return v <= M ? w1[(size_t)(T + v) * H + j] : w2[(size_t)j * M + (v - M - 1)];
     };
-    float2* tr2 = reinterpret_cast<float2*>(sf);
+    float4* to4 = reinterpret_cast<float4*>(sf);
     for (int k = threadIdx.x; k < T * H2; k += blockDim.x) {
         const int t = k / H2, P = k % H2;
         const int j0 = screen_unit<LPE>(P, 0), j1 = screen_unit<LPE>(P, 1);
-        tr2[k] = make_float2(__double2float_rn(__dadd_rn(w1[(size_t)t * H + j0], b1[j0])),
-                             __double2float_rn(__dadd_rn(w1[(size_t)t * H + j1], b1[j1])));
+        to4[k] = make_float4(__double2float_rn(__dadd_rn(w1[(size_t)t * H + j0], b1[j0])),
+                             __double2float_rn(__dadd_rn(w1[(size_t)t * H + j1], b1[j1])),
+                             __double2float_rn(val(NV - 1, j0)), __double2float_rn(val(NV - 1, j1)));
     }
-    float4* q4 = reinterpret_cast<float4*>(sf + (size_t)T * H);
+    float4* q4 = reinterpret_cast<float4*>(sf + QsLayout<M>::q4_off(T, H));
     for (int k = threadIdx.x; k < NQ4 * H2; k += blockDim.x) {
         const int q = k / H2, P = k % H2;
         const int j0 = screen_unit<LPE>(P, 0), j1 = screen_unit<LPE>(P, 1);
         q4[k] = make_float4(__double2float_rn(val(2 * q, j0)), __double2float_rn(val(2 * q, j1)),
                             __double2float_rn(val(2 * q + 1, j0)), __double2float_rn(val(2 * q + 1, j1)));
     }
-    float2* o2 = reinterpret_cast<float2*>(sf + (size_t)T * H + (size_t)2 * NQ4 * H);
-    for (int P = threadIdx.x; P < H2; P += blockDim.x)
-        o2[P] = make_float2(__double2float_rn(val(NV - 1, screen_unit<LPE>(P, 0))),
-                            __double2float_rn(val(NV - 1, screen_unit<LPE>(P, 1))));
     // bound tables: one warp per row r (task row r < T, else input T + (r - T)),
     // fp64 sums over j, maximum over m, rounded up to fp32
-    float* bA = sf + (size_t)(T + NV) * H;
+    float* bA = sf + QsLayout<M>::bA_off(T, H);
     float* bC = bA + T;
     float* b2f = bC + (M + 1);
     int lg = 0;
@@ -574,10 +575,9 @@ __device__ __forceinline__ bool qnet_screen(const float* __restrict__ sf, int T,
     constexpr int NV = QsLayout<M>::NV, NQ4 = QsLayout<M>::NQ4;
     const int g = threadIdx.x & (LPE - 1);
     const int H2 = H / 2;
-    const float2* tr2 = reinterpret_cast<const float2*>(sf) + (size_t)task * H2;
-    const float4* q4 = reinterpret_cast<const float4*>(sf + (size_t)T * H);
-    const float2* o2 = reinterpret_cast<const float2*>(sf + (size_t)T * H + (size_t)2 * NQ4 * H);
-    const float* bA = sf + (size_t)(T + NV) * H;
+    const float4* to4 = reinterpret_cast<const float4*>(sf) + (size_t)task * H2;
+    const float4* q4 = reinterpret_cast<const float4*>(sf + QsLayout<M>::q4_off(T, H));
+    const float* bA = sf + QsLayout<M>::bA_off(T, H);
     const float* bC = bA + T;
     const float* b2f = bC + (M + 1);
     float x32[M + 1];
@@ -596,8 +596,9 @@ __device__ __forceinline__ bool qnet_screen(const float* __restrict__ sf, int T,
             v[2 * q] = make_float2(w.x, w.y);
             v[2 * q + 1] = make_float2(w.z, w.w);
         }
-        v[NV - 1] = o2[P];
-        float2 pre = tr2[P];
+        const float4 tw = to4[P];
+        v[NV - 1] = make_float2(tw.z, tw.w);
+        float2 pre = make_float2(tw.x, tw.y);
 #pragma unroll
         for (int m = 0; m <= M; ++m) pre = ffma2(make_float2(x32[m], x32[m]), v[m], pre);
         const float2 h = make_float2(fmaxf(pre.x, 0.f), fmaxf(pre.y, 0.f));

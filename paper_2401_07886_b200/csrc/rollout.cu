@@ -325,7 +325,7 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
     size_t s = (sizeof(Score) + 15) & ~size_t(15);
     if (policy && !screen) s += sizeof(double) * ((size_t)(T + 2 * M + 1) * H + M);  // QLayout<M>::doubles
     if (policy && screen)  // QsLayout<M>::floats, rounded to 16 bytes
-        s += sizeof(float) * (((size_t)(T + 2 * M + 1) * H + T + (M + 1) + M + 3) & ~size_t(3));
+        s += sizeof(float) * (((size_t)(2 * T + 2 * M) * H + T + (M + 1) + M + 3) & ~size_t(3));
     s += sizeof(double) * (size_t)skip_rows * SKIP_NB;
     return s;
 }
