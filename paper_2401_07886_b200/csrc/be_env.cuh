@@ -587,7 +587,7 @@ __device__ __forceinline__ bool qnet_screen(const float* __restrict__ sf, int T,
     float2 a[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) a[m] = make_float2(0.f, 0.f);
-#pragma unroll 4
+#pragma unroll 8
     for (int P = g; P < H2; P += LPE) {
         float2 v[NV];
 #pragma unroll

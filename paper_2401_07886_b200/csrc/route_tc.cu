@@ -17,6 +17,12 @@
 //     layer-2 dot products on packed FFMA2 — every W2 shared-memory load feeds
 //     two states; after the second pass the two threads exchange partial sums
 //     in shared memory and each finalizes one state;
+//   * the decision is certified with pairwise error bounds (tc_bound_k1/k2
+//     below; the layer-1 term models each tensor-core accumulation step of 8
+//     products as 9 fp32 roundings of <= 2u each and enters through the W2
+//     column differences); states it cannot certify are re-evaluated four per
+//     warp with route_rows_f64 — the exact arithmetic of be_qnet_route_f64 —
+//     so every greedy decision equals the fp64 router's.
 // Weights are packed once per call (route_tc_pack_kernel: tf32 hi/lo UMMA
 // images of [W1; b1]^T, W2 pairs, bound tables) and staged per CTA with one
 // bulk asynchronous copy (TMA engine, mbarrier completion).  Q values out are
@@ -39,6 +45,7 @@ constexpr int TC_THREADS = 256;  // per TMEM lane two threads (lower / upper), e
 constexpr int TC_CW = 16;     // TMEM columns per tcgen05.ld in the epilogue
 constexpr int TC_K = 16;      // inputs (D <= 15) + the bias input, two tf32 K-steps of 8
 constexpr int TC_MP = 4;      // layer-2 outputs padded (n_tiers <= 4)
+constexpr int TC_NP = TC_MP * (TC_MP - 1) / 2;  // action pairs (b < s) of the pairwise bounds
 constexpr int TC_FBS = 4;     // fp64 fallback: states per warp
 constexpr int TC_FBKB = 4;    // fp64 fallback: hidden units per lane per block
 constexpr int TC_FLIST = 4096;  // deferred fp64 re-evaluations per CTA (shared-memory list)
@@ -50,7 +57,8 @@ struct TcLayout {  // byte offsets inside the packed image (= the shared-memory 
     __host__ __device__ int w2p() const { return 2 * H * TC_K * 4; }         // [H/4][4] float4
     __host__ __device__ int b2() const { return w2p() + (H / 2) * TC_MP * 8; }  // [TC_MP] float
     __host__ __device__ int bound() const { return b2() + TC_MP * 4; }         // [TC_K] float
-    __host__ __device__ int bytes() const { return bound() + TC_K * 4; }       // multiple of 16
+    __host__ __device__ int pairs() const { return bound() + TC_K * 4; }       // [TC_NP][TC_K] float
+    __host__ __device__ int bytes() const { return pairs() + TC_NP * TC_K * 4; }  // multiple of 16
 };
 
 // element (n, k) of a K-major no-swizzle UMMA operand with K = 16: 8 x 16-byte core
@@ -59,14 +67,24 @@ __host__ __device__ __forceinline__ int umma_off(int n, int k) {
     return (n >> 3) * 128 + (k >> 2) * 32 + (n & 7) * 4 + (k & 3);
 }
 
-// error-bound constant K (units of u = 2^-24) for hidden width H: layer 1 = input /
-// weight rounding and the dropped lo.lo term (14) + 6 MMAs x 9 accumulations x 2 (108);
-// layer 2 = FFMA2 chains of <= L = 8 ceil(H / 64) terms (a thread's share of a state:
-// 2 passes x <= ceil(H / 64) chunks of 16 units over 2 sets x 2 lanes) + the
-// lower/upper merge, the lane merge, the set merge and the bias add + W2 rounding
-// (<= L + 7); slack 16
-__host__ __device__ __forceinline__ double tc_bound_k(int H) {
-    return (double)(122 + 8 * ((H + 63) / 64) + 7 + 16) * 0x1p-24;
+// Error bound of the fp32 decision (units of u = 2^-24).  Layer 1: input / weight
+// rounding and the dropped lo.lo term (14) + 6 MMAs x 9 accumulations x 2 (108)
+// bound |h32_j - h_j| <= 122 u P_j, P_j = sum_k |x_k| |W1[k][j]| + |b1[j]|; in the
+// difference q_b - q_s of two actions they enter as sum_j (W2[j][b] - W2[j][s]) dh_j,
+// so with K1 = (122 + 8) u:  K1 sum_j |W2[j][b] - W2[j][s]| P_j.  Layer 2: FFMA2
+// chains of <= L = 8 ceil(H / 64) terms (a thread's share of a state: 2 passes x
+// <= ceil(H / 64) chunks of 16 units over 2 sets x 2 lanes) + the lower/upper merge,
+// the lane merge, the set merge and the bias add + W2 / b2 rounding (<= L + 7),
+// independent per action: K2 = (L + 7 + 16) u times S_m = sum_j |W2[j][m]| P_j + |b2[m]|
+// for each of the two.  The leader b is certified when, for every other action s,
+// q32_b - q32_s > K1 D_bs + 2 K2 max_m S_m (evaluated with upward-rounded fp32 terms
+// and a downward-rounded fp64 difference).
+__host__ __device__ __forceinline__ double tc_bound_k1() { return (double)(122 + 8) * 0x1p-24; }
+__host__ __device__ __forceinline__ double tc_bound_k2(int H) {
+    return (double)(8 * ((H + 63) / 64) + 7 + 16) * 0x1p-24;
+}
+__host__ __device__ constexpr int tc_pair(int b, int s) {  // b < s < TC_MP
+    return b * TC_MP - b * (b + 1) / 2 + (s - b - 1);
 }
 
 template <int M>
@@ -102,27 +120,49 @@ __global__ void __launch_bounds__(256) route_tc_pack_kernel(const double* w1, co
     }
     float* fb2 = img + L.b2() / 4;
     for (int m = tid; m < TC_MP; m += nt) fb2[m] = m < M ? __double2float_rn(b2[m]) : 0.f;
-    // bound tables: C[k] = K max_m sum_j |W2[j][m]| |W1[k][j]| (k < D), C[D] = K max_m
-    // (sum_j |W2[j][m]| |b1[j]| + |b2[m]|); one warp per row k
+    // bound tables, one warp per row: C[k] = 2 K2 max_m sum_j |W2[j][m]| |W1[k][j]|
+    // (k < D), C[D] = 2 K2 max_m (sum_j |W2[j][m]| |b1[j]| + |b2[m]|); pairs
+    // Dp[k] = K1 sum_j |W2[j][b] - W2[j][s]| |W1[k][j]| (k < D), Dp[D] = K1 sum_j
+    // |W2[j][b] - W2[j][s]| |b1[j]|; non-finite weights give NaN (never certified)
     float* C = img + L.bound() / 4;
-    const double K = tc_bound_k(H);
+    float* Dp = img + L.pairs() / 4;
+    const double K1 = tc_bound_k1(), K2 = tc_bound_k2(H);
     const int lane = threadIdx.x & 31, gw = tid >> 5, nw = nt >> 5;
-    for (int k = gw; k < TC_K; k += nw) {
+    for (int row = gw; row < TC_K * (1 + TC_NP); row += nw) {
+        const int k = row % TC_K, pr = row / TC_K - 1;  // pr < 0: the per-action table C
         double mx = 0.0;
         bool bad = false;
-        for (int m = 0; m < M; ++m) {
-            double acc = 0.0;
-            for (int j = lane; j < H; j += 32) {
-                const double a = k < D ? w1[(size_t)k * H + j] : (k == D ? b1[j] : 0.0);
-                acc = __fma_rn(fabs(w2[(size_t)j * M + m]), fabs(a), acc);
-            }
+        if (pr < 0) {
+            for (int m = 0; m < M; ++m) {
+                double acc = 0.0;
+                for (int j = lane; j < H; j += 32) {
+                    const double a = k < D ? w1[(size_t)k * H + j] : (k == D ? b1[j] : 0.0);
+                    acc = __fma_rn(fabs(w2[(size_t)j * M + m]), fabs(a), acc);
+                }
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
-            if (k == D) acc = __dadd_ru(acc, fabs(b2[m]));
-            mx = fmax(mx, acc);
-            bad = bad || acc != acc;
+                for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+                if (k == D) acc = __dadd_ru(acc, fabs(b2[m]));
+                mx = fmax(mx, acc);
+                bad = bad || acc != acc;
+            }
+            if (lane == 0) C[k] = bad ? __int_as_float(0x7fc00000) : __double2float_ru(__dmul_ru(2.0 * K2, mx));
+        } else {
+            int b = 0, sx = 1;  // the pair of index pr
+            for (int q = 0; q < pr; ++q)
+                if (++sx == TC_MP) sx = ++b + 1;
+            double acc = 0.0;
+            if (sx < M) {
+                for (int j = lane; j < H; j += 32) {
+                    const double a = k < D ? w1[(size_t)k * H + j] : (k == D ? b1[j] : 0.0);
+                    acc = __fma_rn(fabs(__dsub_rn(w2[(size_t)j * M + b], w2[(size_t)j * M + sx])), fabs(a), acc);
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+            }
+            // |W2 b - W2 s| is rounded to nearest in fp64: the relative error u_64 is far
+            // inside the slack of K1
+            if (lane == 0) Dp[pr * TC_K + k] = acc != acc ? __int_as_float(0x7fc00000) : __double2float_ru(__dmul_ru(K1, acc));
         }
-        if (lane == 0) C[k] = bad ? __int_as_float(0x7fc00000) : __double2float_ru(__dmul_ru(K, mx));
     }
 }
 
@@ -183,6 +223,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     const float4* W2q = reinterpret_cast<const float4*>(img + L.w2p() / 4);
     const float* fb2 = img + L.b2() / 4;
     const float* C = img + L.bound() / 4;
+    const float* Dp = img + L.pairs() / 4;
     const uint32_t idesc = tc::idesc_tf32(TC_ROWS, HP);
     const int ntiles = (p.B + TC_TILE - 1) / TC_TILE;
     uint32_t phase = 0;
@@ -334,9 +375,22 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
         // decision bound (needs only the inputs): against exact arithmetic on the
         // fp32-rounded inputs; the fp64 inputs differ by <= u |x|, covered by the slack in K
         float Bd = C[D];
+        float Bp[TC_NP > 0 && M > 1 ? M * (M - 1) / 2 : 1];
 #pragma unroll
         for (int k = 0; k < DM; ++k)
             if (k < D) Bd = __fmaf_ru(fabsf(xf[k]), C[k], Bd);
+#pragma unroll
+        for (int b = 0; b < M; ++b)
+#pragma unroll
+            for (int sx = b + 1; sx < M; ++sx) {
+                const int pq = b * (2 * M - b - 1) / 2 + (sx - b - 1);  // dense index among M actions
+                const float* dp = Dp + tc_pair(b, sx) * TC_K;
+                float v = dp[D];
+#pragma unroll
+                for (int k = 0; k < DM; ++k)
+                    if (k < D) v = __fmaf_ru(fabsf(xf[k]), dp[k], v);
+                Bp[pq] = __fadd_ru(v, Bd);
+            }
         tc::fence_proxy_async_smem();
         tc::fence_before_sync();  // the previous tile's TMEM loads are complete
         __syncthreads();
@@ -367,7 +421,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
         {
             float q[M];
             int best = 0;
-            float bv = 0.f, sv = -INFINITY;
+            float bv = 0.f;
             bool fin = true;
 #pragma unroll
             for (int m = 0; m < M; ++m) {
@@ -381,17 +435,24 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
                 const float t0 = __fadd_rn(t[0].x, t[0].y), t1 = __fadd_rn(t[1].x, t[1].y);
                 q[m] = __fadd_rn(__fadd_rn(t0, t1), fb2[m]);
                 fin = fin && isfinite(q[m]);
-                if (m == 0 || q[m] > bv) {
-                    sv = bv;
+                if (m == 0 || q[m] > bv) {  // first maximum (a tie is never certified)
                     best = m;
                     bv = q[m];
-                } else if (q[m] > sv) {
-                    sv = q[m];
                 }
-                if (m == 0) sv = -INFINITY;
             }
-            const bool sure =
-                M == 1 || (fin && isfinite(Bd) && __dsub_rd((double)bv, (double)sv) > 2.0 * (double)Bd);
+            // every other action must trail the leader by more than the pair's bound
+            bool sure = fin;
+#pragma unroll
+            for (int b = 0; b < M; ++b)
+#pragma unroll
+                for (int sx = b + 1; sx < M; ++sx) {
+                    const int pq = b * (2 * M - b - 1) / 2 + (sx - b - 1);
+                    if (best == b || best == sx) {
+                        const float other = best == b ? q[sx] : q[b];
+                        sure = sure && isfinite(Bp[pq]) && __dsub_rd((double)bv, (double)other) > (double)Bp[pq];
+                    }
+                }
+            sure = M == 1 || sure;
             if (valid) {
                 ++n_rows;
                 if (!sure) {
