@@ -49,6 +49,25 @@ def test_random_nets_match_fp64_router(cuda, seed):
     assert n == 100_003 and fb < n
 
 
+@pytest.mark.parametrize("M,spread", [(3, 1e-3), (3, 1e-5), (4, 1e-4), (2, 1e-6)])
+def test_correlated_columns_near_ties(cuda, M, spread):
+    """W2 columns that differ by `spread` (as trained Q heads do, only more so):
+    the margins are tiny, the per-action error bound would certify almost nothing,
+    and the pairwise bound (layer-1 error through the column differences) decides
+    most states on the tensor cores. Every action must still equal fp64's."""
+    rng = np.random.default_rng(int(spread * 1e7) + M)
+    T = 4
+    net = QNetwork.init_random(T, M, 256, rng)
+    base = rng.normal(0, 0.1, 256)
+    net.w2 = base[:, None] + spread * rng.normal(0, 0.1, (256, M))
+    net.b1 = rng.normal(0, 0.1, 256)
+    net.b2 = spread * rng.normal(0, 0.1, M)
+    n, fb = compare(net, random_states(rng, 60_001, T, M), cuda)
+    assert n == 60_001
+    if spread >= 1e-3:
+        assert fb < n // 2, f"pairwise bound certified only {n - fb} of {n}"
+
+
 def test_trained_policy_states_match_fp64_and_reference(cuda):
     """States the reference visited with its trained policy: actions equal the
     fp64 router's and the reference's own decisions (goldens carry the fp64
