@@ -284,6 +284,21 @@ def router_probe(dev):
                actions_identical_to_fp64=bool(torch.equal(a0, a1)),
                kernel="route_tc_kernel<3, 8>: tcgen05.mma.kind::tf32 (3xTF32) layer 1, FFMA2 layer 2, "
                       "certified decisions + fp64 re-evaluation")
+    # tensor roofline of layer 1: per state 3 MMAs (3xTF32) x 2 x K (16: 8 inputs + bias,
+    # padded) x H flops issued to the tensor cores; peak = tf32 dense = half the measured
+    # bf16 burst rate (B200 tf32:bf16 = 1:2); algorithmic flops 2 (D H + H M) per state
+    H = int(net.w1.shape[1])
+    try:
+        bf16 = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"])
+        src = "MEASURED_PEAKS.json bf16_tflops / 2"
+    except (OSError, KeyError, ValueError):
+        bf16, src = 2250.0, "nominal dense bf16 2.25 PF / 2"
+    tc_tf = B * 3 * 2 * 16 * H / (ms_tc / 1e3) / 1e12
+    out["roofline"] = dict(bound="tensor", achieved=tc_tf, peak=bf16 / 2, unit="TFLOP/s",
+                           frac=tc_tf / (bf16 / 2), peak_source=src,
+                           algorithmic_tflops=B * 2 * (x.shape[1] * H + H * 3) / (ms_tc / 1e3) / 1e12,
+                           note="the kernel is bound by its CUDA-core epilogue (relu + layer 2 + "
+                                "certification), not the tensor pipe; DESIGN.md 4.4")
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         k = json.load(open(prof)).get("kernels", {}).get("route_tc")
