@@ -49,7 +49,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--envs", type=int, default=65536, help="environments per GPU")
+    ap.add_argument("--envs", type=int, default=65536,
+                    help="total environments, sharded across the GPUs by global id (config 4)")
+    ap.add_argument("--envs-per-gpu", type=int, default=0,
+                    help="weak scaling instead: this many environments on every GPU")
+    ap.add_argument("--parity-envs", type=int, default=64,
+                    help="strided envs (whole job) re-run by the oracle and compared bit for bit")
+    ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling extra")
     ap.add_argument("--requests", type=int, default=10000)
     ap.add_argument("--seed", type=int, default=2401)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -65,9 +71,10 @@ def load_rates(gids):
 
 # ----------------------------------------------------------------- CPU side
 def _ref_worker(args):
-    """One host process: the reference run_eval over a slice of env traces."""
-    (arrs, tasks, rates, deadline_s, ref_path) = args
-    import numpy as np  # noqa: F401
+    """One host process: the reference run_eval over a slice of env traces.
+    Returns (env-steps, seconds, [(sample index, tier u8, reward f64, miss bool)])."""
+    (idx, arrs, tasks, rates, deadline_s, ref_path) = args
+    import numpy as np
     sys.path.insert(0, ref_path)
     from besteffort.config import parse_config
     from besteffort.evalkit import run_eval
@@ -75,36 +82,43 @@ def _ref_worker(args):
     from besteffort.workload import ArrivalEvent, SegmentMark, WorkloadTrace
     cfg = parse_config()
     net = load_checkpoint(POLICY)
-    steps = 0
+    spec = cfg.reward_spec()
+    dl = np.array([t.deadline_ms_per_token for t in spec.tasks])
+    steps, outs = 0, []
     t0 = time.perf_counter()
-    for a, k, r in zip(arrs, tasks, rates):
+    for i, a, k, r in zip(idx, arrs, tasks, rates):
         tr = WorkloadTrace([ArrivalEvent(float(x), int(y)) for x, y in zip(a, k)],
                            [SegmentMark(0, float(r))], seed=0)
-        run_eval(net, tr, cfg.tiers(), cfg.reward_spec(), cfg.encoding(),
-                 estimator_mode="true-rate")
+        run = run_eval(net, tr, cfg.tiers(), spec, cfg.encoding(), estimator_mode="true-rate")
         steps += len(a)
+        outs.append((i, np.array([q.tier_id for q in run.records], np.uint8),
+                     np.array([q.reward for q in run.records]),
+                     np.array([q.realized_ms_per_token for q in run.records]) > dl[k]))
         if time.perf_counter() - t0 > deadline_s:
             break
-    return steps, time.perf_counter() - t0
+    return steps, time.perf_counter() - t0, outs
 
 
 def _oracle_worker(args):
-    (arrs, tasks, rates, deadline_s, _) = args
+    (idx, arrs, tasks, rates, deadline_s, _) = args
     import numpy as np
     sys.path.insert(0, ROOT)
     from oracle import oracle
     from paper_2401_07886_b200.specs import DEFAULT_TIERS, load_checkpoint, RewardSpec
     net = load_checkpoint(POLICY)
     rw = RewardSpec.default()
-    steps = 0
+    dl = np.array([t.deadline_ms_per_token for t in rw.tasks])
+    steps, outs = 0, []
     t0 = time.perf_counter()
-    for a, k, r in zip(arrs, tasks, rates):
-        oracle.run_eval_oracle(tiers=DEFAULT_TIERS, reward=rw, arrival=a, task=k, seg_start=[0],
-                               seg_rate=[r], net=net, estimator_mode="true-rate", want_steps=False)
+    for i, a, k, r in zip(idx, arrs, tasks, rates):
+        o = oracle.run_eval_oracle(tiers=DEFAULT_TIERS, reward=rw, arrival=a, task=k, seg_start=[0],
+                                   seg_rate=[r], net=net, estimator_mode="true-rate",
+                                   want_steps=False)
         steps += len(a)
+        outs.append((i, o["tier"], o["reward"], o["realized"] > dl[k]))
         if time.perf_counter() - t0 > deadline_s:
             break
-    return steps, time.perf_counter() - t0
+    return steps, time.perf_counter() - t0, outs
 
 
 def host_traces(n_envs, n, seed, gid0=0):
@@ -130,32 +144,61 @@ def host_traces(n_envs, n, seed, gid0=0):
     return out
 
 
-def cpu_rollout(samples, seconds, procs=None):
-    """Time the reference CPU path on `procs` host processes (one per core)."""
+def cpu_rollout(samples, seconds, procs=None, oracle_only=False):
+    """Time the reference CPU path on `procs` host processes (one per core).
+    Returns the cpu_baseline dict plus "outputs": {sample index: (tier, reward, miss)}
+    of every env a worker finished (checked against the GPU by `compare`)."""
     import multiprocessing as mp
     ref = os.path.join(ROOT, "baseline", "_ref")
-    kind = "reference" if os.path.isdir(os.path.join(ref, "besteffort")) else "port"
+    kind = "reference" if os.path.isdir(os.path.join(ref, "besteffort")) and not oracle_only else "port"
     worker = _ref_worker if kind == "reference" else _oracle_worker
-    procs = procs or len(os.sched_getaffinity(0))
+    procs = max(1, min(procs or len(os.sched_getaffinity(0)), len(samples)))
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     os.environ["OMP_NUM_THREADS"] = "1"
-    chunks = [([], [], []) for _ in range(procs)]
+    chunks = [([], [], [], []) for _ in range(procs)]
     for i, (a, k, r) in enumerate(samples):
         c = chunks[i % procs]
-        c[0].append(a)
-        c[1].append(k)
-        c[2].append(r)
+        c[0].append(i)
+        c[1].append(a)
+        c[2].append(k)
+        c[3].append(r)
     ctx = mp.get_context("spawn")
     with ctx.Pool(procs) as pool:
         pool.map(abs, range(procs))  # warm the workers (imports happen per task below)
         t0 = time.perf_counter()
-        res = pool.map(worker, [(c[0], c[1], c[2], seconds, ref) for c in chunks])
+        res = pool.map(worker, [(c[0], c[1], c[2], c[3], seconds, ref) for c in chunks])
         wall = time.perf_counter() - t0
-    steps = sum(s for s, _ in res)
+    steps = sum(r[0] for r in res)
+    outputs = {i: (t, w, m) for r in res for (i, t, w, m) in r[2]}
     return dict(value=steps / wall, unit="env-steps/s", cores=procs, kind=kind,
-                sample=f"{steps} env-steps ({len(samples)} envs max, 10k requests each, "
-                       f"load 1x-10x) on {procs} processes, {wall:.1f}s wall, "
-                       f"{'besteffort.run_eval (baseline/_ref)' if kind == 'reference' else 'oracle C port'}")
+                sample=f"{steps} env-steps ({len(outputs)} of {len(samples)} envs finished, "
+                       f"{len(samples[0][0])} requests each, load 1x-10x) on {procs} processes, "
+                       f"{wall:.1f}s wall, "
+                       f"{'besteffort.run_eval (baseline/_ref)' if kind == 'reference' else 'oracle C port'}",
+                outputs=outputs)
+
+
+def compare(outputs, env_index, flags, reward):
+    """Bit-exact parity of GPU rollout records against CPU outputs.
+    outputs: {sample index: (tier u8, reward f64, miss bool)}; env_index[i] = local env
+    row of sample i; flags/reward: host copies of those rows.  Returns
+    (envs compared, requests compared, mismatching requests, first mismatch)."""
+    import numpy as np
+    envs = reqs = bad = 0
+    first = None
+    for i, (tier, rw, miss) in sorted(outputs.items()):
+        n = tier.size
+        f = flags[env_index[i], :n]
+        g_rw = reward[env_index[i], :n]
+        ok = ((f & 0x3F) == tier) & (g_rw.view(np.int64) == rw.view(np.int64)) & \
+            (((f >> 7) & 1).astype(bool) == miss)
+        envs += 1
+        reqs += n
+        nbad = int(n - ok.sum())
+        if nbad and first is None:
+            first = dict(env=int(env_index[i]), request=int(np.argmin(ok)))
+        bad += nbad
+    return envs, reqs, bad, first
 
 
 def run_reference(a):
@@ -170,13 +213,16 @@ def run_reference(a):
         r = cpu_rollout(samples, seconds, procs)
         if i >= a.warmup:
             per_step.append(r)
+    for r in per_step:
+        r.pop("outputs", None)
     v = statistics.median(r["value"] for r in per_step)
     line = dict(metric="simulated env-steps/sec (greedy DQN rollout, 65536 envs)", value=v,
                 unit="env-steps/s", impl="reference", n_gpus=a.gpus, steps=a.steps,
-                warmup=a.warmup, higher_is_better=True, scaling="weak", vs_baseline=None,
-                dtype="f64", data="synthetic",
-                config=dict(workload="config4: 65536 envs/GPU x 10k requests, stable Poisson at "
-                                     "1x-10x of 3 req/s, 3 tiers x 4 replicas, 4 tasks, trained DQN",
+                warmup=a.warmup, higher_is_better=True,
+                scaling="weak" if a.envs_per_gpu else "strong", vs_baseline=None,
+                dtype="f64", data="synthetic (host PCG64 gen_stable traces; reference-trained DQN)",
+                config=dict(workload=workload_text(a.envs_per_gpu * a.gpus if a.envs_per_gpu
+                                                   else a.envs, a.requests, a.gpus, a.envs_per_gpu),
                             sample_per_step=per_step[-1]["sample"]),
                 cpu_baseline=dict(value=v, unit="env-steps/s", cores=per_step[-1]["cores"],
                                   kind=per_step[-1]["kind"], sample=per_step[-1]["sample"]),
@@ -355,6 +401,85 @@ class ClockSampler:
                     reasons=sorted(reasons), samples=len(sm))
 
 
+def workload_text(E_total, N, world, per_gpu):
+    return (f"config4: {E_total} envs x {N} requests "
+            f"({'weak: ' + str(per_gpu) + ' envs per GPU' if per_gpu else 'sharded by global env id across the GPUs'}), "
+            f"stable Poisson at 1x-10x of {LOAD_BASE:g} req/s, 3 tiers x 4 replicas, 4 tasks, "
+            "hard 40 ms/token, true-rate estimator, greedy trained DQN (fp64 decisions)")
+
+
+def env_slice(a, world, rank):
+    """(local envs, first global env id, total envs, scaling): config 4 shards the
+    65,536 envs across the GPUs (strong); --envs-per-gpu gives weak scaling."""
+    from paper_2401_07886_b200 import sharding
+    if a.envs_per_gpu:
+        return a.envs_per_gpu, rank * a.envs_per_gpu, world * a.envs_per_gpu, "weak"
+    lo, hi = sharding.shard_range(a.envs, world, rank)
+    return hi - lo, lo, a.envs, "strong"
+
+
+class Rollout:
+    """One GPU's share of the bench workload: device traces (Philox, keyed by global
+    env id, so env k is the same for any GPU count), the fused rollout and the reducer."""
+
+    def __init__(self, E, gid0, N, seed, dev, ring_capacity=None):
+        from paper_2401_07886_b200 import (GreedyRollout, RewardSpec, StateEncoding, TraceBatch,
+                                           default_tiers, load_checkpoint)
+        self.E, self.gid0, self.N = E, gid0, N
+        gids = list(range(gid0, gid0 + E))
+        self.tiers, self.rw = default_tiers(), RewardSpec.default()
+        self.enc = StateEncoding(N_TASKS, tuple(float(t.max_batch) for t in self.tiers))
+        self.net = load_checkpoint(POLICY)
+        self.tb = TraceBatch.generate_stable(load_rates(gids), N, N_TASKS, seed, device=dev,
+                                             buckets=[g % N_LOADS for g in gids], env_offset=gid0)
+        self.ro = GreedyRollout(self.tiers, self.rw, E, N, self.enc, estimator_mode="true-rate",
+                                want_realized=False, device=dev, ring_capacity=ring_capacity)
+
+    def step(self):
+        from paper_2401_07886_b200 import reduce_eval
+        o = self.ro.launch(self.tb, self.net)
+        return o, reduce_eval(self.tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
+
+    def timed(self, warmup, steps, world, stream, clk_index=None):
+        """W warm-up steps, then exactly K steps between barrier + synchronize;
+        per-kernel CUDA events on the launching stream."""
+        import torch
+        import torch.distributed as dist
+        self.ro.run(self.tb, self.net)  # settles the ("auto") replica ring capacity; warm-up 1
+        for _ in range(warmup - 1):
+            self.step()
+        self.ro.env.check()
+        self.ro.env.screen_stats(reset=True)
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(clk_index) if clk_index is not None else None
+        if clk:
+            clk.__enter__()
+        t0.record(stream)
+        red = out = None
+        from paper_2401_07886_b200 import reduce_eval
+        for k in range(steps):
+            ev[k][0].record(stream)
+            out = self.ro.launch(self.tb, self.net)
+            ev[k][1].record(stream)
+            red = reduce_eval(self.tb, out.flags, out.reward, THRESHOLDS, N_LOADS)
+            ev[k][2].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if clk:
+            clk.__exit__(None, None, None)
+        if world > 1:
+            dist.barrier()
+        self.ro.env.check()
+        self.rollout_ms = [e[0].elapsed_time(e[1]) for e in ev]
+        self.reduce_ms = [e[1].elapsed_time(e[2]) for e in ev]
+        return t0.elapsed_time(t1), out, red, clk
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -376,68 +501,60 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    from paper_2401_07886_b200 import (GreedyRollout, RewardSpec, StateEncoding, TraceBatch,
-                                       default_tiers, load_checkpoint, reduce_eval)
     from paper_2401_07886_b200.evalkit import StreamingEvaluator, pin_trace
     from paper_2401_07886_b200 import sharding
 
-    E, N = a.envs, a.requests
-    gid0 = rank * E
-    gids = list(range(gid0, gid0 + E))
-    tiers, rw = default_tiers(), RewardSpec.default()
-    enc = StateEncoding(N_TASKS, tuple(float(t.max_batch) for t in tiers))
-    net = load_checkpoint(POLICY)
-    tb = TraceBatch.generate_stable(load_rates(gids), N, N_TASKS, a.seed, device=dev,
-                                    buckets=[g % N_LOADS for g in gids], env_offset=gid0)
-    ro = GreedyRollout(tiers, rw, E, N, enc, estimator_mode="true-rate", want_realized=False,
-                       device=dev, ring_capacity=a.ring_capacity or None)
+    E, gid0, E_total, scaling = env_slice(a, world, rank)
+    N = a.requests
+    bench = Rollout(E, gid0, N, a.seed, dev, ring_capacity=a.ring_capacity or None)
     stream = torch.cuda.current_stream(dev)
-
-    def step():
-        o = ro.launch(tb, net)
-        return o, reduce_eval(tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
-
-    ro.run(tb, net)  # settles the ("auto") replica ring capacity; counts as warm-up
-    for _ in range(a.warmup - 1):
-        step()
-    ro.env.check()
-    ro.env.screen_stats(reset=True)
-    torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record(stream)
-        for k in range(a.steps):
-            ev[k][0].record(stream)
-            o = ro.launch(tb, net)
-            ev[k][1].record(stream)
-            red = reduce_eval(tb, o.flags, o.reward, THRESHOLDS, N_LOADS)
-            ev[k][2].record(stream)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ro.env.check()
-    n_screened, n_fallback = ro.env.screen_stats(reset=True)
-    ms = t_start.elapsed_time(t_end)
-    rollout_ms = [e[0].elapsed_time(e[1]) for e in ev]
-    reduce_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    ms, o, red, clk = bench.timed(a.warmup, a.steps, world, stream, clk_index=local)
+    n_screened, n_fallback = bench.ro.env.screen_stats(reset=True)
     ms = sharding.max_over_ranks(ms, dev) if world > 1 else ms
     ms_step = ms / a.steps
-    value = world * E * N / (ms_step / 1e3)
+    value = E_total * N / (ms_step / 1e3)
     stats = sharding.reduce_stats(red, dev) if world > 1 else red.totals()
+    flags_h = o.flags.cpu().numpy()
+    reward_h = o.reward.cpu().numpy()
+    clocks = clk.summary()
+
+    # ------------------------------------------------ parity vs the oracle (strided envs)
+    procs_all = len(os.sched_getaffinity(0))
+    n_par = max(4, min(E, a.parity_envs // world))
+    rows = np.unique(np.linspace(0, E - 1, n_par).round().astype(int))
+    arr_h = bench.tb.arrival[rows].cpu().numpy()
+    tsk_h = bench.tb.task[rows].cpu().numpy()
+    psamples = [(arr_h[i], tsk_h[i], load_rates([gid0 + int(r)])[0]) for i, r in enumerate(rows)]
+    pr = cpu_rollout(psamples, 1e9, max(1, procs_all // world), oracle_only=True)
+    p_envs, p_reqs, p_bad, p_first = compare(pr["outputs"], rows, flags_h, reward_h)
+    if world > 1:
+        t = torch.tensor([p_envs, p_reqs, p_bad], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        p_envs, p_reqs, p_bad = (int(x) for x in t.tolist())
+    parity = dict(envs=p_envs, requests=p_reqs, mismatches=p_bad, first_mismatch=p_first,
+                  checker="oracle C port (oracle/env_oracle.c), strided env sample across every "
+                          "rank's shard; tier, miss flag and reward compared bit for bit")
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        # the same workload bits: device-generated traces of the first envs, through the
+        # unmodified reference (baseline/_ref) or the C port, timed on all host cores;
+        # every env the CPU finishes is also checked against the GPU records
+        nb = min(E, procs_all * 24)
+        arr_c = bench.tb.arrival[:nb].cpu().numpy()
+        tsk_c = bench.tb.task[:nb].cpu().numpy()
+        samples = [(arr_c[i], tsk_c[i], load_rates([gid0 + i])[0]) for i in range(nb)]
+        cpu = cpu_rollout(samples, a.cpu_seconds, procs_all)
+        c_envs, c_reqs, c_bad, c_first = compare(cpu.pop("outputs"), np.arange(nb), flags_h, reward_h)
+        cpu["parity"] = dict(envs=c_envs, requests=c_reqs, mismatches=c_bad, first_mismatch=c_first)
 
     # ------------------------------------------------ end to end (host buffers)
-    host = pin_trace(tb)
-    se = StreamingEvaluator(net, tiers, rw, E, N, enc, estimator_mode="true-rate",
-                            thresholds=THRESHOLDS, n_buckets=N_LOADS, device=dev,
-                            ring_capacity=ro.ring_capacity)
-    se.result(se.submit(host))  # warm
+    host = pin_trace(bench.tb)
+    se = StreamingEvaluator(bench.net, bench.tiers, bench.rw, E, N, bench.enc,
+                            estimator_mode="true-rate", thresholds=THRESHOLDS, n_buckets=N_LOADS,
+                            device=dev, ring_capacity=bench.ro.ring_capacity)
+    e2e_red = se.result(se.submit(host))  # warm
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -446,16 +563,23 @@ def main():
     gc.collect()
     gc.disable()
     t0 = time.perf_counter()
-    hs = [se.submit(host) for _ in range(a.steps)]
-    for h in hs:
-        se.result(h)
+    pending = []
+    for _ in range(a.steps):
+        if len(pending) >= 2:  # two batches in flight: the double-buffered upload slots
+            e2e_red = se.result(pending.pop(0))
+        pending.append(se.submit(host))
+    for h in pending:
+        e2e_red = se.result(h)
     e2e_s = time.perf_counter() - t0
     gc.enable()
+    e2e_same = e2e_red.totals() == red.totals()
     e2e_s = sharding.max_over_ranks(e2e_s, dev) if world > 1 else e2e_s
-    e2e = dict(value=world * E * N * a.steps / e2e_s, unit="env-steps/s",
+    e2e = dict(value=E_total * N * a.steps / e2e_s, unit="env-steps/s",
                h2d_bytes_per_step=se.h2d_bytes, d2h_bytes_per_step=se.d2h_bytes,
-               note="pinned host traces -> H2D (copy stream, double-buffered) -> fused rollout "
-                    "-> reducer -> D2H of the statistics, host wall clock incl. syncs")
+               stats_identical_to_resident_run=bool(e2e_same),
+               note="pinned host traces -> H2D (copy stream, double-buffered, streamed per env "
+                    "chunk) -> fused rollout -> reducer -> D2H of the statistics; <= 2 batches "
+                    "in flight; host wall clock incl. syncs, max over ranks")
     del se, host
 
     # ------------------------------------------------ roofline (rollout = dominant kernel)
@@ -465,13 +589,12 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    r_ms = statistics.mean(rollout_ms)
+    peak_src = "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    r_ms = statistics.mean(bench.rollout_ms)
     achieved = ALG_BYTES_STEP * E * N / (r_ms / 1e3) / 1e9
     traffic = None
     issue = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    clocks = clk.summary()
     if os.path.exists(prof):
         pj = json.load(open(prof))
         k = pj.get("kernels", {}).get("rollout", {})
@@ -488,44 +611,46 @@ def main():
                              warp_inst_per_env_step=per_step,
                              source=f"smsp__inst_executed.sum of {k.get('source', 'ncu')} ({k.get('tag')}) "
                                     f"x live steps/s; peak = {sms} SMs x 4 schedulers x sampled SM clock")
-    red_ms = statistics.mean(reduce_ms)
+    red_ms = statistics.mean(bench.reduce_ms)
     red_gbs = ALG_BYTES_REDUCE * E * N / (red_ms / 1e3) / 1e9
+
+    # ------------------------------------------------ weak-scaling extra (N > 1 only)
+    weak = None
+    if world > 1 and not a.envs_per_gpu and not a.no_weak:
+        del bench
+        wk = Rollout(a.envs, rank * a.envs, N, a.seed, dev)
+        wms, _, _, _ = wk.timed(3, max(3, min(a.steps, 5)), world, stream)
+        wms = sharding.max_over_ranks(wms, dev) / max(3, min(a.steps, 5))
+        weak = dict(envs_per_gpu=a.envs, value=world * a.envs * N / (wms / 1e3), ms_per_step=wms,
+                    unit="env-steps/s")
+        del wk
 
     train = None if a.no_training else training_probe(dev, world)
     router = None if a.no_training else router_probe(dev)
-
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        procs = len(os.sched_getaffinity(0))
-        # the same workload bits: device-generated traces of the first envs
-        arr = tb.arrival[: procs * 24].cpu().numpy()
-        tsk = tb.task[: procs * 24].cpu().numpy()
-        samples = [(arr[i], tsk[i], load_rates([i])[0]) for i in range(arr.shape[0])]
-        cpu = cpu_rollout(samples, a.cpu_seconds, procs)
 
     if rank == 0:
         line = dict(
             metric="simulated env-steps/sec (greedy DQN rollout, 65536 envs)", value=value,
             unit="env-steps/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
-            ms_per_step=ms_step, higher_is_better=True, scaling="weak", vs_baseline=None,
+            ms_per_step=ms_step, higher_is_better=True, scaling=scaling, vs_baseline=None,
             dtype="f64", data="synthetic (on-device Philox gen_stable traces; reference-trained DQN)",
-            config=dict(workload=f"config4: {E} envs/GPU x {N} requests, stable Poisson at "
-                                 f"1x-10x of {LOAD_BASE:g} req/s, 3 tiers x 4 replicas, 4 tasks, "
-                                 "hard 40 ms/token, true-rate estimator, greedy trained DQN (fp64)",
-                        envs_per_gpu=E, requests_per_env=N, total_envs=world * E,
-                        parallelism=f"env-sharded dp{world}", l2="inputs larger than L2 (5.9 GB traces/GPU)",
+            config=dict(workload=workload_text(E_total, N, world, a.envs_per_gpu),
+                        total_envs=E_total, envs_per_gpu=E, requests_per_env=N,
+                        parallelism=f"env-sharded dp{world} (no data-path collective)",
+                        l2=f"inputs larger than L2 ({E * N * 9 / 1e9:.1f} GB traces/GPU)",
                         step="fused rollout kernel + evaluation reducer"),
             gpu_launches=3 * a.steps,  # per step: stage_qpack_kernel, rollout_kernel, reduce_kernel
+            parity=parity,
             roofline=dict(bound="hbm", achieved=achieved, peak=hbm_peak, unit="GB/s",
                           frac=achieved / hbm_peak, traffic=traffic, peak_source=peak_src,
-                          kernel="rollout_kernel<3>", algorithmic_bytes_per_env_step=ALG_BYTES_STEP,
+                          kernel="rollout_kernel", algorithmic_bytes_per_env_step=ALG_BYTES_STEP,
                           note="env step is issue/latency-bound (serial fp64 event recurrence), "
                                "not HBM-bound; see DESIGN.md §5"),
             reducer_roofline=dict(bound="hbm", achieved=red_gbs, peak=hbm_peak, unit="GB/s",
                                   frac=red_gbs / hbm_peak, ms=red_ms,
                                   algorithmic_bytes_per_request=ALG_BYTES_REDUCE),
             kernel_ms=dict(rollout=r_ms, reduce=red_ms),
-            issue_roofline=issue, training=train, router=router,
+            issue_roofline=issue, weak_scaling=weak, training=train, router=router,
             q_screen=dict(decisions=n_screened, fp64_fallbacks=n_fallback,
                           fallback_frac=n_fallback / max(n_screened, 1),
                           note="certified fp32 decision screen (FFMA2) with exact fp64 fallback; "

@@ -176,6 +176,14 @@ int32_t be_rollout_greedy(be_env* env, const be_trace_soa* trace, const be_qweig
                           int32_t static_tier, const uint8_t* forced_action, be_records* rec,
                           void* stream);
 
+/* What the last be_rollout_greedy on this handle launched (host-side record,
+ * no sync): out[0] = n_tiers (template M), [1] lanes per env (16 | 32),
+ * [2] 1 = true-rate estimator variant, [3] 1 = the throughput variant
+ * (BE_ROLLOUT_MINB CTAs/SM, fewer registers; chosen when the batch fills them),
+ * [4] 1 = skip table staged in shared memory (0 = read through L1),
+ * [5] 1 = certified fp32 decision screen, [6] resident CTAs per SM, [7] CTAs. */
+int32_t be_env_rollout_plan(const be_env* env, int32_t* out /* [8] */);
+
 /* Batched router: q = relu(x W1 + b1) W2 + b2; action = argmax (first max),
  * or uniform random with probability epsilon (Philox4x32-10). x: [B][D]. */
 int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers,

@@ -263,6 +263,12 @@ int32_t be_env_screen_stats(be_env* env, int64_t* out, int32_t reset) {
     return BE_OK;
 }
 
+int32_t be_env_rollout_plan(const be_env* env, int32_t* out) {
+    if (!env || !out) return set_error(BE_EINVAL, "NULL argument");
+    for (int k = 0; k < 8; ++k) out[k] = env->last_plan[k];
+    return BE_OK;
+}
+
 int32_t be_rollout_greedy(be_env* env, const be_trace_soa* trace, const be_qweights* W,
                           int32_t static_tier, const uint8_t* forced_action, be_records* rec,
                           void* stream) {

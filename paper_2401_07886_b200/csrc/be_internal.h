@@ -30,6 +30,7 @@ struct be_env {
     int32_t skip_rows;
     unsigned long long* d_screen;  // [2] screened decisions, fp64 fallbacks (rollout)
     double* d_qpack;    // packed fp64 Q weights for the screened rollout's fallback (max size)
+    int32_t last_plan[8];  // be_env_rollout_plan: what the last be_rollout_greedy launched
 };
 
 namespace be {

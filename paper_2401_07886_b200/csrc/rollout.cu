@@ -331,7 +331,7 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
 }
 
 template <int M, int LPE>
-static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
+static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms, int32_t* plan) {
     // the throughput variant once the batch fills BE_ROLLOUT_MINB CTAs on every SM
     const bool many = (long long)p.E >= (long long)sms * BE_ROLLOUT_MINB * (BE_ROLLOUT_THREADS / LPE);
     auto kern = !p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 0, 0>
@@ -354,19 +354,23 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
     kern<<<(unsigned)blocks, threads, smem, st>>>(p);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "rollout launch");
+    const int32_t pl[8] = {M, LPE, p.cfg.estimator_true_rate ? 1 : 0,
+                           (p.cfg.estimator_true_rate && many) ? 1 : 0, p.skip_smem, p.screen, per_sm,
+                           (int32_t)blocks};
+    for (int k = 0; k < 8; ++k) plan[k] = pl[k];
     return BE_OK;
 }
 
 template <int M>
-static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms) {
+static int launch_rollout_lpe(const RolloutParams& p, size_t smem, cudaStream_t st, int sms, int32_t* plan) {
     if (p.screen) {
         stage_qpack_kernel<M><<<QPACK_CTAS, 256, 0, st>>>(p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H,
                                                  const_cast<double*>(p.qpack));
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
     }
-    if (p.R <= 16 && (p.H == 0 || p.H % 32 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms);
-    return launch_rollout_m<M, 32>(p, smem, st, sms);
+    if (p.R <= 16 && (p.H == 0 || p.H % 32 == 0)) return launch_rollout_m<M, 16>(p, smem, st, sms, plan);
+    return launch_rollout_m<M, 32>(p, smem, st, sms, plan);
 }
 
 int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, int static_tier,
@@ -426,14 +430,14 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     cudaError_t e = cudaMemsetAsync(env->d_counter, 0, sizeof(int32_t), st);
     if (e != cudaSuccess) return set_cuda_error(e, "memset counter");
     switch (M) {
-        case 1: return launch_rollout_lpe<1>(p, smem, st, env->sms);
-        case 2: return launch_rollout_lpe<2>(p, smem, st, env->sms);
-        case 3: return launch_rollout_lpe<3>(p, smem, st, env->sms);
-        case 4: return launch_rollout_lpe<4>(p, smem, st, env->sms);
-        case 5: return launch_rollout_lpe<5>(p, smem, st, env->sms);
-        case 6: return launch_rollout_lpe<6>(p, smem, st, env->sms);
-        case 7: return launch_rollout_lpe<7>(p, smem, st, env->sms);
-        case 8: return launch_rollout_lpe<8>(p, smem, st, env->sms);
+        case 1: return launch_rollout_lpe<1>(p, smem, st, env->sms, env->last_plan);
+        case 2: return launch_rollout_lpe<2>(p, smem, st, env->sms, env->last_plan);
+        case 3: return launch_rollout_lpe<3>(p, smem, st, env->sms, env->last_plan);
+        case 4: return launch_rollout_lpe<4>(p, smem, st, env->sms, env->last_plan);
+        case 5: return launch_rollout_lpe<5>(p, smem, st, env->sms, env->last_plan);
+        case 6: return launch_rollout_lpe<6>(p, smem, st, env->sms, env->last_plan);
+        case 7: return launch_rollout_lpe<7>(p, smem, st, env->sms, env->last_plan);
+        case 8: return launch_rollout_lpe<8>(p, smem, st, env->sms, env->last_plan);
         default: return set_error(BE_EINVAL, "n_tiers out of range");
     }
 }

@@ -143,6 +143,14 @@ class EnvBatch:
         _lib.check(self._L.be_env_screen_stats(self._h, out, 1 if reset else 0))
         return int(out[0]), int(out[1])
 
+    def rollout_plan(self) -> dict:
+        """What the last fused rollout on this handle launched (be_env_rollout_plan)."""
+        out = (ctypes.c_int32 * 8)()
+        _lib.check(self._L.be_env_rollout_plan(self._h, out))
+        keys = ("n_tiers", "lanes_per_env", "true_rate", "throughput_variant", "skip_smem",
+                "screen", "ctas_per_sm", "ctas")
+        return dict(zip(keys, (int(x) for x in out)))
+
     def reset(self, mask: Optional[torch.Tensor] = None, stream=None) -> None:
         _lib.check(self._L.be_env_reset(self._h, _lib.ptr(mask), _lib.stream_ptr(stream)))
 

@@ -82,17 +82,38 @@ def test_peer_exchange_two_processes_matches_allreduce(cuda):
             assert np.array_equal(a, b)
 
 
-def test_bench_two_ranks_one_gpu(cuda, tmp_path):
-    env = dict(os.environ, BE_DIST_BACKEND="gloo", OMP_NUM_THREADS="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--steps", "2", "--warmup", "3", "--envs", "2048", "--requests", "2000",
-           "--no-cpu-baseline", "--no-training"]
+def _bench(args, world, env=None):
+    if world > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}"]
+    else:
+        cmd = [sys.executable]
+    cmd += [os.path.join(ROOT, "bench.py"), "--gpus", str(world)] + args
     r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1  # rank 0 only
-    d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["config"]["total_envs"] == 4096
-    assert d["value"] > 0 and d["e2e"]["value"] > 0
-    assert sum(d["results"]["requests"]) == 4096 * 2000
+    return json.loads(lines[0])
+
+
+def test_bench_two_ranks_one_gpu(cuda, tmp_path):
+    """Config 4's split: the same 4,096 global envs on one rank and sharded over two
+    (by global id, traces keyed by global id): the all-reduced integer statistics
+    are bit-equal, rewards equal up to the rank-order summation; both runs pass the
+    in-line oracle parity check."""
+    env = dict(os.environ, BE_DIST_BACKEND="gloo", OMP_NUM_THREADS="1")
+    args = ["--steps", "2", "--warmup", "3", "--envs", "4096", "--requests", "2000",
+            "--no-cpu-baseline", "--no-training", "--parity-envs", "8"]
+    d1 = _bench(args, 1, env)
+    d2 = _bench(args, 2, env)
+    for d, n in ((d1, 1), (d2, 2)):
+        assert d["n_gpus"] == n and d["config"]["total_envs"] == 4096 and d["scaling"] == "strong"
+        assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["e2e"]["stats_identical_to_resident_run"]
+        assert d["parity"]["mismatches"] == 0 and d["parity"]["envs"] >= 8
+    assert d2["config"]["envs_per_gpu"] == 2048
+    assert d2["weak_scaling"]["envs_per_gpu"] == 4096 and d2["weak_scaling"]["value"] > 0
+    r1, r2 = d1["results"], d2["results"]
+    assert sum(r2["requests"]) == 4096 * 2000
+    for k in ("win_counts", "n_windows", "requests", "misses"):
+        assert r1[k] == r2[k], k
+    np.testing.assert_allclose(r1["mean_reward"], r2["mean_reward"], rtol=1e-12)
