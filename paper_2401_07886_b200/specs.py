@@ -211,96 +211,155 @@ def event_rates(trace) -> np.ndarray:
     return rates
 
 
-class QNetwork:
-    """QNetwork parameters (policy.py:68-118), fp64 host arrays.
+def param_layout(n_tasks: int, n_tiers: int, hidden: int) -> tuple:
+    """(name, shape, offset) of w1, b1, w2, b2 in the flat fp64 parameter vector —
+    the BEQN1 payload order and the device learner's `params` layout."""
+    d = n_tasks + n_tiers + 1
+    out, off = [], 0
+    for name, shape in (("w1", (d, hidden)), ("b1", (hidden,)), ("w2", (hidden, n_tiers)),
+                        ("b2", (n_tiers,))):
+        out.append((name, shape, off))
+        off += int(np.prod(shape))
+    return tuple(out)
 
-    `forward` runs on the GPU (route kernel); there is no CPU forward."""
+
+def _param_property(name: str):
+    def get(self):
+        return self._views[name]
+
+    def put(self, value):
+        v = self._views[name]
+        value = np.asarray(value, dtype=np.float64)
+        if value.shape != v.shape:
+            raise ValueError(f"{name}: expected shape {v.shape}, got {value.shape}")
+        v[...] = value
+
+    return property(get, put, doc=f"{name} (a view into `flat`)")
+
+
+class QNetwork:
+    """Router MLP parameters (the reference QNetwork, policy.py:68-118), held as ONE
+    contiguous fp64 vector `flat` in BEQN1 payload order (w1 | b1 | w2 | b2);
+    w1/b1/w2/b2 are views into it.  The GPU path uploads `flat` in one copy and
+    checkpoints are `flat` behind a two-line header.  `forward` runs on the GPU."""
+
+    w1 = _param_property("w1")
+    b1 = _param_property("b1")
+    w2 = _param_property("w2")
+    b2 = _param_property("b2")
 
     def __init__(self, n_tasks, n_tiers, w1, b1, w2, b2):
-        self.n_tasks = int(n_tasks)
-        self.n_tiers = int(n_tiers)
-        self.hidden = int(np.shape(w1)[1])
-        self.input_dim = self.n_tasks + self.n_tiers + 1
-        if np.shape(w1) != (self.input_dim, self.hidden) or np.shape(b1) != (self.hidden,):
-            raise ValueError("layer 1 shape mismatch")
-        if np.shape(w2) != (self.hidden, self.n_tiers) or np.shape(b2) != (self.n_tiers,):
-            raise ValueError("layer 2 shape mismatch")
-        self.w1 = np.asarray(w1, dtype=np.float64)
-        self.b1 = np.asarray(b1, dtype=np.float64)
-        self.w2 = np.asarray(w2, dtype=np.float64)
-        self.b2 = np.asarray(b2, dtype=np.float64)
+        t, m = int(n_tasks), int(n_tiers)
+        arrays = [np.asarray(x) for x in (w1, b1, w2, b2)]
+        h = arrays[0].shape[1] if arrays[0].ndim == 2 else -1
+        layout = param_layout(t, m, max(h, 0))
+        for k, ((name, shape, _), arr) in enumerate(zip(layout, arrays)):
+            if arr.shape != shape or h < 0:
+                raise ValueError("layer 1 shape mismatch" if k < 2 else "layer 2 shape mismatch")
+        self._init_flat(t, m, h, np.concatenate([x.astype(np.float64).ravel() for x in arrays]))
+
+    def _init_flat(self, t: int, m: int, h: int, flat: np.ndarray) -> None:
+        self.n_tasks, self.n_tiers, self.hidden = t, m, h
+        self.input_dim = t + m + 1
+        self.flat = flat
+        self._views = {name: flat[off:off + int(np.prod(shape))].reshape(shape)
+                       for name, shape, off in param_layout(t, m, h)}
+
+    @classmethod
+    def from_flat(cls, n_tasks: int, n_tiers: int, hidden: int, flat) -> "QNetwork":
+        flat = np.array(flat, dtype=np.float64).ravel()
+        need = param_layout(n_tasks, n_tiers, hidden)[-1]
+        if flat.size != need[2] + n_tiers:
+            raise ValueError(f"expected {need[2] + n_tiers} parameters, got {flat.size}")
+        net = cls.__new__(cls)
+        net._init_flat(int(n_tasks), int(n_tiers), int(hidden), flat)
+        return net
 
     @classmethod
     def init_random(cls, n_tasks, n_tiers, hidden=HIDDEN_DEFAULT, rng=None):
-        """policy.py:86-98: U(+-sqrt(6/fan_in)) weights, zero biases."""
-        rng = rng if rng is not None else np.random.default_rng()
-        d = n_tasks + n_tiers + 1
-        b1, b2 = math.sqrt(6.0 / d), math.sqrt(6.0 / hidden)
-        return cls(n_tasks, n_tiers, w1=rng.uniform(-b1, b1, size=(d, hidden)),
-                   b1=np.zeros(hidden), w2=rng.uniform(-b2, b2, size=(hidden, n_tiers)),
-                   b2=np.zeros(n_tiers))
+        """Reference initialisation (policy.py:86-98): w1 ~ U(+-sqrt(6/D)), then
+        w2 ~ U(+-sqrt(6/H)) from the same Generator (same draws, same order),
+        zero biases."""
+        g = np.random.default_rng() if rng is None else rng
+        net = cls.from_flat(n_tasks, n_tiers, hidden,
+                            np.zeros(param_layout(n_tasks, n_tiers, hidden)[-1][2] + n_tiers))
+        lim_in = math.sqrt(6.0 / net.input_dim)
+        net.w1 = g.uniform(-lim_in, lim_in, size=net.w1.shape)
+        lim_h = math.sqrt(6.0 / hidden)
+        net.w2 = g.uniform(-lim_h, lim_h, size=net.w2.shape)
+        return net
 
     @classmethod
     def from_any(cls, net) -> "QNetwork":
         if isinstance(net, cls):
             return net
         if isinstance(net, dict):
-            w1 = np.asarray(net["w1"])
-            return cls(w1.shape[0] - len(net["b2"]) - 1, len(net["b2"]), net["w1"], net["b1"],
-                       net["w2"], net["b2"])
+            m = len(net["b2"])
+            return cls(np.shape(net["w1"])[0] - m - 1, m, net["w1"], net["b1"], net["w2"], net["b2"])
         return cls(net.n_tasks, net.n_tiers, net.w1, net.b1, net.w2, net.b2)
 
     def params(self):
         return [self.w1, self.b1, self.w2, self.b2]
 
     def copy(self) -> "QNetwork":
-        return QNetwork(self.n_tasks, self.n_tiers, self.w1.copy(), self.b1.copy(),
-                        self.w2.copy(), self.b2.copy())
+        return QNetwork.from_flat(self.n_tasks, self.n_tiers, self.hidden, self.flat.copy())
 
     def load_from(self, other) -> None:
-        for dst, src in zip(self.params(), (other.w1, other.b1, other.w2, other.b2)):
-            np.copyto(dst, src)
+        src = other.flat if isinstance(other, QNetwork) else np.concatenate(
+            [np.asarray(x, np.float64).ravel() for x in (other.w1, other.b1, other.w2, other.b2)])
+        if src.shape != self.flat.shape:
+            raise ValueError("parameter count mismatch")
+        self.flat[...] = src
 
     def forward(self, x):
         from .policy import q_forward_batch
         return q_forward_batch(self, x)
 
 
+# ---------------------------------------------------------------- BEQN1 checkpoints
+# File = b"BEQN1\n" + b"<n_tasks> <n_tiers> <hidden>\n" + the flat parameter vector as
+# little-endian float64 (policy.py:193-199 format).  Read errors are CheckpointError
+# with the reference's messages (policy.py:202-232).
+
 def save_checkpoint(net, path: str) -> None:
-    """policy.py:193-199: magic line, dims line, fp64 LE W1, b1, W2, b2."""
+    q = QNetwork.from_any(net)
+    head = f"{CHECKPOINT_MAGIC}\n{q.n_tasks} {q.n_tiers} {q.hidden}\n".encode("ascii")
     with open(path, "wb") as f:
-        f.write(f"{CHECKPOINT_MAGIC}\n".encode("ascii"))
-        f.write(f"{net.n_tasks} {net.n_tiers} {np.shape(net.w1)[1]}\n".encode("ascii"))
-        for p in (net.w1, net.b1, net.w2, net.b2):
-            f.write(np.ascontiguousarray(p, dtype="<f8").tobytes())
+        f.write(head + q.flat.astype("<f8").tobytes())
+
+
+def _take_line(blob: bytes, pos: int) -> tuple:
+    """The line starting at `pos` including its newline (file.readline semantics)."""
+    end = blob.find(b"\n", pos)
+    end = len(blob) if end < 0 else end + 1
+    return blob[pos:end], end
 
 
 def load_checkpoint(path: str, n_tasks=None, n_tiers=None) -> QNetwork:
-    """policy.py:202-232 (same errors)."""
     with open(path, "rb") as f:
-        magic = f.readline().decode("ascii", errors="replace").strip()
-        if magic != CHECKPOINT_MAGIC:
-            raise CheckpointError(f"{path}: bad magic {magic!r}")
-        header = f.readline().decode("ascii", errors="replace").split()
-        if len(header) != 3:
-            raise CheckpointError(f"{path}: malformed dimension header")
-        try:
-            t, m, hidden = (int(v) for v in header)
-        except ValueError:
-            raise CheckpointError(f"{path}: malformed dimension header")
-        if t < 1 or m < 1 or hidden < 1:
-            raise CheckpointError(f"{path}: nonpositive dimensions")
-        if (n_tasks is not None and t != n_tasks) or (n_tiers is not None and m != n_tiers):
-            raise CheckpointError(f"{path}: dimensions ({t}, {m}) do not match expected "
-                                  f"({n_tasks}, {n_tiers})")
-        d = t + m + 1
-        arrays = []
-        for shape in [(d, hidden), (hidden,), (hidden, m), (m,)]:
-            count = int(np.prod(shape))
-            buf = f.read(count * 8)
-            if len(buf) != count * 8:
-                raise CheckpointError(f"{path}: truncated parameter payload")
-            arrays.append(np.frombuffer(buf, dtype="<f8").reshape(shape).copy())
-        if f.read(1):
-            raise CheckpointError(f"{path}: trailing bytes after parameters")
-    return QNetwork(t, m, *arrays)
+        blob = f.read()
+    line, pos = _take_line(blob, 0)
+    magic = line.decode("ascii", errors="replace").strip()
+    if magic != CHECKPOINT_MAGIC:
+        raise CheckpointError(f"{path}: bad magic {magic!r}")
+    line, pos = _take_line(blob, pos)
+    fields = line.decode("ascii", errors="replace").split()
+    try:
+        if len(fields) != 3:
+            raise ValueError
+        dims = [int(v) for v in fields]
+    except ValueError:
+        raise CheckpointError(f"{path}: malformed dimension header")
+    t, m, h = dims
+    if min(dims) < 1:
+        raise CheckpointError(f"{path}: nonpositive dimensions")
+    if (n_tasks is not None and t != n_tasks) or (n_tiers is not None and m != n_tiers):
+        raise CheckpointError(f"{path}: dimensions ({t}, {m}) do not match expected "
+                              f"({n_tasks}, {n_tiers})")
+    count = param_layout(t, m, h)[-1][2] + m
+    payload = memoryview(blob)[pos:]
+    if len(payload) < 8 * count:
+        raise CheckpointError(f"{path}: truncated parameter payload")
+    if len(payload) > 8 * count:
+        raise CheckpointError(f"{path}: trailing bytes after parameters")
+    return QNetwork.from_flat(t, m, h, np.frombuffer(payload, dtype="<f8"))
