@@ -117,8 +117,11 @@ typedef struct {
 
 /* QNetwork parameters (policy.py:68-118), fp64, BEQN1 order/layout. */
 typedef struct {
-    int32_t hidden;      /* multiple of 32, <= 1024 */
-    int32_t _pad;
+    int32_t hidden;      /* even, in [2, 1024] (the tensor-core router: multiple of 32, <= 256) */
+    int16_t n_tasks;     /* QNetwork.n_tasks: must equal the env's / router's T */
+    int16_t n_tiers;     /* QNetwork.n_tiers: must equal M (policy.py:111-116 rejects
+                            an input of the wrong dimension; a mismatched net would
+                            read past w1 / w2) */
     const double* w1;    /* [D][H], D = T + M + 1 */
     const double* b1;    /* [H] */
     const double* w2;    /* [H][M] */
@@ -383,7 +386,8 @@ int32_t be_learner_open_peers_ipc(be_learner* learner, int32_t world, int32_t ra
  *          Huber backward) + one tile-reduction/Adam kernel.
  * phase 4: whole iteration with the peer-memory gradient exchange (data-parallel,
  *          be_learner_set_peers first): no host round trip, graph-capturable.
- * phase 3: the env part only (workload, env step, commits);
+ * phase 3: the env part only (workload, env step, commits; with
+ *          updates_per_step == 0 it also advances the iteration);
  * phase 1: the gradients of update `update_index` into views.grad — all-reduce
  *          them here (DP learner);
  * phase 2: optimizer step of update `update_index`; the last one advances it.

@@ -61,7 +61,7 @@ class BeTraceSoa(ctypes.Structure):
 
 
 class BeQWeights(ctypes.Structure):
-    _fields_ = [("hidden", ctypes.c_int32), ("_pad", ctypes.c_int32),
+    _fields_ = [("hidden", ctypes.c_int32), ("n_tasks", ctypes.c_int16), ("n_tiers", ctypes.c_int16),
                 ("w1", ctypes.c_void_p), ("b1", ctypes.c_void_p),
                 ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p)]
 

@@ -124,8 +124,13 @@ static int validate_cfg(const be_cfg* c, int* lanes) {
 
 static int validate_weights(const be_qweights* W, const be_cfg& c) {
     if (!W || !W->w1 || !W->b1 || !W->w2 || !W->b2) return set_error(BE_EINVAL, "policy weights missing");
-    if (W->hidden < 32 || W->hidden % 32 != 0 || W->hidden > 1024)
-        return set_error(BE_EINVAL, "hidden must be a multiple of 32 in [32, 1024]");
+    if (W->n_tasks != c.n_tasks || W->n_tiers != c.n_tiers)
+        return set_error(BE_EINVAL, "expected input dim: the policy network's (n_tasks, n_tiers) differ from "
+                                    "the environment's");
+    // any even width (the packed layouts pair hidden units); the fused rollout's fp32
+    // decision screen switches itself off unless H is a multiple of 2 x lanes per env
+    if (W->hidden < 2 || W->hidden % 2 != 0 || W->hidden > 1024)
+        return set_error(BE_EINVAL, "hidden must be even, in [2, 1024]");
     size_t smem = rollout_smem_bytes(c.n_tasks, c.n_tiers, W->hidden, true);
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "Q-network too large for shared memory");
     return BE_OK;
@@ -326,6 +331,8 @@ int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers
         return set_error(BE_EINVAL, "NULL argument");
     if (n_tasks < 1 || n_tasks > BE_MAX_TASKS || n_tiers < 1 || n_tiers > BE_MAX_TIERS)
         return set_error(BE_EINVAL, "dimensions out of range");
+    if (W->n_tasks != n_tasks || W->n_tiers != n_tiers)
+        return set_error(BE_EINVAL, "expected input dim: the network's (n_tasks, n_tiers) differ from the router's");
     if (W->hidden < 1 || W->hidden > 4096) return set_error(BE_EINVAL, "hidden out of range");
     if (!(epsilon >= 0.0 && epsilon <= 1.0)) return set_error(BE_EINVAL, "epsilon must lie in [0, 1]");
     if (batch < 0) return set_error(BE_EINVAL, "batch must be >= 0");
@@ -350,6 +357,8 @@ int32_t be_qnet_route_tc(const be_qweights* W, int32_t n_tasks, int32_t n_tiers,
         return set_error(BE_EINVAL, "NULL argument");
     if (n_tasks < 1 || n_tasks > BE_MAX_TASKS || n_tiers < 1 || n_tiers > BE_MAX_TIERS)
         return set_error(BE_EINVAL, "dimensions out of range");
+    if (W->n_tasks != n_tasks || W->n_tiers != n_tiers)
+        return set_error(BE_EINVAL, "expected input dim: the network's (n_tasks, n_tiers) differ from the router's");
     if (!route_tc_supported(n_tasks, n_tiers, W->hidden))
         return set_error(BE_EINVAL, "route_tc needs n_tiers <= 4, n_tasks + n_tiers + 2 <= 16 and hidden a "
                                     "multiple of 32 in [32, 256]; use be_qnet_route_f64");

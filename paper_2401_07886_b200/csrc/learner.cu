@@ -823,11 +823,15 @@ int32_t be_learner_views(be_learner* L, be_learner_views_t* v) {
     if (!L || !v) return set_error(BE_EINVAL, "NULL argument");
     const int D = L->D, H = L->cfg.hidden, M = L->cfg.n_tiers;
     v->online.hidden = H;
+    v->online.n_tasks = (int16_t)L->cfg.n_tasks;
+    v->online.n_tiers = (int16_t)M;
     v->online.w1 = L->params;
     v->online.b1 = L->params + D * H;
     v->online.w2 = L->params + D * H + H;
     v->online.b2 = L->params + D * H + H + H * M;
     v->target.hidden = H;
+    v->target.n_tasks = (int16_t)L->cfg.n_tasks;
+    v->target.n_tiers = (int16_t)M;
     v->target.w1 = L->target;
     v->target.b1 = L->target + D * H;
     v->target.w2 = L->target + D * H + H;
@@ -1119,6 +1123,8 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                               L->it_arrival, L->it_task, L->it_rate, it};
         be_qweights W;
         W.hidden = H;
+        W.n_tasks = (int16_t)cf.n_tasks;
+        W.n_tiers = (int16_t)M;
         W.w1 = L->params;
         W.b1 = L->params + D * H;
         W.w2 = L->params + D * H + H;
@@ -1164,6 +1170,9 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         }
     } else if (c->phase == 2) {
         rc = launch_update(L, 0, 1, apply_params(L, 0, c->update_index == ups - 1), gate, st);
+        if (rc) return rc;
+    } else if (c->phase == 3 && ups == 0) {  // no phase 2 follows: advance the iteration here
+        rc = launch_update(L, 0, 0, apply_params(L, 1, 1), nullptr, st);
         if (rc) return rc;
     }
     cudaError_t e = cudaGetLastError();

@@ -129,13 +129,18 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
     constexpr bool true_rate = TR != 0;
     const bool reset_segs = p.cfg.reset_between_segments != 0;
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
-    // encode (policy.py:63-64) divides by the scales; multiplying by the
-    // reciprocal is bit-identical for power-of-two scales (the shipped
-    // 128/32/8) and within 1 ulp otherwise (Q tolerance)
+    // encode (policy.py:63-64) divides by the scales: a / s as a * (1/s) plus one
+    // Markstein correction step (residual a - q s exact by FMA, q + r (1/s) rounded
+    // once) — the correctly rounded quotient, bit-identical to __ddiv_rn for every
+    // scale (not only the power-of-two ones), two DFMA instead of a DDIV sequence
     double inv_scale[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) inv_scale[m] = __ddiv_rn(1.0, p.cfg.batch_scales[m]);
     const double inv_rate_scale = __ddiv_rn(1.0, p.cfg.rate_scale);
+    auto div_by = [](double a, double s, double inv) {
+        const double q = __dmul_rn(a, inv);
+        return __fma_rn(__fma_rn(-q, s, a), inv, q);
+    };
 
     // per-group ("group-uniform") env state
     int env = -1;
@@ -222,6 +227,10 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         int task = __shfl_sync(FULL, pf_task, g0 + sub);
         const int ftier = p.forced ? __shfl_sync(FULL, pf_forced, g0 + sub) : 0;
         if (!live) task = 0;  // keep idle groups' shared-memory reads in range
+        if (task >= T) {      // task id outside the reward spec (encode raises, policy.py:57-58)
+            bad = bad || live;
+            task = 0;
+        }
         double rate = 0.0;
         if (live) {
             while (i >= next_seg) {  // segment boundaries (evalkit.py:186-192)
@@ -258,8 +267,8 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         } else {
             double xt[M], q[M];
 #pragma unroll
-            for (int m = 0; m < M; ++m) xt[m] = __dmul_rn((double)obs[m], inv_scale[m]);
-            const double xr = __dmul_rn(rate, inv_rate_scale);
+            for (int m = 0; m < M; ++m) xt[m] = div_by((double)obs[m], p.cfg.batch_scales[m], inv_scale[m]);
+            const double xr = div_by(rate, p.cfg.rate_scale, inv_rate_scale);
             if (screen) {
                 // certified fp32 decision; exact fp64 evaluation only where it cannot certify
                 const bool sure = qnet_screen<M, LPE>(sf, T, H, task, xt, xr, tier);

@@ -147,7 +147,9 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         return;
     }
     const double U = p.arrival[e];
-    const int task = live ? p.task[e] : 0;
+    int task = live ? p.task[e] : 0;
+    const bool bad_task = live && task >= T;  // encode raises (policy.py:57-58)
+    if (task >= T) task = 0;
     if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out);
     Estimator est;
 #pragma unroll
@@ -235,8 +237,8 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         es->next_id = id + 1;
     }
     const bool all_ok = (__ballot_sync(FULL, !ok) & gmask) == 0;
-    if (live && gl == 0 && (bad || !all_ok)) {
-        if (atomicCAS(&p.status[0], 0, bad ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
+    if (live && gl == 0 && (bad || bad_task || !all_ok)) {
+        if (atomicCAS(&p.status[0], 0, (bad || bad_task) ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
     }
 }
 

@@ -162,6 +162,12 @@ class EnvBatch:
         rate [E] f64, action [E] u8, q [E, M] f64 and x [E, D] f64 (encoded state)."""
         E, M = self.n_envs, self.n_tiers
         dev = self.device
+        _check_vec(arrival, "arrival", torch.float64, E, dev)
+        _check_vec(task, "task", torch.uint8, E, dev)  # ids >= n_tasks: EINVAL from the kernel
+        if true_rate is not None:
+            _check_vec(true_rate, "true_rate", torch.float64, E, dev)
+        if forced is not None:
+            _check_vec(forced, "forced", torch.uint8, E, dev)
         out = dict(obs=torch.empty((E, M), dtype=torch.int32, device=dev),
                    rate=torch.empty(E, dtype=torch.float64, device=dev),
                    action=torch.empty(E, dtype=torch.uint8, device=dev))
@@ -185,6 +191,12 @@ class EnvBatch:
         rec = records.struct()
         _lib.check(self._L.be_env_drain(self._h, records.ld, ctypes.byref(rec),
                                         _lib.stream_ptr(stream)))
+
+
+def _check_vec(t, name, dtype, n, dev):
+    if not isinstance(t, torch.Tensor) or t.dtype != dtype or t.device != dev or t.numel() < n \
+            or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of >= {n} elements on {dev}")
 
 
 class StepRecords:

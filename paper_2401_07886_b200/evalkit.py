@@ -203,6 +203,9 @@ class GreedyRollout:
         """Asynchronous: enqueue the fused rollout on `stream` (no sync)."""
         if trace.n_envs > self.n_envs or trace.ld != self.ld:
             raise ValueError("trace batch does not match the rollout shape")
+        if trace.n_tasks > self.env.n_tasks:  # the kernel also flags ids >= n_tasks (EINVAL)
+            raise ValueError(f"trace task ids reach {trace.n_tasks - 1}, the reward spec has "
+                             f"{self.env.n_tasks} tasks")
         o = self.out
         rec = _lib.BeRecords()
         rec.flags, rec.reward = o.flags.data_ptr(), o.reward.data_ptr()

@@ -37,6 +37,7 @@ class DeviceQNet:
     def weights(self) -> _lib.BeQWeights:
         w = _lib.BeQWeights()
         w.hidden = self.hidden
+        w.n_tasks, w.n_tiers = self.n_tasks, self.n_tiers
         w.w1, w.b1, w.w2, w.b2 = (t.data_ptr() for t in (self.w1, self.b1, self.w2, self.b2))
         return w
 

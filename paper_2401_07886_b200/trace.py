@@ -68,7 +68,10 @@ class TraceBatch:
         sequences of SegmentMark start indices / rates."""
         dev = _lib.require_cuda(device)
         arrival = np.atleast_2d(np.asarray(arrival, np.float64))
-        task = np.atleast_2d(np.asarray(task, np.uint8))
+        task = np.atleast_2d(np.asarray(task))
+        if task.size and (not np.issubdtype(task.dtype, np.integer) or task.min() < 0 or task.max() > 255):
+            raise _lib.InvalidParameterError("task ids must be integers in [0, 256)")
+        task = task.astype(np.uint8)
         E = arrival.shape[0]
         if seg_start and np.ndim(seg_start[0]) == 0:
             seg_start, seg_rate = [seg_start], [seg_rate]

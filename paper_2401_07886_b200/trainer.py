@@ -142,6 +142,8 @@ class DeviceLearner:
         self.ring_states = _wrap(v.ring_states, (C, self.D), torch.float64, self.device)
         self.ring_next_states = _wrap(v.ring_next_states, (C, self.D), torch.float64, self.device)
         self.ring_actions = _wrap(v.ring_actions, (C,), torch.uint8, self.device)
+        self.ring_cont = _wrap(v.ring_cont, (C,), torch.float64, self.device)
+        self.workload_state = _wrap(v.workload_state, (self.n_envs, 3), torch.float64, self.device)
         self.pending_x = _wrap(v.pending_x, (self.P, self.n_envs, self.D), torch.float64, self.device)
         self.pending_action = _wrap(v.pending_action, (self.P, self.n_envs), torch.uint8, self.device)
         self.pending_flags = _wrap(v.pending_flags, (self.n_envs, self.P), torch.uint8, self.device)
@@ -298,6 +300,12 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         raise ValueError("tier count must match reward matrix width")
     if mode not in ("graph", "device", "host"):
         raise ValueError("mode must be 'graph', 'device' or 'host'")
+    if completion_log is not None:
+        # the audit trail is harvested per iteration from the pending store: the
+        # host-driven loop (same results as the device / graph modes)
+        if world is not None:
+            raise ValueError("completion_log is not supported with a data-parallel world")
+        mode = "host"
     if exchange not in ("nccl", "peer"):
         raise ValueError("exchange must be 'nccl' or 'peer'")
     if encoding is None:
@@ -361,7 +369,7 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     t_begin.record()
     if mode == "host":
         _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
-                       log_every, log_row)
+                       log_every, log_row, completion_log)
     else:
         tic = _lib.BeTrainIterCfg()
         tic.workload_seed, tic.policy_seed, tic.sample_seed = wl_seed, pol_seed, smp_seed
@@ -397,10 +405,6 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                 dist.all_reduce(learner.grad)
                 learner.grad.mul_(1.0 / dist.get_world_size())
                 tic.phase = 2
-                _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
-                                                         _lib.stream_ptr()))
-            if updates_per_step == 0:
-                tic.phase, tic.update_index, tic.use_gate = 0, 0, 0
                 _lib.check(learner._L.be_train_iteration(learner.handle, env.handle, ctypes.byref(tic),
                                                          _lib.stream_ptr()))
 
@@ -450,11 +454,19 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
 
 
 def _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
-                   log_every, log_row):
-    """The reference loop's structure (trainer.py:374-404), one C-ABI call per stage."""
+                   log_every, log_row, completion_log=None):
+    """The reference loop's structure (trainer.py:374-404), one C-ABI call per stage.
+
+    completion_log (trainer.py:381-383): (request id, task, tier, realized ms/token,
+    reward) of every completed request.  A request's pending slot (id mod P) is final
+    once the slot is about to be reused (a request unresolved after P decisions is an
+    error), so slot (it + 1) mod P is harvested after iteration it and the last P
+    slots after the loop; entries are in request-id order (env-major within an id),
+    not in the reference's completion-time order."""
     dev = learner.device
     P = learner.P
-    rec = _PendingRecords(learner)
+    rec = _PendingRecords(learner, want_realized=completion_log is not None)
+    audit = _AuditHarvest(learner, rec, completion_log) if completion_log is not None else None
     arrival = torch.empty(E, dtype=torch.float64, device=dev)
     task = torch.empty(E, dtype=torch.uint8, device=dev)
     rate = torch.empty(E, dtype=torch.float64, device=dev)
@@ -473,23 +485,64 @@ def _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_s
                 learner.grad.mul_(1.0 / dist.get_world_size())
             learner.apply()
         learner.counters[3] += 1  # keep the device iteration index in step (views.counters[3])
+        if audit is not None:
+            audit.slot(it + 1 - P)
         if (it + 1) % log_every == 0:
             log_row(it)
+    if audit is not None:
+        for j in range(max(0, cfg.total_iterations - P + 1), cfg.total_iterations):
+            audit.slot(j)
+        audit.flush()
+
+
+class _AuditHarvest:
+    """Collects completion_log rows from the learner's pending store (device
+    tensors staged per request id, copied to the host in blocks)."""
+
+    def __init__(self, learner, rec, out):
+        self.L, self.rec, self.out = learner, rec, out
+        self.T = learner.n_tasks
+        self.rows, self.ids = [], []
+
+    def slot(self, j):
+        if j < 0:
+            return
+        s = j % self.L.P
+        f = self.rec.flags[:, s]
+        done = (f & 0x60) != 0  # completed (0x40) or already committed (0x20)
+        task = self.L.pending_x[s, :, :self.T].argmax(dim=1)
+        self.rows.append(torch.stack([done.double(), task.double(),
+                                      self.L.pending_action[s].double(),
+                                      self.rec.realized[:, s], self.rec.reward[:, s]]))
+        self.ids.append(j)
+        if len(self.rows) >= 4096:
+            self.flush()
+
+    def flush(self):
+        if not self.rows:
+            return
+        blk = torch.stack(self.rows).cpu().numpy()  # [n ids][5][E]
+        for j, r in zip(self.ids, blk):
+            for e in np.nonzero(r[0])[0]:
+                self.out.append((j, int(r[1, e]), int(r[2, e]), float(r[3, e]), float(r[4, e])))
+        self.rows, self.ids = [], []
 
 
 class _PendingRecords:
     """StepRecords view onto the learner's pending reward/flag store (rec_ld = P)."""
 
-    def __init__(self, learner: DeviceLearner):
+    def __init__(self, learner: DeviceLearner, want_realized: bool = False):
         self.ld = learner.P
         self.flags = learner.pending_flags
         self.reward = learner.pending_reward
-        self.realized = None
+        self.realized = (torch.full_like(learner.pending_reward, float("nan"))
+                         if want_realized else None)
 
     def struct(self) -> _lib.BeRecords:
         r = _lib.BeRecords()
         r.flags = self.flags.data_ptr()
         r.reward = self.reward.data_ptr()
+        r.realized = _lib.ptr(self.realized)
         return r
 
 

@@ -30,7 +30,8 @@ def transitions_from_golden(name="unpredictable-1_trained"):
 
 
 def params_of(net):
-    return {k: np.array(net[k], dtype=np.float64) for k in ("w1", "b1", "w2", "b2")}
+    get = net.__getitem__ if isinstance(net, dict) else lambda k: getattr(net, k)
+    return {k: np.array(get(k), dtype=np.float64) for k in ("w1", "b1", "w2", "b2")}
 
 
 def flat(d):
@@ -74,7 +75,7 @@ def test_learner_matches_oracle(cuda, loss, opt):
         params = new
         if step % cfg.target_sync_every == 0:  # trainer.py:288-289
             target = {k: v.copy() for k, v in params.items()}
-        assert np.max(np.abs(flat(params_of(L.target_net().__dict__)) - flat(target))) <= 1e-12 * 100
+        assert np.max(np.abs(flat(params_of(L.target_net())) - flat(target))) <= 1e-12 * 100
 
 
 def test_replay_commits_follow_deferred_reward_rule(cuda):
@@ -165,7 +166,7 @@ def test_learner_matches_reference_golden(cuda, loss, opt):
         p_ref = gl["params"][step - 1]
         p_dev = L.params.cpu().numpy()
         assert np.max(np.abs(p_dev - p_ref)) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))
-        t_dev = flat(params_of(L.target_net().__dict__))
+        t_dev = flat(params_of(L.target_net()))
         assert np.max(np.abs(t_dev - gl["target"][step - 1])) <= 1e-13 + 1e-10 * np.max(np.abs(p_ref))
 
 
