@@ -12,6 +12,7 @@
  *   be_env_step                      advance + observe + encode +  evalkit.py:185-205,
  *                                    forward/argmax + submit        simcore.py:94-157
  *   be_env_drain                     ClusterSim.drain              simcore.py:151-153
+ *   be_env_new_segment               segment reset of run_eval     evalkit.py:186-192
  *   be_rollout_greedy                run_eval (whole trace)        evalkit.py:154-209
  *   be_qnet_route_f64                select_action / argmax(forward) policy.py:111-132
  *   be_qnet_route_tc                 the same on the tensor cores   policy.py:111-132
@@ -171,6 +172,13 @@ int32_t be_env_step(be_env* env, const double* arrival_ms, const uint8_t* task,
                     uint8_t* action_out, double* q_out, double* x_out, void* stream);
 /* Run every replica to completion (simcore.py:151-153). */
 int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream);
+/* Stable-segment reset of run_eval (evalkit.py:186-192) for the envs with
+ * mask[e] != 0 (device u8 [E]; NULL = all): drain every replica (completions
+ * scored into rec), then a fresh ClusterSim (simcore.py:72-84) and an empty
+ * estimator window (workload.py:249-250).  Request ids continue (they index
+ * the trace), unlike be_env_reset, which also restarts them at 0. */
+int32_t be_env_new_segment(be_env* env, const uint8_t* mask, int64_t rec_ld, be_records* rec,
+                           void* stream);
 
 /* Whole greedy rollout (run_eval) of E envs over a trace batch, fused in one
  * persistent kernel: one warp per env, one lane per replica.  Routing:
@@ -220,10 +228,19 @@ int32_t be_qnet_route_tc(const be_qweights* W, int32_t n_tasks, int32_t n_tiers,
  *   win_counts [E][n_theta] int64, n_windows [E] int64,
  *   bucket_miss / bucket_req [E][n_buckets] int64, bucket_reward [E][n_buckets] f64
  * Buckets come from trace->seg_bucket (NULL -> everything in bucket 0).
- * `thetas` is a HOST array (the thresholds are turned into exact difference
- * cut-offs on the host, see reduce.cu). */
+ * The thresholds travel BY VALUE (no host/device pointer ambiguity; the
+ * library turns each theta into an exact cut-off on the window sum, see
+ * reduce.cu).  Miss flags are the rollout's per-request flags bit 7
+ * (realized > deadline[task], evalkit.py:65-67, decided where realized is made). */
+#define BE_MAX_THETA 8
+typedef struct {
+    int32_t n;                      /* number of thresholds, 1..BE_MAX_THETA */
+    int32_t _pad;
+    double theta[BE_MAX_THETA];     /* each in [0, 1]; 1.0 counts exact peaks only */
+} be_thresholds;
+
 int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const double* reward,
-                       int32_t window, const double* thetas, int32_t n_theta,
+                       int32_t window, be_thresholds thresholds,
                        int32_t n_buckets, int64_t* win_counts, int64_t* n_windows,
                        int64_t* bucket_miss, int64_t* bucket_req, double* bucket_reward,
                        void* stream);
@@ -324,7 +341,8 @@ typedef struct {
     uint8_t* ring_actions;       /* [C] */
     double* ring_rewards;        /* [C] */
     double* ring_cont;           /* [C] */
-    int64_t* ring_state;         /* [0] cursor, [1] size, [2] total commits */
+    int64_t* ring_state;         /* [0] cursor, [1] size, [2] total commits, [3] commits of the
+                                    last step, [4] most decisions a request stayed in flight */
     double* pending_x;           /* [P][E][D]: x_out of be_env_step for request id = step */
     uint8_t* pending_action;     /* [P][E]:    action_out of be_env_step */
     uint8_t* pending_flags;      /* [E][P]:    be_records.flags with rec_ld = P */

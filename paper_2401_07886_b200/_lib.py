@@ -66,6 +66,13 @@ class BeQWeights(ctypes.Structure):
                 ("w2", ctypes.c_void_p), ("b2", ctypes.c_void_p)]
 
 
+MAX_THETA = 8
+
+
+class BeThresholds(ctypes.Structure):  # passed by value
+    _fields_ = [("n", ctypes.c_int32), ("_pad", ctypes.c_int32), ("theta", ctypes.c_double * MAX_THETA)]
+
+
 class BeRecords(ctypes.Structure):
     _fields_ = [("flags", ctypes.c_void_p), ("reward", ctypes.c_void_p),
                 ("realized", ctypes.c_void_p), ("obs", ctypes.c_void_p),
@@ -131,6 +138,7 @@ SIGNATURES = {
     "be_env_step": (_I32, [_P, _P, _P, _P, _P, ctypes.POINTER(BeQWeights), _I32, _D, _U64, _U64,
                            _I64, ctypes.POINTER(BeRecords), _P, _P, _P, _P, _P, _P]),
     "be_env_drain": (_I32, [_P, _I64, ctypes.POINTER(BeRecords), _P]),
+    "be_env_new_segment": (_I32, [_P, _P, _I64, ctypes.POINTER(BeRecords), _P]),
     "be_rollout_greedy": (_I32, [_P, ctypes.POINTER(BeTraceSoa), ctypes.POINTER(BeQWeights), _I32,
                                  _P, ctypes.POINTER(BeRecords), _P]),
     "be_qnet_route_f64": (_I32, [ctypes.POINTER(BeQWeights), _I32, _I32, _P, _I32, _D, _U64, _U64,
@@ -139,7 +147,7 @@ SIGNATURES = {
     "be_qnet_route_tc_workspace_bytes": (_SZ, [_I32]),
     "be_qnet_route_tc": (_I32, [ctypes.POINTER(BeQWeights), _I32, _I32, _P, _I32, _D, _U64, _U64,
                                 _P, _P, _P, _P, _P]),
-    "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, _P, _I32, _I32, _P, _P, _P,
+    "be_reduce_eval": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _P, _I32, BeThresholds, _I32, _P, _P, _P,
                               _P, _P, _P]),
     "be_reduce_selection": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _I32, _I32, _I32, _P, _P]),
     "be_windowed": (_I32, [ctypes.POINTER(BeTraceSoa), _P, _I32, _P, _P]),

@@ -323,6 +323,12 @@ int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream)
     return launch_env_drain(env, rec_ld, rec, (cudaStream_t)stream);
 }
 
+int32_t be_env_new_segment(be_env* env, const uint8_t* mask, int64_t rec_ld, be_records* rec, void* stream) {
+    if (!env || !rec || !rec->flags || !rec->reward) return set_error(BE_EINVAL, "NULL argument");
+    if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");
+    return launch_env_drain(env, rec_ld, rec, (cudaStream_t)stream, mask, 1);
+}
+
 int32_t be_qnet_route_f64(const be_qweights* W, int32_t n_tasks, int32_t n_tiers, const double* x,
                           int32_t batch, double epsilon, uint64_t philox_seed,
                           uint64_t philox_counter, double* q_out, uint8_t* action_out,
@@ -370,17 +376,18 @@ int32_t be_qnet_route_tc(const be_qweights* W, int32_t n_tasks, int32_t n_tiers,
 }
 
 int32_t be_reduce_eval(const be_trace_soa* trace, const uint8_t* flags, const double* reward,
-                       int32_t window, const double* thetas, int32_t n_theta, int32_t n_buckets,
+                       int32_t window, be_thresholds thresholds, int32_t n_buckets,
                        int64_t* win_counts, int64_t* n_windows, int64_t* bucket_miss,
                        int64_t* bucket_req, double* bucket_reward, void* stream) {
     if (!trace || !flags || !reward || !win_counts || !n_windows || !bucket_miss || !bucket_req ||
-        !bucket_reward || (n_theta > 0 && !thetas))
+        !bucket_reward)
         return set_error(BE_EINVAL, "NULL argument");
     if (window < 1) return set_error(BE_EINVAL, "window must be >= 1");
-    if (n_theta < 0 || n_theta > 16) return set_error(BE_EINVAL, "n_theta must be in [0, 16]");
+    if (thresholds.n < 1 || thresholds.n > BE_MAX_THETA)
+        return set_error(BE_EINVAL, "the number of thresholds must be in [1, 8]");
     if (n_buckets < 1) return set_error(BE_EINVAL, "n_buckets must be >= 1");
     if (!trace->seg_offsets) return set_error(BE_EINVAL, "trace segments missing");
-    return launch_reduce(trace, flags, reward, window, thetas, n_theta, n_buckets, win_counts,
+    return launch_reduce(trace, flags, reward, window, thresholds.theta, thresholds.n, n_buckets, win_counts,
                          n_windows, bucket_miss, bucket_req, bucket_reward, (cudaStream_t)stream);
 }
 

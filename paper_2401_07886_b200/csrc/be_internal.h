@@ -88,7 +88,8 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
                     int static_tier, double epsilon, uint64_t seed, uint64_t counter,
                     int64_t rec_ld, const be_records* rec, int32_t* obs_out, double* rate_out,
                     uint8_t* action_out, double* q_out, double* x_out, cudaStream_t st);
-int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st);
+int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st,
+                     const uint8_t* mask = nullptr, int new_segment = 0);
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,

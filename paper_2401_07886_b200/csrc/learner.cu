@@ -77,7 +77,7 @@ constexpr int CENVS = 32;  // envs (warps) per commit CTA
 constexpr unsigned FULL_MASK = 0xffffffffu;
 
 __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane, int64_t base, int64_t cursor,
-                                          bool write) {
+                                          bool write, int64_t* window = nullptr) {
     const int64_t step = p.step_dev ? *p.step_dev : p.step;
     const int64_t hi = step - 1;  // inclusive upper candidate
     const int64_t lo = p.low[e];
@@ -129,6 +129,7 @@ __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane
     if (write && lane == 0) {
         p.low[e] = new_low;
         if (step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
+        if (window) *window = step + 1 - new_low;
     }
     return total;
 }
@@ -204,8 +205,17 @@ __global__ void __launch_bounds__(CENVS * 32) commit_fused_kernel(const CommitPa
             }
         }
     }
+    __shared__ unsigned long long wmax_sh;
+    if (threadIdx.x == 0) wmax_sh = 0ull;
     __syncthreads();
-    if (e < p.E) commit_env(p, e, lane, excl_sh + wpre[warp], cursor_sh, true);
+    int64_t win = 0;
+    if (e < p.E) commit_env(p, e, lane, excl_sh + wpre[warp], cursor_sh, true, &win);
+    if (lane == 0 && e < p.E) atomicMax(&wmax_sh, (unsigned long long)win);
+    __syncthreads();
+    // high-water mark of in-flight decisions per env (ring_state[4]; diagnostics for
+    // sizing pending_capacity)
+    if (threadIdx.x == 0 && wmax_sh > (unsigned long long)__ldcg(p.ring_state + 4))
+        atomicMax(reinterpret_cast<unsigned long long*>(p.ring_state + 4), wmax_sh);
     pdl_trigger();
 }
 

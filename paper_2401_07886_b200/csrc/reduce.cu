@@ -27,6 +27,8 @@ namespace be {
 
 // Build-time tunables (measured on B200 at 65,536 envs x 10k, bench r1c): 2 warps x
 // 2 stages x 8 CTAs/SM 1.20 ms; 4 x 3 x 4 1.26 ms; 2 x 3 x 8 1.24 ms; 4 x 2 x 4 1.22 ms.
+// Measured and dropped (r2d, tools/probe_reduce.py): a cp.async.bulk.prefetch.L2 of
+// each env's own row 4-16 chunks ahead (512 B-1 KB bursts) — 1.60-2.00 ms vs 1.21 ms.
 #ifndef RED_W
 #define RED_W 2
 #endif
@@ -37,7 +39,7 @@ namespace be {
 #define RED_MINB 8
 #endif
 constexpr int RED_WARPS = RED_W;
-constexpr int MAX_THETA = 8;
+constexpr int MAX_THETA = BE_MAX_THETA;
 constexpr int CH = 16;       // requests per stage
 constexpr int NST = RED_NST;  // pipeline stages
 constexpr int W = 20;        // evalkit.WINDOW

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <climits>
+#include <math.h>
 
 #include "be_env.cuh"
 #include "be_internal.h"
@@ -76,6 +77,7 @@ struct RolloutParams {
     int32_t skip_rows;
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
+    int32_t pow2_scales;  // 1 = every encoding batch scale is a power of two (x * (1/s) exact)
     unsigned long long* screen_stats;  // [2] decisions screened, fp64 fallbacks (nullable)
     int32_t pack_obs;    // 1: per-tier queue sums fit 10-bit fields (observe with one REDUX)
     const double* qpack;  // screen on: the fp64 fallback's packed weights (QLayout) in global
@@ -141,6 +143,8 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         const double q = __dmul_rn(a, inv);
         return __fma_rn(__fma_rn(-q, s, a), inv, q);
     };
+    // power-of-two batch scales (the shipped 128/32/8): the product IS the quotient
+    const bool pow2_scales = p.pow2_scales != 0;
 
     // per-group ("group-uniform") env state
     int env = -1;
@@ -150,7 +154,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
 
     int n = 0, i = 0, next_seg = INT_MAX;
     auto seg_mark = [&](int64_t k) { return k < seg_end ? (int)min(p.seg_start[k], (int64_t)INT_MAX) : INT_MAX; };
-    double cur_rate = 0.0;
+    double cur_rate = 0.0, cur_xr = 0.0;  // true-rate mode: the segment's rate / rate_scale
     Slot* ring = p.rings;
     Rep r;
     rep_reset(r);
@@ -220,6 +224,10 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                 // rows gain nothing from L1 anyway (A/B: 1% faster than a branch)
                 pf_arr = __ldcg(p.arrival + base + ii);
                 pf_task = __ldcg(p.task + base + ii);
+                if (pf_task >= T) {  // task id outside the reward spec (encode raises,
+                    bad = true;      // policy.py:57-58): the env fails with BE_EINVAL
+                    pf_task = 0;
+                }
                 if (p.forced) pf_forced = __ldg(p.forced + base + ii);
             }
         }
@@ -227,10 +235,6 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         int task = __shfl_sync(FULL, pf_task, g0 + sub);
         const int ftier = p.forced ? __shfl_sync(FULL, pf_forced, g0 + sub) : 0;
         if (!live) task = 0;  // keep idle groups' shared-memory reads in range
-        if (task >= T) {      // task id outside the reward spec (encode raises, policy.py:57-58)
-            bad = bad || live;
-            task = 0;
-        }
         double rate = 0.0;
         if (live) {
             while (i >= next_seg) {  // segment boundaries (evalkit.py:186-192)
@@ -240,6 +244,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                     est.n = 0;
                 }
                 cur_rate = p.seg_rate[seg];
+                if (true_rate) cur_xr = __ddiv_rn(cur_rate, p.cfg.rate_scale);  // once per segment
                 ++seg;
                 next_seg = seg_mark(seg);
             }
@@ -267,8 +272,10 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         } else {
             double xt[M], q[M];
 #pragma unroll
-            for (int m = 0; m < M; ++m) xt[m] = div_by((double)obs[m], p.cfg.batch_scales[m], inv_scale[m]);
-            const double xr = div_by(rate, p.cfg.rate_scale, inv_rate_scale);
+            for (int m = 0; m < M; ++m)
+                xt[m] = pow2_scales ? __dmul_rn((double)obs[m], inv_scale[m])
+                                    : div_by((double)obs[m], p.cfg.batch_scales[m], inv_scale[m]);
+            const double xr = true_rate ? cur_xr : div_by(rate, p.cfg.rate_scale, inv_rate_scale);
             if (screen) {
                 // certified fp32 decision; exact fp64 evaluation only where it cannot certify
                 const bool sure = qnet_screen<M, LPE>(sf, T, H, task, xt, xr, tier);
@@ -422,6 +429,12 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
                rollout_smem_bytes(T, M, p.H, true, 0, true) <= 200 * 1024;
     p.screen_stats = p.screen ? env->d_screen : nullptr;
     p.qpack = env->d_qpack;
+    p.pow2_scales = 1;
+    for (int m = 0; m < M; ++m) {
+        int ex = 0;
+        const double s = env->cfg.batch_scales[m];
+        if (!(s > 0.0) || frexp(s, &ex) != 0.5 || ex < -1000 || ex > 1000) p.pow2_scales = 0;
+    }
     {
         int ok_pack = M <= 3;
         for (int m = 0; m < M; ++m)

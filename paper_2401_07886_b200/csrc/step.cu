@@ -74,6 +74,8 @@ struct StepParams {
     double* x_out;
     int32_t* status;
     int32_t drain;
+    int32_t new_segment;      // drain + reset replicas and estimator (be_env_new_segment)
+    const uint8_t* seg_mask;  // drain / new_segment: only envs with mask[e] != 0 (NULL = all)
     const double* skip;  // skip table (global), NULL = skipping off
     // device-step mode (be_train_iteration): epsilon, Philox counter and the
     // pending slot of x_out / action_out come from the iteration index *iter_dev
@@ -140,10 +142,20 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     const RecOut out = RecOut::row(p.rec, (int64_t)e * p.rec_ld);
     bool ok = true;
     if (p.drain) {
-        if (al) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out);
-        if (al) reps_of(p.state, e, p.R)[gl] = r;
+        // drain (simcore.py:151-153); new_segment: the stable-segment reset of run_eval
+        // (evalkit.py:186-192) — drain, then a fresh ClusterSim and estimator for the
+        // selected envs; request ids keep counting (they are trace indices)
+        const bool sel = live && (!p.seg_mask || p.seg_mask[e]);
+        if (al && sel) ok = advance_lane(r, tc, __longlong_as_double(0x7ff0000000000000LL), ring, mask, sc, out);
+        if (sel && p.new_segment) rep_reset(r);  // the FIFO is empty: its cursor may stay
+        if (al && sel) reps_of(p.state, e, p.R)[gl] = r;
+        if (sel && p.new_segment && gl == 0) {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) es->w[k] = 0.0;
+            es->n = 0;
+        }
         const bool all_ok = (__ballot_sync(FULL, !ok) & gmask) == 0;
-        if (live && !all_ok && gl == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
+        if (sel && !all_ok && gl == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
         return;
     }
     const double U = p.arrival[e];
@@ -385,9 +397,12 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     return dispatch_step(p, step_smem_bytes(), st, wl);
 }
 
-int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st) {
+int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st,
+                     const uint8_t* mask, int new_segment) {
     StepParams p = base_params(env, rec_ld, rec);
     p.drain = 1;
+    p.seg_mask = mask;
+    p.new_segment = new_segment;
     return dispatch_step(p, step_smem_bytes(), st);
 }
 

@@ -192,6 +192,17 @@ class EnvBatch:
         _lib.check(self._L.be_env_drain(self._h, records.ld, ctypes.byref(rec),
                                         _lib.stream_ptr(stream)))
 
+    def new_segment(self, records: "StepRecords", mask: Optional[torch.Tensor] = None,
+                    stream=None) -> None:
+        """run_eval's stable-segment reset (evalkit.py:186-192) for the envs with
+        mask[e] != 0 (all if None): drain into `records`, fresh replicas and an
+        empty estimator window; request ids keep counting."""
+        if mask is not None:
+            _check_vec(mask, "mask", torch.uint8, self.n_envs, self.device)
+        rec = records.struct()
+        _lib.check(self._L.be_env_new_segment(self._h, _lib.ptr(mask), records.ld, ctypes.byref(rec),
+                                              _lib.stream_ptr(stream)))
+
 
 def _check_vec(t, name, dtype, n, dev):
     if not isinstance(t, torch.Tensor) or t.dtype != dtype or t.device != dev or t.numel() < n \

@@ -305,7 +305,12 @@ def reduce_eval(trace: TraceBatch, flags: torch.Tensor, reward: torch.Tensor,
                 window: int = WINDOW, stream=None) -> ReduceResult:
     """On-device windowed + threshold_counts + per-bucket miss/request/reward."""
     E, dev = trace.n_envs, trace.device
-    th = torch.tensor(list(thresholds), dtype=torch.float64)  # host array: taus computed on host
+    if not 1 <= len(thresholds) <= _lib.MAX_THETA:
+        raise ValueError(f"between 1 and {_lib.MAX_THETA} thresholds")
+    th = _lib.BeThresholds()
+    th.n = len(thresholds)
+    for k, t in enumerate(thresholds):
+        th.theta[k] = float(t)
     K = int(n_buckets)
     out = ReduceResult(tuple(thresholds),
                        torch.empty((E, len(thresholds)), dtype=torch.int64, device=dev),
@@ -315,7 +320,7 @@ def reduce_eval(trace: TraceBatch, flags: torch.Tensor, reward: torch.Tensor,
                        torch.empty((E, K), dtype=torch.float64, device=dev))
     L = _lib.load()
     _lib.check(L.be_reduce_eval(trace.soa(), flags.data_ptr(), reward.data_ptr(), int(window),
-                                th.data_ptr(), len(thresholds), K, out.win_counts.data_ptr(),
+                                th, K, out.win_counts.data_ptr(),
                                 out.n_windows.data_ptr(), out.bucket_miss.data_ptr(),
                                 out.bucket_req.data_ptr(), out.bucket_reward.data_ptr(),
                                 _lib.stream_ptr(stream)))

@@ -94,6 +94,7 @@ class TrainResult:
     log: list = field(default_factory=list)
     updates: int = 0
     transitions: int = 0
+    max_inflight: int = 0  # most decisions any request stayed unresolved (pending store high-water)
 
 
 class DeviceLearner:
@@ -447,7 +448,7 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     if timing is not None:
         timing["loop_ms"] = t_begin.elapsed_time(t_end)
     res = TrainResult(net=learner.net(), log=log, updates=int(learner.counters[1]),
-                      transitions=int(learner.ring_state[2]))
+                      transitions=int(learner.ring_state[2]), max_inflight=int(learner.ring_state[4]))
     learner.close()
     env.close()
     return res

@@ -15,8 +15,10 @@ SEEDS = (7, 8, 9, 10)
 # device replay, batch 512, 8-256-3 Q-MLP, Adam 1e-4, Huber, target sync 500, epsilon
 # 1.0 -> 0.05 over 25 %, warm-up 10k; one update per iteration (= per 4096 env-steps),
 # 200k iterations = the reference recipe's number of updates (trainer.py:374-401)
+# pending_capacity: decisions a request may stay in flight (exploration overloads tiers
+# for long stretches; measured high-water mark in profiles/r2_config3_policies.json)
 CONFIG3 = dict(n_envs=4096, batch_size=512, buffer_capacity=1 << 20, iterations=200_000,
-               updates_per_step=1)
+               updates_per_step=1, pending_capacity=1 << 16)
 
 
 def traces():
@@ -53,7 +55,7 @@ def train_config3(seed, device, iterations=None, timing=None):
                       total_iterations=its, log_every=its, seed=seed)
     return run_training(default_tiers(), RewardSpec.default(), cfg, n_envs=CONFIG3["n_envs"],
                         updates_per_step=CONFIG3["updates_per_step"], mode="graph", device=device,
-                        timing=timing)
+                        pending_capacity=CONFIG3["pending_capacity"], timing=timing)
 
 
 def welch_ok(ref, dev, slack=0.02):

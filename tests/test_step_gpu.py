@@ -13,12 +13,11 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("name", ["unpredictable-1_mixed1", "unpredictable-2_static2",
                                   "hellaswag-copa-soft_mixed2", "cfg1_32_trained_t1",
-                                  "unpredictable-1_trained", "hw-utility-8gpu_trained"])
+                                  "unpredictable-1_trained", "hw-utility-8gpu_trained",
+                                  "stable_mixed0", "stable_trained", "stable_static1"])
 def test_step_api_matches_reference(cuda, name):
     g = goldens.load(name)
     m = g["meta"]
-    if m["reset"]:
-        pytest.skip("segment resets are driven by the caller in the step API")
     E = 3  # identical copies: every env must reproduce the golden
     n = len(g["arrival"])
     env = EnvBatch(tiers_of(m), reward_of(m), E, enc_of(m), estimator_mode=m["estimator_mode"],
@@ -34,7 +33,13 @@ def test_step_api_matches_reference(cuda, name):
         rates[starts[k]:starts[k + 1]] = g["seg_rate"][k]
     tr = torch.as_tensor(np.repeat(rates[:, None], E, 1), device=cuda)
     obs, rate, act, xs = [], [], [], []
+    seg_starts = set(int(x) for x in g["seg_start"]) if m["reset"] else set()
+    half = torch.tensor([1, 0, 1][:E], dtype=torch.uint8, device=cuda)
     for i in range(n):
+        if i in seg_starts and i > 0:
+            # run_eval's segment reset (evalkit.py:186-192); masked in two calls
+            env.new_segment(rec, mask=half)
+            env.new_segment(rec, mask=1 - half)
         o = env.step(arr[i], tsk[i], rec, true_rate=tr[i], policy=dn, static_tier=m["static_tier"],
                      want_x=True)
         obs.append(o["obs"])

@@ -45,7 +45,7 @@ def main():
         f = ps.window_fractions_gpu(res.net, z, dev)
         out["gpu"][s] = f.tolist()
         out["train"][s] = dict(loop_s=t["loop_ms"] / 1e3, wall_s=wall, updates=res.updates,
-                               transitions=res.transitions,
+                               transitions=res.transitions, max_inflight=res.max_inflight,
                                iterations_per_s=a.iterations / (t["loop_ms"] / 1e3),
                                final_loss=res.log[-1].loss if res.log else None)
         if not a.no_save:
