@@ -179,6 +179,19 @@ int32_t be_env_create(const be_cfg* cfg, int32_t n_envs, int32_t device, be_env*
     cudaMemset(env->d_status, 0, 64);
     cudaMemset(env->d_screen, 0, 16);
     env->envs = nullptr;
+    // a replica holds at most `capacity` requests, so obs_m <= replicas_m x capacity
+    env->exact_mul = 1;
+    for (int m = 0; m < cfg->n_tiers && env->exact_mul; ++m) {
+        const double s = cfg->batch_scales[m], inv = 1.0 / s;
+        const long long top = (long long)cfg->tiers[m].replicas << cap_log2;
+        for (long long o = 0; o <= top; ++o) {
+            volatile double a = (double)o * inv, b = (double)o / s;
+            if (a != b) {
+                env->exact_mul = 0;
+                break;
+            }
+        }
+    }
     if (cfg->skip_ahead) {
         env->skip_rows = build_skip_table(*cfg, nullptr);
         const size_t tb = (size_t)env->skip_rows * SKIP_NB * sizeof(double);

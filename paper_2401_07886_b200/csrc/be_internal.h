@@ -31,6 +31,8 @@ struct be_env {
     unsigned long long* d_screen;  // [2] screened decisions, fp64 fallbacks (rollout)
     double* d_qpack;    // packed fp64 Q weights for the screened rollout's fallback (max size)
     int32_t last_plan[8];  // be_env_rollout_plan: what the last be_rollout_greedy launched
+    int32_t exact_mul;     // obs * (1/s_m) == obs / s_m for every reachable obs (<= R_m x ring
+                           // capacity) and tier m: encode may multiply (policy.py:63)
 };
 
 namespace be {

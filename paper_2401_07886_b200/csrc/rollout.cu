@@ -77,7 +77,9 @@ struct RolloutParams {
     int32_t skip_rows;
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
-    int32_t pow2_scales;  // 1 = every encoding batch scale is a power of two (x * (1/s) exact)
+    int32_t exact_mul;   // 1 = obs * (1/s) == obs / s for every reachable obs and tier
+                         // (be_env.exact_mul; always so for power-of-two scales); the
+                         // throughput variant (OCC = 1) is launched only then
     unsigned long long* screen_stats;  // [2] decisions screened, fp64 fallbacks (nullable)
     int32_t pack_obs;    // 1: per-tier queue sums fit 10-bit fields (observe with one REDUX)
     const double* qpack;  // screen on: the fp64 fallback's packed weights (QLayout) in global
@@ -143,8 +145,9 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
         const double q = __dmul_rn(a, inv);
         return __fma_rn(__fma_rn(-q, s, a), inv, q);
     };
-    // power-of-two batch scales (the shipped 128/32/8): the product IS the quotient
-    const bool pow2_scales = p.pow2_scales != 0;
+    // the product IS the quotient for every reachable obs (the shipped 128/32/8 are
+    // powers of two); the throughput variant relies on it (host-checked)
+    const bool mul_ok = OCC ? true : p.exact_mul != 0;
 
     // per-group ("group-uniform") env state
     int env = -1;
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
             double xt[M], q[M];
 #pragma unroll
             for (int m = 0; m < M; ++m)
-                xt[m] = pow2_scales ? __dmul_rn((double)obs[m], inv_scale[m])
+                xt[m] = mul_ok ? __dmul_rn((double)obs[m], inv_scale[m])
                                     : div_by((double)obs[m], p.cfg.batch_scales[m], inv_scale[m]);
             const double xr = true_rate ? cur_xr : div_by(rate, p.cfg.rate_scale, inv_rate_scale);
             if (screen) {
@@ -349,7 +352,8 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
 template <int M, int LPE>
 static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms, int32_t* plan) {
     // the throughput variant once the batch fills BE_ROLLOUT_MINB CTAs on every SM
-    const bool many = (long long)p.E >= (long long)sms * BE_ROLLOUT_MINB * (BE_ROLLOUT_THREADS / LPE);
+    const bool many = (long long)p.E >= (long long)sms * BE_ROLLOUT_MINB * (BE_ROLLOUT_THREADS / LPE) &&
+                      p.exact_mul;
     auto kern = !p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 0, 0>
                 : many                     ? rollout_kernel<M, LPE, 1, 1>
                                            : rollout_kernel<M, LPE, 1, 0>;
@@ -429,12 +433,7 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
                rollout_smem_bytes(T, M, p.H, true, 0, true) <= 200 * 1024;
     p.screen_stats = p.screen ? env->d_screen : nullptr;
     p.qpack = env->d_qpack;
-    p.pow2_scales = 1;
-    for (int m = 0; m < M; ++m) {
-        int ex = 0;
-        const double s = env->cfg.batch_scales[m];
-        if (!(s > 0.0) || frexp(s, &ex) != 0.5 || ex < -1000 || ex > 1000) p.pow2_scales = 0;
-    }
+    p.exact_mul = env->exact_mul;
     {
         int ok_pack = M <= 3;
         for (int m = 0; m < M; ++m)

@@ -266,7 +266,7 @@ class _DevPtr:
 
 def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=None,
                  completion_log=None, *, n_envs: int = 1, updates_per_step: int = 1,
-                 pending_capacity: int = 4096, ring_capacity: int = 1024, device=None,
+                 pending_capacity: Optional[int] = None, ring_capacity: int = 1024, device=None,
                  world=None, mode: str = "device", graph_chunk: int = 0,
                  timing: Optional[dict] = None, exchange: str = "nccl") -> TrainResult:
     """trainer.py:333-406 on the GPU for `n_envs` lockstep environments.
@@ -313,6 +313,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         encoding = StateEncoding(n_tasks=n_tasks, batch_scales=tuple(float(t.max_batch) for t in tiers))
     dev = _lib.require_cuda(device)
     E = int(n_envs)
+    if pending_capacity is None:
+        pending_capacity = default_pending_capacity(E, n_tasks + n_tiers + 1)
     learner = DeviceLearner(n_tasks, n_tiers, cfg, E, pending_capacity, dev)
     if init_net is None:
         rng = np.random.default_rng(np.random.SeedSequence(cfg.seed).spawn(4)[0])
@@ -452,6 +454,19 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     learner.close()
     env.close()
     return res
+
+
+def default_pending_capacity(n_envs: int, input_dim: int, budget_bytes: float = 8e9) -> int:
+    """Decisions a request may stay unresolved (the pending store is [P][E] states +
+    actions + rewards + flags): the largest power of two in [4096, 65536] within
+    `budget_bytes`.  Exploration can overload a tier for long stretches — the
+    config-3 recipe (4096 envs, 200k iterations) peaked at 6,430 decisions
+    (profiles/r2_config3_policies.json); the reference's dict has no bound."""
+    per = float(n_envs) * (8 * input_dim + 1 + 1 + 8)
+    p = 65536
+    while p > 4096 and p * per > budget_bytes:
+        p //= 2
+    return p
 
 
 def _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
