@@ -11,6 +11,8 @@
  *   be_env_reset                     ClusterSim(tiers) (re-create) evalkit.py:189-191
  *   be_env_step                      advance + observe + encode +  evalkit.py:185-205,
  *                                    forward/argmax + submit        simcore.py:94-157
+ *   be_env_step_observe / _submit    the same, split around any    evalkit.py:185-205
+ *                                    router (e.g. be_qnet_route_tc)
  *   be_env_drain                     ClusterSim.drain              simcore.py:151-153
  *   be_env_new_segment               segment reset of run_eval     evalkit.py:186-192
  *   be_rollout_greedy                run_eval (whole trace)        evalkit.py:154-209
@@ -170,6 +172,20 @@ int32_t be_env_step(be_env* env, const double* arrival_ms, const uint8_t* task,
                     uint64_t philox_seed, uint64_t philox_counter, int64_t rec_ld,
                     be_records* rec, int32_t* obs_out, double* rate_out,
                     uint8_t* action_out, double* q_out, double* x_out, void* stream);
+/* The same step split around a router of the caller's choice (the reference's
+ * own order, evalkit.py:185-205: advance / observe / encode, then select_action,
+ * then submit).  be_env_step_observe advances every env to its arrival (scoring
+ * completions into rec), updates the estimator and writes the encoded state
+ * x_out [E][D] (required), obs_out [E][M] and rate_out [E] (nullable); it makes
+ * no decision.  be_env_step_submit then submits request `next id` of every env
+ * to the tier in action [E] (e.g. the output of be_qnet_route_tc on x_out) — the
+ * same arrival/task arrays as the observe call.  observe + route + submit ==
+ * be_env_step with that router's decisions. */
+int32_t be_env_step_observe(be_env* env, const double* arrival_ms, const uint8_t* task,
+                            const double* true_rate, int64_t rec_ld, be_records* rec, double* x_out,
+                            int32_t* obs_out, double* rate_out, void* stream);
+int32_t be_env_step_submit(be_env* env, const double* arrival_ms, const uint8_t* task, const uint8_t* action,
+                           int64_t rec_ld, be_records* rec, void* stream);
 /* Run every replica to completion (simcore.py:151-153). */
 int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream);
 /* Stable-segment reset of run_eval (evalkit.py:186-192) for the envs with
@@ -420,7 +436,13 @@ typedef struct {
     int32_t phase;
     int32_t update_index;
     int32_t use_gate;
+    int32_t router;   /* BE_ROUTER_FP64: the decision inside the env step (fp64 Q);
+                         BE_ROUTER_TC: observe -> tensor-core router (be_qnet_route_tc,
+                         tcgen05, certified + fp64 fallback: the same decisions) -> submit */
+    int32_t _pad;
 } be_train_iter_cfg;
+#define BE_ROUTER_FP64 0
+#define BE_ROUTER_TC 1
 
 int32_t be_train_iteration(be_learner* learner, be_env* env, const be_train_iter_cfg* cfg,
                            void* stream);

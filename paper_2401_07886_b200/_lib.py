@@ -106,7 +106,8 @@ class BeTrainIterCfg(ctypes.Structure):
                 ("sample_seed", ctypes.c_uint64), ("epsilon_start", ctypes.c_double),
                 ("epsilon_end", ctypes.c_double), ("epsilon_decay_steps", ctypes.c_int64),
                 ("updates_per_step", ctypes.c_int32), ("phase", ctypes.c_int32),
-                ("update_index", ctypes.c_int32), ("use_gate", ctypes.c_int32)]
+                ("update_index", ctypes.c_int32), ("use_gate", ctypes.c_int32),
+                ("router", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class BeLearnerViews(ctypes.Structure):
@@ -139,6 +140,8 @@ SIGNATURES = {
                            _I64, ctypes.POINTER(BeRecords), _P, _P, _P, _P, _P, _P]),
     "be_env_drain": (_I32, [_P, _I64, ctypes.POINTER(BeRecords), _P]),
     "be_env_new_segment": (_I32, [_P, _P, _I64, ctypes.POINTER(BeRecords), _P]),
+    "be_env_step_observe": (_I32, [_P, _P, _P, _P, _I64, ctypes.POINTER(BeRecords), _P, _P, _P, _P]),
+    "be_env_step_submit": (_I32, [_P, _P, _P, _P, _I64, ctypes.POINTER(BeRecords), _P]),
     "be_rollout_greedy": (_I32, [_P, ctypes.POINTER(BeTraceSoa), ctypes.POINTER(BeQWeights), _I32,
                                  _P, ctypes.POINTER(BeRecords), _P]),
     "be_qnet_route_f64": (_I32, [ctypes.POINTER(BeQWeights), _I32, _I32, _P, _I32, _D, _U64, _U64,

@@ -330,6 +330,26 @@ int32_t be_env_step(be_env* env, const double* arrival_ms, const uint8_t* task,
                            q_out, x_out, (cudaStream_t)stream);
 }
 
+int32_t be_env_step_observe(be_env* env, const double* arrival_ms, const uint8_t* task,
+                            const double* true_rate, int64_t rec_ld, be_records* rec, double* x_out,
+                            int32_t* obs_out, double* rate_out, void* stream) {
+    if (!env || !arrival_ms || !task || !rec || !rec->flags || !rec->reward || !x_out)
+        return set_error(BE_EINVAL, "NULL argument");
+    if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");
+    if (env->cfg.estimator_true_rate && !true_rate) return set_error(BE_EINVAL, "true-rate mode needs true_rate");
+    return launch_env_step_split(env, 1, arrival_ms, task, true_rate, nullptr, x_out, obs_out, rate_out, rec_ld,
+                                 rec, (cudaStream_t)stream);
+}
+
+int32_t be_env_step_submit(be_env* env, const double* arrival_ms, const uint8_t* task, const uint8_t* action,
+                           int64_t rec_ld, be_records* rec, void* stream) {
+    if (!env || !arrival_ms || !task || !action || !rec || !rec->flags || !rec->reward)
+        return set_error(BE_EINVAL, "NULL argument");
+    if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");
+    return launch_env_step_split(env, 2, arrival_ms, task, nullptr, const_cast<uint8_t*>(action), nullptr, nullptr,
+                                 nullptr, rec_ld, rec, (cudaStream_t)stream);
+}
+
 int32_t be_env_drain(be_env* env, int64_t rec_ld, be_records* rec, void* stream) {
     if (!env || !rec || !rec->flags || !rec->reward) return set_error(BE_EINVAL, "NULL argument");
     if (rec_ld < 1) return set_error(BE_EINVAL, "rec_ld must be >= 1");

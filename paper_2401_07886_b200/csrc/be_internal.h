@@ -96,7 +96,13 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st, const struct WorkloadArgs* wl = nullptr);
+                        double* x_base, cudaStream_t st, const struct WorkloadArgs* wl = nullptr,
+                        int phase = 0);
+// split step: phase 1 = advance + observe + encode into x_out (no decision), phase 2 =
+// submit the decisions in `action` (a router runs in between)
+int launch_env_step_split(be_env* env, int phase, const double* arrival, const uint8_t* task,
+                          const double* true_rate, uint8_t* action, double* x_out, int32_t* obs_out,
+                          double* rate_out, int64_t rec_ld, const be_records* rec, cudaStream_t st);
 size_t env_state_bytes_per_env(int R);
 int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* reward, int window,
                   const double* thetas, int n_theta, int n_buckets, int64_t* win_counts,
@@ -105,10 +111,18 @@ int launch_reduce(const be_trace_soa* tr, const uint8_t* flags, const double* re
 int launch_route(const be_qweights* W, int T, int M, const double* x, int B, double eps,
                  uint64_t seed, uint64_t counter, double* q_out, uint8_t* a_out, cudaStream_t st);
 bool route_tc_supported(int T, int M, int H);
+// sets the router kernel's shared-memory attribute ahead of any CUDA-graph capture
+void route_tc_prepare(int T, int M, int H);
 size_t route_tc_workspace_bytes(int H);
 int launch_route_tc(const be_qweights* W, int T, int M, const double* x, int B, double eps, uint64_t seed,
                     uint64_t counter, float* q_out, uint8_t* a_out, void* workspace, int64_t* stats,
                     cudaStream_t st);
+// device-iteration form (be_train_iteration, router = tensor cores): x / a_out are the
+// pending store's bases, slot *iter_dev % pending_P; epsilon_at(*iter_dev) and the
+// Philox counter *iter_dev are read on the device, so a CUDA graph replays it unchanged
+int launch_route_tc_dev(const be_qweights* W, int T, int M, const double* x_base, int B, uint64_t seed,
+                        const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
+                        int32_t pending_P, uint8_t* a_base, void* workspace, int64_t* stats, cudaStream_t st);
 int launch_tracegen(int E, int64_t env_offset, int64_t n, int64_t ld, const double* rate, int n_tasks, uint64_t seed,
                     double* arrival, uint8_t* task, cudaStream_t st);
 int launch_tracegen_general(const be_gen_cfg* cfg, int E, int64_t env_offset, int64_t ld,

@@ -52,4 +52,17 @@ __host__ __device__ __forceinline__ uint32_t below(uint32_t r, uint32_t n) {
     return (uint32_t)(((uint64_t)r * n) >> 32);
 }
 
+// TrainConfig.epsilon_at (trainer.py:85-90), the same IEEE operations as the host
+__host__ __device__ __forceinline__ double epsilon_at(int64_t it, double start, double end, int64_t decay) {
+    if (decay <= 0) return end;
+#ifdef __CUDA_ARCH__
+    const double frac = fmin(1.0, __ddiv_rn((double)it, (double)decay));
+    return __dadd_rn(start, __dmul_rn(__dsub_rn(end, start), frac));
+#else
+    const double q = (double)it / (double)decay;
+    const double frac = q < 1.0 ? q : 1.0;
+    return start + (end - start) * frac;
+#endif
+}
+
 }  // namespace be

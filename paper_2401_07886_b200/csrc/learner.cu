@@ -718,13 +718,18 @@ struct be_learner {
     const unsigned long long* x_flag[XMAX_RANKS];
     void* x_opened[XMAX_RANKS];  // peer allocations opened through CUDA IPC (closed at destroy)
     int64_t* gate;     // DP update gate (be_train_iteration use_gate)
+    // tensor-core router (be_train_iteration router = BE_ROUTER_TC): packed weight image
+    // (rebuilt every iteration: the weights change with every update) and statistics
+    void* tc_img;       // NULL when the network shape is outside route_tc's support
+    int64_t* tc_stats;  // [2] states routed, fp64 re-evaluations
 };
 
 static void learner_free(be_learner* L) {
     void* ptrs[] = {L->params, L->target, L->m, L->v, L->grad, L->partial, L->loss, L->counters,
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
                     L->preward, L->low, L->status, L->wl_state,
-                    L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket};
+                    L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket,
+                    L->tc_img, L->tc_stats};
     for (void* p : ptrs) cudaFree(p);
     for (int r = 0; r < XMAX_RANKS; ++r)
         if (L->x_opened[r]) cudaIpcCloseMemHandle(L->x_opened[r]);
@@ -790,6 +795,15 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         return set_cuda_error(e, "be_learner_create: exchange buffer");
     }
     cudaMemset(L->xmem, 0, xmem_bytes(L));
+    if (route_tc_supported(c->n_tasks, c->n_tiers, c->hidden)) {
+        if ((e = cudaMalloc(&L->tc_img, route_tc_workspace_bytes(c->hidden))) != cudaSuccess ||
+            (e = cudaMalloc((void**)&L->tc_stats, 16)) != cudaSuccess) {
+            learner_free(L);
+            return set_cuda_error(e, "be_learner_create: tensor-core router workspace");
+        }
+        cudaMemset(L->tc_stats, 0, 16);
+        route_tc_prepare(c->n_tasks, c->n_tiers, c->hidden);
+    }
     // configured here, not at launch time: launches may be captured in a CUDA graph
     cudaFuncSetAttribute(learner_partial_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(learner_partial_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1121,6 +1135,10 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         return set_error(BE_EINVAL, "bad phase / update index");
     if (!(cf.rate_low > 0) || cf.rate_high < cf.rate_low)
         return set_error(BE_EINVAL, "need 0 < rate_low <= rate_high");
+    if (c->router != BE_ROUTER_FP64 && c->router != BE_ROUTER_TC) return set_error(BE_EINVAL, "unknown router");
+    if (c->router == BE_ROUTER_TC && !L->tc_img)
+        return set_error(BE_EINVAL, "the tensor-core router needs n_tiers <= 4, n_tasks + n_tiers + 2 <= 16 and "
+                                    "hidden a multiple of 32 in [32, 256]");
     const int64_t* it = L->counters + 3;
     const int E = cf.n_envs, D = L->D, H = cf.hidden, M = cf.n_tiers;
     int rc;
@@ -1142,9 +1160,25 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         be_records rec{};
         rec.flags = L->pflags;
         rec.reward = L->preward;
-        rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
-                                 c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
-                                 cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl);
+        if (c->router == BE_ROUTER_TC) {
+            // observe + encode (pending slot) -> certified tcgen05 router on the E states
+            // (epsilon and Philox counter from the device iteration index) -> submit
+            rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                     c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 1);
+            if (rc) return rc;
+            rc = launch_route_tc_dev(&W, cf.n_tasks, M, L->px, E, c->policy_seed, it, c->epsilon_start,
+                                     c->epsilon_end, c->epsilon_decay_steps, cf.pending_capacity, L->pa,
+                                     L->tc_img, L->tc_stats, st);
+            if (rc) return rc;
+            rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                     c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2);
+        } else {
+            rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                     c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl);
+        }
         if (rc) return rc;
         rc = commit_impl(L, 0, it, st);
         if (rc) return rc;

@@ -29,6 +29,24 @@
 // table in shared memory, 0.84e9 at 3 CTAs/SM), so it keeps 2 CTAs/SM and stages the
 // skip table; the true-rate variant runs 3 CTAs/SM and reads it through L1 when the
 // batch fills them (config 4), else 2 CTAs/SM (config 1: 18 envs, latency-bound).
+#ifndef BE_TRACE_EVICT_FIRST
+#define BE_TRACE_EVICT_FIRST 0
+#endif
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int ld_stream_u8(const uint8_t* p, uint64_t pol) {
+    unsigned short v;
+    asm volatile("ld.global.cg.L2::cache_hint.u8 %0, [%1], %2;" : "=h"(v) : "l"(p), "l"(pol));
+    return (int)v;
+}
 #ifndef BE_ROLLOUT_MINB
 #define BE_ROLLOUT_MINB 3  // resident CTAs per SM the register allocation is capped for (true rate)
 #endif
@@ -77,6 +95,8 @@ struct RolloutParams {
     int32_t skip_rows;
     int32_t skip_smem;   // 1 = stage the skip table in shared memory
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
+    double inv_scale[BE_MAX_TIERS];  // 1 / batch_scales[m] (host IEEE division)
+    double inv_rate_scale;           // 1 / rate_scale
     int32_t exact_mul;   // 1 = obs * (1/s) == obs / s for every reachable obs and tier
                          // (be_env.exact_mul; always so for power-of-two scales); the
                          // throughput variant (OCC = 1) is launched only then
@@ -130,6 +150,9 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
     const TierC tc = lane_tier(p.cfg, gl, skip_tab);
     const bool active_lane = tc.tier >= 0;
     const uint32_t mask = (1u << p.cap_log2) - 1u;
+#if BE_TRACE_EVICT_FIRST
+    const uint64_t l2_first = l2_policy_evict_first();
+#endif
     constexpr bool true_rate = TR != 0;
     const bool reset_segs = p.cfg.reset_between_segments != 0;
     const double INF = __longlong_as_double(0x7ff0000000000000LL);
@@ -137,10 +160,10 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
     // Markstein correction step (residual a - q s exact by FMA, q + r (1/s) rounded
     // once) — the correctly rounded quotient, bit-identical to __ddiv_rn for every
     // scale (not only the power-of-two ones), two DFMA instead of a DDIV sequence
-    double inv_scale[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) inv_scale[m] = __ddiv_rn(1.0, p.cfg.batch_scales[m]);
-    const double inv_rate_scale = __ddiv_rn(1.0, p.cfg.rate_scale);
+    // 1/s precomputed on the host (IEEE division there too) and read as constant-bank
+    // operands: no registers held across the request loop
+#define INV_SCALE(m) p.inv_scale[m]
+#define INV_RATE_SCALE p.inv_rate_scale
     auto div_by = [](double a, double s, double inv) {
         const double q = __dmul_rn(a, inv);
         return __fma_rn(__fma_rn(-q, s, a), inv, q);
@@ -157,7 +180,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
 
     int n = 0, i = 0, next_seg = INT_MAX;
     auto seg_mark = [&](int64_t k) { return k < seg_end ? (int)min(p.seg_start[k], (int64_t)INT_MAX) : INT_MAX; };
-    double cur_rate = 0.0, cur_xr = 0.0;  // true-rate mode: the segment's rate / rate_scale
+    double cur_xr = 0.0;  // true-rate mode: the current segment's rate / rate_scale (NaN before a mark)
     Slot* ring = p.rings;
     Rep r;
     rep_reset(r);
@@ -204,7 +227,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                 seg = p.seg_off[env];
                 seg_end = p.seg_off[env + 1];
                 next_seg = seg_mark(seg);
-                cur_rate = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
+                cur_xr = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
                 ring = p.rings + ((size_t)env * p.R + (active_lane ? gl : 0)) * ((size_t)mask + 1);
                 rep_reset(r);
                 r.head = 0;
@@ -225,8 +248,15 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                 // through L2 only (ld.global.cg): rows that arrive during the kernel
                 // (streamed upload) are never served from a stale L1 line; read-once
                 // rows gain nothing from L1 anyway (A/B: 1% faster than a branch)
+#if BE_TRACE_EVICT_FIRST
+                // read-once trace rows: evict-first in L2, so the 9 B/request stream does
+                // not push the FIFO rings, records and spill lines of the envs in flight out
+                pf_arr = ld_stream_f64(p.arrival + base + ii, l2_first);
+                pf_task = ld_stream_u8(p.task + base + ii, l2_first);
+#else
                 pf_arr = __ldcg(p.arrival + base + ii);
                 pf_task = __ldcg(p.task + base + ii);
+#endif
                 if (pf_task >= T) {  // task id outside the reward spec (encode raises,
                     bad = true;      // policy.py:57-58): the env fails with BE_EINVAL
                     pf_task = 0;
@@ -246,14 +276,13 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                     rep_reset(r);
                     est.n = 0;
                 }
-                cur_rate = p.seg_rate[seg];
-                if (true_rate) cur_xr = __ddiv_rn(cur_rate, p.cfg.rate_scale);  // once per segment
+                if (true_rate) cur_xr = __ddiv_rn(p.seg_rate[seg], p.cfg.rate_scale);  // once per segment
                 ++seg;
                 next_seg = seg_mark(seg);
             }
             if (active_lane) ok &= advance_lane(r, tc, U, ring, mask, sc, out);
             // true-rate mode never reads the arrival window (workload.py:241-242)
-            rate = true_rate ? cur_rate : estimator_observe(est, U, false, cur_rate, p.cfg.prior_rate);
+            if (!true_rate) rate = estimator_observe(est, U, false, 0.0, p.cfg.prior_rate);
         }
         int obs[M];
         if (M <= 3 && p.pack_obs) {
@@ -276,9 +305,9 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
             double xt[M], q[M];
 #pragma unroll
             for (int m = 0; m < M; ++m)
-                xt[m] = mul_ok ? __dmul_rn((double)obs[m], inv_scale[m])
-                                    : div_by((double)obs[m], p.cfg.batch_scales[m], inv_scale[m]);
-            const double xr = true_rate ? cur_xr : div_by(rate, p.cfg.rate_scale, inv_rate_scale);
+                xt[m] = mul_ok ? __dmul_rn((double)obs[m], INV_SCALE(m))
+                                    : div_by((double)obs[m], p.cfg.batch_scales[m], INV_SCALE(m));
+            const double xr = true_rate ? cur_xr : div_by(rate, p.cfg.rate_scale, INV_RATE_SCALE);
             if (screen) {
                 // certified fp32 decision; exact fp64 evaluation only where it cannot certify
                 const bool sure = qnet_screen<M, LPE>(sf, T, H, task, xt, xr, tier);
@@ -305,7 +334,9 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
             for (int m = 0; m < M; ++m)
                 if (gl == m) p.rec.obs[(base + i) * M + m] = obs[m];
         }
-        if (live && p.rec.rate && gl == 0) p.rec.rate[base + i] = rate;
+        if (live && p.rec.rate && gl == 0) {  // true-rate mode: the segment's rate (NaN before a mark)
+            p.rec.rate[base + i] = !true_rate ? rate : cur_xr == cur_xr ? p.seg_rate[seg - 1] : cur_xr;
+        }
         // replica argmin of (len(active), len(queue), id) == argmin (count, replica)
         const unsigned key = (live && tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)gl) : 0xffffffffu;
         const unsigned best = group_min<LPE>(key, grp);
@@ -434,6 +465,8 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     p.screen_stats = p.screen ? env->d_screen : nullptr;
     p.qpack = env->d_qpack;
     p.exact_mul = env->exact_mul;
+    for (int m = 0; m < M; ++m) p.inv_scale[m] = 1.0 / env->cfg.batch_scales[m];
+    p.inv_rate_scale = 1.0 / env->cfg.rate_scale;
     {
         int ok_pack = M <= 3;
         for (int m = 0; m < M; ++m)

@@ -179,6 +179,12 @@ struct RouteTcParams {
     float* q_out;
     uint8_t* a_out;
     unsigned long long* stats;  // [2] states, fp64 fallbacks (nullable)
+    // device-iteration mode (nullable): x / a_out advance by slot * B rows, slot =
+    // *iter_dev % pending_P; epsilon = epsilon_at(*iter_dev), Philox counter = *iter_dev
+    const int64_t* iter_dev;
+    double eps_start, eps_end;
+    int64_t eps_decay;
+    int32_t pending_P;
 };
 
 // DM: compile-time bound of the input count D (8 for the shipped 4 tasks x 3 tiers)
@@ -197,6 +203,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
     int* flist = fcount + 1;  // [TC_FLIST]
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int r = tid & (TC_ROWS - 1);  // TMEM lane of this thread
+    const double* X = p.x;
+    uint8_t* A = p.a_out;
+    double eps = p.eps;
+    uint64_t ctr = p.counter;
+    if (p.iter_dev) {
+        const int64_t it = *p.iter_dev;
+        const size_t slot = (size_t)(it % p.pending_P);
+        X += slot * (size_t)p.B * p.D;
+        A += slot * (size_t)p.B;
+        eps = epsilon_at(it, p.eps_start, p.eps_end, p.eps_decay);
+        ctr = (uint64_t)it;
+    }
     const int hs = tid >> 7;            // 0: lower threads, 1: upper threads
     const int D = p.D, H = p.H, HP = H / 2;
     const int nch = HP / TC_CW, c_mid = (nch + 1) / 2;
@@ -239,7 +257,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
 #pragma unroll
             for (int s = 0; s < TC_FBS; ++s) {
                 rf[s] = flist[f0 + s < nf ? f0 + s : f0];  // past the end: repeat the first, no output
-                xv[s] = lane < D ? __ldg(p.x + (size_t)rf[s] * D + lane) : 0.0;
+                xv[s] = lane < D ? __ldg(X + (size_t)rf[s] * D + lane) : 0.0;
             }
             double q64[TC_FBS][M];
             route_rows_f64<M, TC_FBS, TC_FBKB, 1>(xv, D, H, p.w1, p.b1, p.w2, M, 1, p.b2, q64);
@@ -247,16 +265,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
             for (int s = 0; s < TC_FBS; ++s) {
                 if (f0 + s >= nf) break;
                 int b = route_argmax<M>(q64[s]);
-                if (p.eps > 0.0) {
-                    P4 rn = philox4x32_10(p.counter, (uint64_t)rf[s], p.seed);
-                    if (u01(rn.x[0], rn.x[1]) < p.eps) b = (int)below(rn.x[2], (uint32_t)M);
+                if (eps > 0.0) {
+                    P4 rn = philox4x32_10(ctr, (uint64_t)rf[s], p.seed);
+                    if (u01(rn.x[0], rn.x[1]) < eps) b = (int)below(rn.x[2], (uint32_t)M);
                 }
                 if (lane < M && p.q_out) {
 #pragma unroll
                     for (int m = 0; m < M; ++m)
                         if (lane == m) p.q_out[(size_t)rf[s] * M + m] = (float)q64[s][m];
                 }
-                if (lane == 0) p.a_out[rf[s]] = (uint8_t)b;
+                if (lane == 0) A[rf[s]] = (uint8_t)b;
             }
         }
     };
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
         const int row = tile * TC_TILE + tid;
 #pragma unroll
         for (int k = 0; k < DM; ++k)
-            xd[k] = (k < D && tile < ntiles && row < p.B) ? __ldg(p.x + (size_t)row * D + k) : 0.0;
+            xd[k] = (k < D && tile < ntiles && row < p.B) ? __ldg(X + (size_t)row * D + k) : 0.0;
     };
     // one pass: layer 1 for hidden units [pass * HP, pass * HP + HP) of both
     // 128-state halves (TMEM columns [0, HP) and [HP, 2 HP)); one thread issues
@@ -459,15 +477,15 @@ __global__ void __launch_bounds__(TC_THREADS, 2) route_tc_kernel(const RouteTcPa
                     ++n_fb;
                     flist[atomicAdd(fcount, 1)] = row;
                 } else {
-                    if (p.eps > 0.0) {
-                        P4 rn = philox4x32_10(p.counter, (uint64_t)row, p.seed);
-                        if (u01(rn.x[0], rn.x[1]) < p.eps) best = (int)below(rn.x[2], (uint32_t)M);
+                    if (eps > 0.0) {
+                        P4 rn = philox4x32_10(ctr, (uint64_t)row, p.seed);
+                        if (u01(rn.x[0], rn.x[1]) < eps) best = (int)below(rn.x[2], (uint32_t)M);
                     }
                     if (p.q_out) {
 #pragma unroll
                         for (int m = 0; m < M; ++m) p.q_out[(size_t)row * M + m] = q[m];
                     }
-                    p.a_out[row] = (uint8_t)best;
+                    A[row] = (uint8_t)best;
                 }
             }
         }
@@ -502,6 +520,25 @@ bool route_tc_supported(int T, int M, int H) {
 
 size_t route_tc_workspace_bytes(int H) { return (size_t)TcLayout{H}.bytes(); }
 
+static size_t route_tc_smem(int H);
+
+template <int M>
+static void route_tc_prepare_m(int D, int H) {
+    auto kern = D <= 8 ? route_tc_kernel<M, 8> : route_tc_kernel<M, TC_K - 1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)route_tc_smem(H));
+}
+
+void route_tc_prepare(int T, int M, int H) {
+    const int D = T + M + 1;
+    switch (M) {
+        case 1: route_tc_prepare_m<1>(D, H); break;
+        case 2: route_tc_prepare_m<2>(D, H); break;
+        case 3: route_tc_prepare_m<3>(D, H); break;
+        case 4: route_tc_prepare_m<4>(D, H); break;
+        default: break;
+    }
+}
+
 static size_t route_tc_smem(int H) {
     const size_t img = ((size_t)TcLayout{H}.bytes() + 1023) & ~size_t(1023);
     const size_t need = img + 4 * sizeof(float) * TC_ROWS * TC_K + sizeof(float2) * 2 * TC_MP * TC_TILE + 2 * 8 +
@@ -510,10 +547,17 @@ static size_t route_tc_smem(int H) {
     return need > 80 * 1024 ? need : 80 * 1024;
 }
 
+struct TcDevIter {
+    const int64_t* iter_dev;
+    double eps_start, eps_end;
+    int64_t eps_decay;
+    int32_t pending_P;
+};
+
 template <int M>
 static int launch_route_tc_m(const be_qweights* W, int T, const double* x, int B, double eps, uint64_t seed,
                              uint64_t counter, float* q_out, uint8_t* a_out, void* workspace,
-                             unsigned long long* stats, cudaStream_t st) {
+                             unsigned long long* stats, cudaStream_t st, const TcDevIter* dv = nullptr) {
     const int D = T + M + 1, H = W->hidden;
     float* img = reinterpret_cast<float*>(workspace);
     route_tc_pack_kernel<M><<<8, 256, 0, st>>>(W->w1, W->b1, W->w2, W->b2, D, H, img);
@@ -537,10 +581,19 @@ static int launch_route_tc_m(const be_qweights* W, int T, const double* x, int B
     p.q_out = q_out;
     p.a_out = a_out;
     p.stats = stats;
+    if (dv) {
+        p.iter_dev = dv->iter_dev;
+        p.eps_start = dv->eps_start;
+        p.eps_end = dv->eps_end;
+        p.eps_decay = dv->eps_decay;
+        p.pending_P = dv->pending_P;
+    }
     const size_t smem = route_tc_smem(H);
     auto kern = D <= 8 ? route_tc_kernel<M, 8> : route_tc_kernel<M, TC_K - 1>;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return set_cuda_error(e, "route_tc smem attribute");
+    if (!dv) {  // the device-iteration form is configured at learner creation (graph capture)
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return set_cuda_error(e, "route_tc smem attribute");
+    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -560,6 +613,20 @@ int launch_route_tc(const be_qweights* W, int T, int M, const double* x, int B, 
         case 2: return launch_route_tc_m<2>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
         case 3: return launch_route_tc_m<3>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
         case 4: return launch_route_tc_m<4>(W, T, x, B, eps, seed, counter, q_out, a_out, workspace, s, st);
+        default: return set_error(BE_EINVAL, "route_tc: n_tiers must be <= 4");
+    }
+}
+
+int launch_route_tc_dev(const be_qweights* W, int T, int M, const double* x_base, int B, uint64_t seed,
+                        const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
+                        int32_t pending_P, uint8_t* a_base, void* workspace, int64_t* stats, cudaStream_t st) {
+    const TcDevIter dv{iter_dev, eps_start, eps_end, eps_decay, pending_P};
+    auto* s = reinterpret_cast<unsigned long long*>(stats);
+    switch (M) {
+        case 1: return launch_route_tc_m<1>(W, T, x_base, B, 0.0, seed, 0, nullptr, a_base, workspace, s, st, &dv);
+        case 2: return launch_route_tc_m<2>(W, T, x_base, B, 0.0, seed, 0, nullptr, a_base, workspace, s, st, &dv);
+        case 3: return launch_route_tc_m<3>(W, T, x_base, B, 0.0, seed, 0, nullptr, a_base, workspace, s, st, &dv);
+        case 4: return launch_route_tc_m<4>(W, T, x_base, B, 0.0, seed, 0, nullptr, a_base, workspace, s, st, &dv);
         default: return set_error(BE_EINVAL, "route_tc: n_tiers must be <= 4");
     }
 }

@@ -74,6 +74,9 @@ struct StepParams {
     double* x_out;
     int32_t* status;
     int32_t drain;
+    // split step (a router between): 1 = observe (advance, estimator, observe, encode
+    // into x_out; no decision, no submit), 2 = submit the decision read from action_out
+    int32_t phase;
     int32_t new_segment;      // drain + reset replicas and estimator (be_env_new_segment)
     const uint8_t* seg_mask;  // drain / new_segment: only envs with mask[e] != 0 (NULL = all)
     const double* skip;  // skip table (global), NULL = skipping off
@@ -85,13 +88,6 @@ struct StepParams {
     int32_t pending_P;
     const double* qpack;  // packed fp64 weights (QLayout) in global memory, read through L1
 };
-
-// TrainConfig.epsilon_at (trainer.py:85-90), same IEEE operations as the host
-__device__ __forceinline__ double epsilon_at(int64_t it, double start, double end, int64_t decay) {
-    if (decay <= 0) return end;
-    const double frac = fmin(1.0, __ddiv_rn((double)it, (double)decay));
-    return __dadd_rn(start, __dmul_rn(__dsub_rn(end, start), frac));
-}
 
 template <int M, int LPE>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
@@ -106,7 +102,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     const int T = p.cfg.n_tasks;
     const int H = p.H, D = T + M + 1;
-    const bool policy = !p.drain && p.forced == nullptr && p.static_tier < 0;
+    const bool policy = !p.drain && p.phase == 0 && p.forced == nullptr && p.static_tier < 0;
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     __syncthreads();
     // persistent grid (one wave): the weights are staged once per CTA, then every
@@ -158,6 +154,30 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         if (sel && !all_ok && gl == 0 && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
         return;
     }
+    if (p.phase == 2) {
+        // submit (simcore.py:94-111) of the decision the router left in action_out
+        const double U2 = p.arrival[e];
+        const int task2 = live ? p.task[e] : 0;
+        const int64_t id2 = es->next_id;
+        const uint8_t* act = p.action_out;
+        if (p.iter_dev) act += (size_t)(*p.iter_dev % p.pending_P) * (size_t)p.E;
+        const int tier2 = live ? (int)act[e] : 0;
+        const unsigned key2 = (al && tc.tier == tier2) ? (((unsigned)r.count << 5) | (unsigned)gl) : 0xffffffffu;
+        const unsigned best2 = group_min<LPE>(key2, grp);
+        const bool bad2 = best2 == 0xffffffffu || task2 >= T;
+        if (live && !bad2 && (int)(best2 & 31u) == gl) {
+            const uint32_t rid = (uint32_t)(id2 % p.rec_ld);
+            p.rec.flags[(int64_t)e * p.rec_ld + rid] = 0;  // record slot now "in flight"
+            ok &= submit_lane(r, tc, U2, rid | ((uint32_t)task2 << 24), ring, mask);
+        }
+        if (al) reps_of(p.state, e, p.R)[gl] = r;
+        if (live && gl == 0) es->next_id = id2 + 1;
+        const bool all_ok2 = (__ballot_sync(FULL, !ok) & gmask) == 0;
+        if (live && gl == 0 && (bad2 || !all_ok2)) {
+            if (atomicCAS(&p.status[0], 0, bad2 ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
+        }
+        return;
+    }
     const double U = p.arrival[e];
     int task = live ? p.task[e] : 0;
     const bool bad_task = live && task >= T;  // encode raises (policy.py:57-58)
@@ -180,9 +200,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         q[m] = 0.0;
     }
     const double xr = __ddiv_rn(rate, p.cfg.rate_scale);
-    int tier;
+    int tier = 0;
     bool explore = false;
-    if (p.forced) {
+    if (p.phase == 1) {
+        // observe only: the decision comes from a separate router launch
+    } else if (p.forced) {
         tier = p.forced[e];
     } else if (p.static_tier >= 0) {
         tier = p.static_tier;
@@ -232,9 +254,9 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         x_out[(size_t)e * D + gl] = v;
     }
     unsigned key = (al && tc.tier == tier) ? (((unsigned)r.count << 5) | (unsigned)gl) : 0xffffffffu;
-    unsigned best = group_min<LPE>(key, grp);
+    unsigned best = p.phase == 1 ? 0u : group_min<LPE>(key, grp);
     bool bad = best == 0xffffffffu;
-    if (live && !bad && (int)(best & 31u) == gl) {
+    if (p.phase == 0 && live && !bad && (int)(best & 31u) == gl) {
         uint32_t rid = (uint32_t)(id % p.rec_ld);
         p.rec.flags[(int64_t)e * p.rec_ld + rid] = 0;  // record slot now "in flight"
         ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
@@ -242,11 +264,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     if (al) reps_of(p.state, e, p.R)[gl] = r;
     if (live && gl == 0) {
         if (p.rate_out) p.rate_out[e] = rate;
-        if (action_out) action_out[e] = (uint8_t)tier;
+        if (action_out && p.phase == 0) action_out[e] = (uint8_t)tier;
 #pragma unroll
         for (int k = 0; k < 5; ++k) es->w[k] = est.w[k];
         es->n = est.n;
-        es->next_id = id + 1;
+        if (p.phase == 0) es->next_id = id + 1;
     }
     const bool all_ok = (__ballot_sync(FULL, !ok) & gmask) == 0;
     if (live && gl == 0 && (bad || bad_task || !all_ok)) {
@@ -371,12 +393,28 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
     return dispatch_step(p, step_smem_bytes(), st);
 }
 
+int launch_env_step_split(be_env* env, int phase, const double* arrival, const uint8_t* task,
+                          const double* true_rate, uint8_t* action, double* x_out, int32_t* obs_out,
+                          double* rate_out, int64_t rec_ld, const be_records* rec, cudaStream_t st) {
+    StepParams p = base_params(env, rec_ld, rec);
+    p.phase = phase;
+    p.arrival = arrival;
+    p.task = task;
+    p.true_rate = true_rate;
+    p.action_out = action;
+    p.x_out = x_out;
+    p.obs_out = obs_out;
+    p.rate_out = rate_out;
+    return dispatch_step(p, step_smem_bytes(), st);
+}
+
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st, const WorkloadArgs* wl) {
+                        double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase) {
     StepParams p = base_params(env, rec_ld, rec);
+    p.phase = phase;
     p.arrival = arrival;
     p.task = task;
     p.true_rate = true_rate;
@@ -393,7 +431,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     p.b1 = W->b1;
     p.w2 = W->w2;
     p.b2 = W->b2;
-    p.qpack = env->d_qpack;
+    p.qpack = phase == 2 ? nullptr : env->d_qpack;  // submit: no weights needed
     return dispatch_step(p, step_smem_bytes(), st, wl);
 }
 

@@ -187,6 +187,37 @@ class EnvBatch:
             _lib.ptr(out.get("q")), _lib.ptr(out.get("x")), _lib.stream_ptr(stream)))
         return out
 
+    def observe(self, arrival: torch.Tensor, task: torch.Tensor, records: "StepRecords", *,
+                true_rate: Optional[torch.Tensor] = None, stream=None) -> dict:
+        """First half of a step split around a router (be_env_step_observe): advance,
+        score completions, estimator, observe, encode.  Returns x [E, D] f64,
+        obs [E, M] i32, rate [E] f64 (device); no decision is made."""
+        E, M, dev = self.n_envs, self.n_tiers, self.device
+        _check_vec(arrival, "arrival", torch.float64, E, dev)
+        _check_vec(task, "task", torch.uint8, E, dev)
+        if true_rate is not None:
+            _check_vec(true_rate, "true_rate", torch.float64, E, dev)
+        out = dict(x=torch.empty((E, self.n_tasks + M + 1), dtype=torch.float64, device=dev),
+                   obs=torch.empty((E, M), dtype=torch.int32, device=dev),
+                   rate=torch.empty(E, dtype=torch.float64, device=dev))
+        rec = records.struct()
+        _lib.check(self._L.be_env_step_observe(
+            self._h, arrival.data_ptr(), task.data_ptr(), _lib.ptr(true_rate), records.ld, ctypes.byref(rec),
+            out["x"].data_ptr(), out["obs"].data_ptr(), out["rate"].data_ptr(), _lib.stream_ptr(stream)))
+        return out
+
+    def submit(self, arrival: torch.Tensor, task: torch.Tensor, action: torch.Tensor,
+               records: "StepRecords", stream=None) -> None:
+        """Second half (be_env_step_submit): submit every env's request to the tier
+        in `action` (u8 [E], e.g. from TensorCoreRouter on observe()'s x)."""
+        E, dev = self.n_envs, self.device
+        _check_vec(arrival, "arrival", torch.float64, E, dev)
+        _check_vec(task, "task", torch.uint8, E, dev)
+        _check_vec(action, "action", torch.uint8, E, dev)
+        rec = records.struct()
+        _lib.check(self._L.be_env_step_submit(self._h, arrival.data_ptr(), task.data_ptr(), action.data_ptr(),
+                                              records.ld, ctypes.byref(rec), _lib.stream_ptr(stream)))
+
     def drain(self, records: "StepRecords", stream=None) -> None:
         rec = records.struct()
         _lib.check(self._L.be_env_drain(self._h, records.ld, ctypes.byref(rec),

@@ -268,7 +268,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
                  completion_log=None, *, n_envs: int = 1, updates_per_step: int = 1,
                  pending_capacity: Optional[int] = None, ring_capacity: int = 1024, device=None,
                  world=None, mode: str = "device", graph_chunk: int = 0,
-                 timing: Optional[dict] = None, exchange: str = "nccl") -> TrainResult:
+                 timing: Optional[dict] = None, exchange: str = "nccl",
+                 router: str = "fp64") -> TrainResult:
     """trainer.py:333-406 on the GPU for `n_envs` lockstep environments.
 
     Every iteration: TrainingWorkload arrivals (Philox), one env step with
@@ -293,6 +294,12 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     update kernel per rank exchanges the gradients through the ranks' exchange
     buffers in peer memory (CUDA IPC handles swapped once over `world`), no
     collective on the update path, graph-capturable (be_train_iteration phase 4).
+    `router`: "fp64" — the decision is made inside the env step (fp64 Q);
+    "tc" — the step is split around the tensor-core router: observe + encode, then
+    be_qnet_route_tc's certified tcgen05 forward (fp64 re-evaluation of the states it
+    cannot certify) on the E states, then submit — the same decisions and exploration
+    draws, so the same training run bit for bit (test); it pays off for large
+    lockstep batches.
     `timing`: optional dict, receives the device time of the iteration loop
     ("loop_ms", CUDA events on the launching stream; setup and the one-time graph
     capture excluded, intermediate log rows included, the final one excluded)."""
@@ -309,6 +316,8 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
         mode = "host"
     if exchange not in ("nccl", "peer"):
         raise ValueError("exchange must be 'nccl' or 'peer'")
+    if router not in ("fp64", "tc"):
+        raise ValueError("router must be 'fp64' or 'tc'")
     if encoding is None:
         encoding = StateEncoding(n_tasks=n_tasks, batch_scales=tuple(float(t.max_batch) for t in tiers))
     dev = _lib.require_cuda(device)
@@ -372,13 +381,14 @@ def run_training(tiers, reward_spec, cfg: TrainConfig, encoding=None, init_net=N
     t_begin.record()
     if mode == "host":
         _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
-                       log_every, log_row, completion_log)
+                       log_every, log_row, completion_log, router)
     else:
         tic = _lib.BeTrainIterCfg()
         tic.workload_seed, tic.policy_seed, tic.sample_seed = wl_seed, pol_seed, smp_seed
         tic.epsilon_start, tic.epsilon_end = float(cfg.epsilon_start), float(cfg.epsilon_end)
         tic.epsilon_decay_steps = int(cfg.epsilon_decay_fraction * total)
         tic.updates_per_step = int(updates_per_step)
+        tic.router = 1 if router == "tc" else 0
         min_size = max(int(cfg.batch_size), int(cfg.warmup))
         gate_b = torch.empty(1, dtype=torch.bool, device=dev)
 
@@ -470,7 +480,7 @@ def default_pending_capacity(n_envs: int, input_dim: int, budget_bytes: float = 
 
 
 def _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_seed, smp_seed,
-                   log_every, log_row, completion_log=None):
+                   log_every, log_row, completion_log=None, router="fp64"):
     """The reference loop's structure (trainer.py:374-404), one C-ABI call per stage.
 
     completion_log (trainer.py:381-383): (request id, task, tier, realized ms/token,
@@ -487,11 +497,20 @@ def _run_host_loop(learner, env, cfg, E, updates_per_step, world, wl_seed, pol_s
     task = torch.empty(E, dtype=torch.uint8, device=dev)
     rate = torch.empty(E, dtype=torch.float64, device=dev)
     W = learner.online_weights()
+    tc_ws = None
+    if router == "tc":
+        L = learner._L
+        tc_ws = torch.empty((int(L.be_qnet_route_tc_workspace_bytes(cfg.hidden)) + 15) // 16 * 4,
+                            dtype=torch.float32, device=dev)
     for it in range(cfg.total_iterations):
         learner.workload(wl_seed, it, arrival, task, rate)
         slot = it % P
-        _env_step(env, arrival, task, rate, W, cfg.epsilon_at(it), pol_seed, it, rec,
-                  learner.pending_x[slot], learner.pending_action[slot])
+        if router == "tc":
+            _env_step_tc(env, learner, arrival, task, rate, W, cfg.epsilon_at(it), pol_seed, it, rec,
+                         learner.pending_x[slot], learner.pending_action[slot], tc_ws)
+        else:
+            _env_step(env, arrival, task, rate, W, cfg.epsilon_at(it), pol_seed, it, rec,
+                      learner.pending_x[slot], learner.pending_action[slot])
         learner.commit(it)
         for u in range(updates_per_step):
             learner.backward(smp_seed, it * updates_per_step + u)
@@ -569,6 +588,21 @@ def _env_step(env: EnvBatch, arrival, task, rate, W, epsilon, seed, counter, rec
                                   None, ctypes.byref(W), -1, float(epsilon), seed & (2**64 - 1),
                                   counter & (2**64 - 1), rec.ld, ctypes.byref(r), None, None,
                                   a_out.data_ptr(), None, x_out.data_ptr(), _lib.stream_ptr()))
+
+
+def _env_step_tc(env: EnvBatch, learner, arrival, task, rate, W, epsilon, seed, counter, rec, x_out, a_out,
+                 workspace):
+    """The split step of router="tc": observe + encode into the pending slot, the
+    tensor-core router on it (same epsilon / Philox draws as the fused step), submit."""
+    L = env._L
+    r = rec.struct()
+    _lib.check(L.be_env_step_observe(env.handle, arrival.data_ptr(), task.data_ptr(), rate.data_ptr(), rec.ld,
+                                     ctypes.byref(r), x_out.data_ptr(), None, None, _lib.stream_ptr()))
+    _lib.check(L.be_qnet_route_tc(ctypes.byref(W), learner.n_tasks, learner.n_tiers, x_out.data_ptr(),
+                                  env.n_envs, float(epsilon), seed & (2**64 - 1), counter & (2**64 - 1), None,
+                                  a_out.data_ptr(), workspace.data_ptr(), None, _lib.stream_ptr()))
+    _lib.check(L.be_env_step_submit(env.handle, arrival.data_ptr(), task.data_ptr(), a_out.data_ptr(), rec.ld,
+                                    ctypes.byref(r), _lib.stream_ptr()))
 
 
 def fine_tune(net, reward_spec, cfg: TrainConfig, tiers, encoding=None, completion_log=None, **kw):
