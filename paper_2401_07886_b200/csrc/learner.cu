@@ -803,6 +803,7 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         }
         cudaMemset(L->tc_stats, 0, 16);
         route_tc_prepare(c->n_tasks, c->n_tiers, c->hidden);
+        step_tc_prepare(c->n_tiers, c->hidden);
     }
     // configured here, not at launch time: launches may be captured in a CUDA graph
     cudaFuncSetAttribute(learner_partial_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1160,9 +1161,17 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         be_records rec{};
         rec.flags = L->pflags;
         rec.reward = L->preward;
-        if (c->router == BE_ROUTER_TC) {
-            // observe + encode (pending slot) -> certified tcgen05 router on the E states
-            // (epsilon and Philox counter from the device iteration index) -> submit
+        if (c->router == BE_ROUTER_TC && env->R <= 16) {
+            // the decision on the tensor cores inside the env step: prep_kernel also packs
+            // the router image; env_step_tc_kernel runs layer 1 of 16 envs per CTA as one
+            // tcgen05 tile (certified, fp64 fallback: the fp64 step's decisions)
+            rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                     c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,
+                                     reinterpret_cast<float*>(L->tc_img));
+        } else if (c->router == BE_ROUTER_TC) {
+            // > 16 replicas per env: observe + encode (pending slot) -> the batched
+            // tcgen05 router on the E states -> submit
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 1);

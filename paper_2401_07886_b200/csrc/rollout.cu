@@ -30,7 +30,7 @@
 // skip table; the true-rate variant runs 3 CTAs/SM and reads it through L1 when the
 // batch fills them (config 4), else 2 CTAs/SM (config 1: 18 envs, latency-bound).
 #ifndef BE_TRACE_EVICT_FIRST
-#define BE_TRACE_EVICT_FIRST 0
+#define BE_TRACE_EVICT_FIRST 1
 #endif
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
     uint64_t pol;

@@ -9,6 +9,7 @@
 #include "be_env.cuh"
 #include "be_internal.h"
 #include "be_philox.cuh"
+#include "be_route_tc.cuh"
 #include "be_workload.cuh"
 
 namespace be {
@@ -87,11 +88,28 @@ struct StepParams {
     int64_t eps_decay;
     int32_t pending_P;
     const double* qpack;  // packed fp64 weights (QLayout) in global memory, read through L1
+    // decision on the tensor cores (env_step_tc_kernel): the router's packed image
+    // (TcLayout, rebuilt by prep_kernel every iteration) and the TMEM columns to allocate
+    const float* tc_img;
+    int32_t tc_ncols;
 };
 
-template <int M, int LPE>
+// Per-CTA tensor-core decision context of env_step_tc_kernel (shared memory + TMEM).
+struct TcStepCtx {
+    const float* img;  // TcLayout image in shared memory
+    float* Ah;         // A operand, tf32 hi: [128 rows][TC_K] UMMA K-major (rows >= 16 stay 0)
+    float* Al;         // tf32 lo
+    float2* part;      // [2 column halves][16 rows][2 sets][TC_MP] layer-2 partial sums
+    uint64_t* bar;     // MMA completion
+    uint64_t* img_bar; // the image's bulk copy (waited for once, before the first MMA)
+    uint32_t tmem;
+    uint32_t phase;
+    bool img_ready;
+};
+
+template <int M, int LPE, bool TCQ = false>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
-                                         bool policy, int T, int H, int D);
+                                         bool policy, int T, int H, int D, TcStepCtx* tcx = nullptr);
 
 // LPE lanes per env: 16 (two envs per warp) when the cluster has <= 16 replicas and
 // the encoded state fits 16 lanes, else 32
@@ -117,11 +135,272 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     pdl_trigger();  // this CTA is done: the next kernel may start filling the SM
 }
 
+// The greedy decision of one env on the tensor cores, inside the env step (every
+// thread of the CTA calls it once per round: two CTA barriers).  Layer 1 of the 16
+// envs of the CTA as one tcgen05.mma.kind::tf32 tile (3xTF32 split, M = 128 rows of
+// which 16 are envs, N = H, accumulators in TMEM); relu + layer 2 by warps 0 and 4
+// (TMEM lanes 0-31) on FFMA2 with the same summation structure as route_tc, so the
+// router's pairwise error bounds certify the leader; a decision the bound cannot
+// certify is re-evaluated by the group in fp64 (qnet_group, the fused step's own
+// arithmetic).  Returns the greedy tier (identical to the fp64 step's).
+template <int M>
+__device__ __forceinline__ int tc_decide(TcStepCtx& cx, bool live, bool explore, int task, const double (&xt)[M],
+                                         double xr, const double* sw, int T, int H, int D, int le, int gl) {
+    const TcLayout L{H};
+    const float* B1h = cx.img + L.b1h() / 4;
+    const float* B1l = cx.img + L.b1l() / 4;
+    const float4* W2q = reinterpret_cast<const float4*>(cx.img + L.w2p() / 4);
+    const float* fb2 = cx.img + L.b2() / 4;
+    const float* C = cx.img + L.bound() / 4;
+    const float* Dp = cx.img + L.pairs() / 4;
+    // ---- A row le: input gl (fp32-rounded, then tf32 hi + lo), the bias input = 1
+    float xk = 0.f;
+    if (gl < T) xk = gl == task ? 1.f : 0.f;
+#pragma unroll
+    for (int m = 0; m < M; ++m)
+        if (gl == T + m) xk = __double2float_rn(xt[m]);
+    if (gl == T + M) xk = __double2float_rn(xr);
+    if (gl == D) xk = 1.f;
+    if (!live) xk = 0.f;
+    if (gl < TC_K) {
+        const float hi = tc::to_tf32(xk);
+        cx.Ah[umma_off(le, gl)] = hi;
+        cx.Al[umma_off(le, gl)] = tc::to_tf32(__fsub_rn(xk, hi));
+    }
+    tc::fence_proxy_async_smem();
+    if (!cx.img_ready) {  // issued at kernel start: the copy overlapped the first round's advance
+        tc::mbar_wait(cx.img_bar, 0);
+        cx.img_ready = true;
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        tc::fence_after_sync();
+        const uint32_t idesc = tc::idesc_tf32(128, H);
+#pragma unroll
+        for (int s = 0; s < TC_K / 8; ++s) {  // K-step s reads K-groups 2s, 2s + 1
+            const uint64_t ah = tc::smem_desc(cx.Ah + s * 64, 128, 512), al = tc::smem_desc(cx.Al + s * 64, 128, 512);
+            const uint64_t bh = tc::smem_desc(B1h + s * 64, 128, 512), bl = tc::smem_desc(B1l + s * 64, 128, 512);
+            tc::mma_tf32(cx.tmem, ah, bh, idesc, s > 0);
+            tc::mma_tf32(cx.tmem, ah, bl, idesc, true);
+            tc::mma_tf32(cx.tmem, al, bh, idesc, true);
+        }
+        tc::mma_commit(cx.bar);
+    }
+    tc::mbar_wait(cx.bar, cx.phase);
+    cx.phase ^= 1u;
+    tc::fence_after_sync();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if ((warp & 3) == 0) {  // warps 0 and 4: TMEM lanes 0-31 = rows 0-31 (rows 0-15 are envs)
+        const int half = warp >> 2, HP = H / 2;
+        float2 a[2][M];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+            for (int m = 0; m < M; ++m) a[s2][m] = make_float2(0.f, 0.f);
+        const int nch = HP / TC_CW;
+        auto consume = [&](const float(&u)[TC_CW], int jb) {
+#pragma unroll
+            for (int i = 0; i < TC_CW / 2; i += 2) {
+                const float2 h0 = make_float2(fmaxf(u[2 * i], 0.f), fmaxf(u[2 * i + 1], 0.f));
+                const float2 h1 = make_float2(fmaxf(u[2 * i + 2], 0.f), fmaxf(u[2 * i + 3], 0.f));
+                const float4* g = W2q + (size_t)((jb + 2 * i) >> 2) * 4;
+                const float4 g0 = g[0], g1 = g[1];
+                a[0][0] = ffma2(h0, make_float2(g0.x, g0.y), a[0][0]);
+                a[1][0] = ffma2(h1, make_float2(g1.x, g1.y), a[1][0]);
+                if (M > 1) {
+                    constexpr int m1 = M > 1 ? 1 : 0;
+                    a[0][m1] = ffma2(h0, make_float2(g0.z, g0.w), a[0][m1]);
+                    a[1][m1] = ffma2(h1, make_float2(g1.z, g1.w), a[1][m1]);
+                }
+                if (M > 2) {
+                    constexpr int m2 = M > 2 ? 2 : 0;
+                    const float4 g2 = g[2];
+                    a[0][m2] = ffma2(h0, make_float2(g2.x, g2.y), a[0][m2]);
+                    a[1][m2] = ffma2(h1, make_float2(g2.z, g2.w), a[1][m2]);
+                }
+                if (M > 3) {
+                    constexpr int m3 = M > 3 ? 3 : 0;
+                    const float4 g3 = g[3];
+                    a[0][m3] = ffma2(h0, make_float2(g3.x, g3.y), a[0][m3]);
+                    a[1][m3] = ffma2(h1, make_float2(g3.z, g3.w), a[1][m3]);
+                }
+            }
+        };
+        // double-buffered TMEM loads (two named buffers: no local-memory indexing)
+        float u0[TC_CW], u1[TC_CW];
+        const uint32_t col0 = cx.tmem + (uint32_t)(half * HP);
+        tc::tmem_ld_issue(col0, u0);
+        for (int c = 0; c < nch; c += 2) {
+            tc::tmem_ld_wait(u0);
+            if (c + 1 < nch) tc::tmem_ld_issue(col0 + (uint32_t)((c + 1) * TC_CW), u1);
+            consume(u0, half * HP + c * TC_CW);
+            if (c + 1 < nch) {
+                tc::tmem_ld_wait(u1);
+                if (c + 2 < nch) tc::tmem_ld_issue(col0 + (uint32_t)((c + 2) * TC_CW), u0);
+                consume(u1, half * HP + (c + 1) * TC_CW);
+            }
+        }
+        if (lane < 16) {
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+                for (int m = 0; m < M; ++m) cx.part[((half * 16 + lane) * 2 + s2) * TC_MP + m] = a[s2][m];
+        }
+    }
+    tc::fence_before_sync();  // this round's TMEM loads complete before the next round's MMA
+    __syncthreads();
+    // ---- q (fp32) of row le: the two column halves merged as route_tc merges them
+    float q[M];
+    int best = 0;
+    float bv = 0.f;
+    bool fin = true;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        float2 t[2];
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const float2 own = cx.part[((0 * 16 + le) * 2 + s2) * TC_MP + m];
+            const float2 oth = cx.part[((1 * 16 + le) * 2 + s2) * TC_MP + m];
+            t[s2] = make_float2(__fadd_rn(own.x, oth.x), __fadd_rn(own.y, oth.y));
+        }
+        const float t0 = __fadd_rn(t[0].x, t[0].y), t1 = __fadd_rn(t[1].x, t[1].y);
+        q[m] = __fadd_rn(__fadd_rn(t0, t1), fb2[m]);
+        fin = fin && isfinite(q[m]);
+        if (m == 0 || q[m] > bv) {  // first maximum (a tie is never certified)
+            best = m;
+            bv = q[m];
+        }
+    }
+    // ---- certification: the leader beats every other action by more than the pair's bound
+    float xf[TC_K];
+#pragma unroll
+    for (int k = 0; k < TC_K; ++k) xf[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < TC_K; ++k) {
+        if (k < T) xf[k] = k == task ? 1.f : 0.f;
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+            if (k == T + m) xf[k] = __double2float_rn(xt[m]);
+        if (k == T + M) xf[k] = __double2float_rn(xr);
+    }
+    float Bd = C[D];
+#pragma unroll
+    for (int k = 0; k < TC_K; ++k)
+        if (k < D) Bd = __fmaf_ru(fabsf(xf[k]), C[k], Bd);
+    bool sure = fin;
+#pragma unroll
+    for (int b = 0; b < M; ++b)
+#pragma unroll
+        for (int sx = b + 1; sx < M; ++sx) {
+            if (best == b || best == sx) {
+                const float* dp = Dp + tc_pair(b, sx) * TC_K;
+                float v = dp[D];
+#pragma unroll
+                for (int k = 0; k < TC_K; ++k)
+                    if (k < D) v = __fmaf_ru(fabsf(xf[k]), dp[k], v);
+                const float Bp = __fadd_ru(v, Bd);
+                const float other = best == b ? q[sx] : q[b];
+                sure = sure && isfinite(Bp) && __dsub_rd((double)bv, (double)other) > (double)Bp;
+            }
+        }
+    sure = M == 1 || sure;
+    int tier = best;
+    // fp64 re-evaluation where the bound cannot certify (group-wide shuffles: both
+    // groups of the warp run it when either needs it)
+    if (__ballot_sync(FULL, live && !explore && !sure)) {
+        double q64[M];
+        qnet_group<M, 16>(sw, T, H, task, xt, xr, q64);
+        if (!sure) tier = argmax_first<M>(q64);
+    }
+    return tier;
+}
+
+// Shared-memory plan of env_step_tc_kernel: [Score | image | A hi | A lo | partials | barriers]
+struct TcStepSmem {
+    size_t img, ah, al, part, bars, bytes;
+    __host__ __device__ static size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+    __host__ __device__ explicit TcStepSmem(int H) {
+        img = up(sizeof(Score), 128);
+        ah = up(img + (size_t)TcLayout{H}.bytes(), 128);
+        al = ah + sizeof(float) * 128 * TC_K;
+        part = al + sizeof(float) * 128 * TC_K;
+        bars = up(part + sizeof(float2) * 2 * 16 * 2 * TC_MP, 16);
+        bytes = bars + 2 * sizeof(uint64_t) + 16;
+    }
+};
+
+// The training env step with the greedy decision on the tensor cores (be_train_iteration,
+// router = BE_ROUTER_TC).  256 threads = 16 envs (16 lanes each) per CTA round, rounds
+// CTA-uniform (every thread reaches the two MMA barriers); per CTA: one TMEM allocation
+// of H columns and one bulk copy of the packed image for all rounds.
+template <int M>
+__global__ void __launch_bounds__(256) env_step_tc_kernel(const StepParams p) {
+    pdl_wait();  // prep_kernel (weights image, workload) has completed
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    const TcStepSmem S(p.H);
+    Score& sc = *reinterpret_cast<Score*>(smem_raw);
+    TcStepCtx cx;
+    cx.img = reinterpret_cast<const float*>(smem_raw + S.img);
+    cx.Ah = reinterpret_cast<float*>(smem_raw + S.ah);
+    cx.Al = reinterpret_cast<float*>(smem_raw + S.al);
+    cx.part = reinterpret_cast<float2*>(smem_raw + S.part);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + S.bars);
+    uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bars + 2);
+    cx.bar = &bars[1];
+    cx.img_bar = &bars[0];
+    cx.phase = 0;
+    cx.img_ready = false;
+    const int T = p.cfg.n_tasks, H = p.H, D = T + M + 1;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid < 32) load_score(sc, p.cfg, p.aux);
+    for (int k = tid; k < 2 * 128 * TC_K; k += blockDim.x) cx.Ah[k] = 0.f;  // Ah, Al: rows >= 16 stay 0
+    if (tid == 0) {
+        tc::mbar_init(&bars[0], 1);
+        tc::mbar_init(&bars[1], 1);
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_sh, (uint32_t)p.tc_ncols);
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    cx.tmem = *tmem_sh;
+    if (tid == 0) {
+        const uint32_t nb = (uint32_t)TcLayout{H}.bytes();
+        tc::mbar_expect_tx(&bars[0], nb);
+        tc::bulk_g2s(const_cast<float*>(cx.img), p.tc_img, nb, &bars[0]);
+    }
+    const int grp = (tid & 31) >> 4;
+    const int per_round = 16 * gridDim.x;
+    const int rounds = (p.E + per_round - 1) / per_round;
+    for (int k = 0; k < rounds; ++k) {
+        const int e = (k * gridDim.x + blockIdx.x) * 16 + warp * 2 + grp;
+        step_env<M, 16, true>(p, e < p.E ? e : p.E - 1, e < p.E, sc, p.qpack, true, T, H, D, &cx);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(cx.tmem, (uint32_t)p.tc_ncols);
+    pdl_trigger();
+}
+
+size_t step_tc_smem_bytes(int H) { return TcStepSmem(H).bytes; }
+
+void step_tc_prepare(int M, int H) {
+    const int smem = (int)TcStepSmem(H).bytes;
+    switch (M) {
+        case 1: cudaFuncSetAttribute(env_step_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 2: cudaFuncSetAttribute(env_step_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 3: cudaFuncSetAttribute(env_step_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        case 4: cudaFuncSetAttribute(env_step_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+        default: break;
+    }
+}
+
 // One env per LPE-lane group (all 32 lanes of the warp call it: the group
 // reductions are warp-wide); `live` = false for a padding group past the last env.
-template <int M, int LPE>
+template <int M, int LPE, bool TCQ>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
-                                         bool policy, int T, int H, int D) {
+                                         bool policy, int T, int H, int D, TcStepCtx* tcx) {
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPE - 1), grp = LPE == 32 ? 0 : lane / LPE;
     const unsigned gmask = LPE == 32 ? FULL : (0xffffu << (grp * LPE));
@@ -224,8 +503,14 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
                 tier = (int)below(rnd.x[2], (uint32_t)M);
             }
         }
-        qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
-        if (!explore) tier = argmax_first<M>(q);
+        if constexpr (TCQ) {
+            const int dec = tc_decide<M>(*tcx, live, explore, task, xt, xr, sw, T, H, D,
+                                         (threadIdx.x >> 5) * 2 + grp, gl);
+            if (!explore) tier = dec;
+        } else {
+            qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
+            if (!explore) tier = argmax_first<M>(q);
+        }
     }
     if (live && gl < M) {
 #pragma unroll
@@ -286,14 +571,22 @@ int launch_env_reset(be_env* env, const uint8_t* mask, cudaStream_t st) {
 
 // Weight packing for the env step, fused with the next training arrival of every env
 // (be_train_iteration): CTAs [0, QPACK_CTAS) pack, the rest run the workload.
+// With a tensor-core image requested (tc_img), CTAs [QPACK_CTAS, + TCPACK_CTAS) pack it.
+constexpr int TCPACK_CTAS = 8;
 template <int M>
 __global__ void __launch_bounds__(256) prep_kernel(const double* w1, const double* b1, const double* w2,
-                                                   const double* b2, int T, int H, double* out, WorkloadArgs wl) {
+                                                   const double* b2, int T, int H, double* out, WorkloadArgs wl,
+                                                   float* tc_img) {
     pdl_wait();  // the weights were updated by the previous kernel
+    const int ntc = tc_img ? TCPACK_CTAS : 0;
     if (blockIdx.x < QPACK_CTAS) {
         stage_qnet<M>(w1, b1, w2, b2, T, H, out, blockIdx.x * blockDim.x + threadIdx.x, QPACK_CTAS * blockDim.x);
+    } else if ((int)blockIdx.x < QPACK_CTAS + ntc) {
+        if constexpr (M <= TC_MP)
+            tc_pack_image<M>(w1, b1, w2, b2, T + M + 1, H, tc_img,
+                             (blockIdx.x - QPACK_CTAS) * blockDim.x + threadIdx.x, TCPACK_CTAS * blockDim.x);
     } else {
-        const int e = (blockIdx.x - QPACK_CTAS) * blockDim.x + threadIdx.x;
+        const int e = (blockIdx.x - QPACK_CTAS - ntc) * blockDim.x + threadIdx.x;
         if (e < wl.E) train_workload_env(wl, e);
     }
     pdl_trigger();
@@ -303,14 +596,29 @@ template <int M>
 static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, const WorkloadArgs* wl) {
     const bool two = p.R <= 16 && p.cfg.n_tasks + M + 1 <= 16;
     auto kern = two ? env_step_kernel<M, 16> : env_step_kernel<M, 32>;
-    if (p.qpack && wl) {  // pack the weights + the training workload, one launch
-        cudaError_t e = launch_pdl(prep_kernel<M>, dim3(QPACK_CTAS + (wl->E + 255) / 256), dim3(256), 0, st, p.w1,
-                                   p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack), *wl);
+    float* tc_img = const_cast<float*>(p.tc_img);
+    if (p.qpack && wl) {  // pack the weights (+ the tensor-core image) + the training workload, one launch
+        const int ntc = tc_img ? TCPACK_CTAS : 0;
+        cudaError_t e = launch_pdl(prep_kernel<M>, dim3(QPACK_CTAS + ntc + (wl->E + 255) / 256), dim3(256), 0, st,
+                                   p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack), *wl,
+                                   tc_img);
         if (e != cudaSuccess) return set_cuda_error(e, "prep launch");
     } else if (p.qpack) {  // pack the (possibly just updated) weights for this step
         cudaError_t e = launch_pdl(stage_qpack_kernel<M>, dim3(QPACK_CTAS), dim3(256), 0, st, p.w1, p.b1, p.w2, p.b2,
                                    p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack));
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
+    }
+    if constexpr (M <= TC_MP) {
+        if (tc_img) {  // the decision on the tensor cores (attribute set by step_tc_prepare)
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            long long blocks = ((long long)p.E + 15) / 16;
+            if (blocks > 2LL * sms) blocks = 2LL * sms;  // two CTAs per SM share its TMEM
+            cudaError_t e = launch_pdl(env_step_tc_kernel<M>, dim3((unsigned)blocks), dim3(256),
+                                       step_tc_smem_bytes(p.H), st, p);
+            return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step (tensor cores) launch");
+        }
     }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -412,9 +720,11 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase) {
+                        double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase, float* tc_img) {
     StepParams p = base_params(env, rec_ld, rec);
     p.phase = phase;
+    p.tc_img = tc_img;
+    p.tc_ncols = W->hidden <= 32 ? 32 : W->hidden <= 64 ? 64 : W->hidden <= 128 ? 128 : 256;
     p.arrival = arrival;
     p.task = task;
     p.true_rate = true_rate;
