@@ -97,7 +97,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
                         double* x_base, cudaStream_t st, const struct WorkloadArgs* wl = nullptr,
-                        int phase = 0, float* tc_img = nullptr);
+                        int phase = 0, float* tc_img = nullptr, int64_t* crange = nullptr);
 // the training step with the decision on the tensor cores (tc_img != NULL above):
 // shared-memory size and the kernel attribute (set before any graph capture)
 size_t step_tc_smem_bytes(int H);

@@ -60,6 +60,10 @@ struct CommitParams {
     double* rc;              // ring continue flags [C]
     int32_t* status;
     const int64_t* step_dev;  // be_train_iteration: `step` read from device memory
+    // be_train_iteration: per env {lowest, highest id completed this step, oldest in flight}
+    // from the env step — every completion of the step is committable now, and nothing
+    // else is, so only that id range is scanned (nullable: scan from `low`)
+    const int64_t* crange;
     // single-pass commit (commit_fused_kernel): decoupled look-back scan state
     unsigned long long* scan;  // [E / 8] (epoch << 40 | flag << 38 | value)
     unsigned* ticket;          // [0] virtual CTA ticket, [1] epoch (both advanced by the last CTA)
@@ -79,14 +83,19 @@ constexpr unsigned FULL_MASK = 0xffffffffu;
 __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane, int64_t base, int64_t cursor,
                                           bool write, int64_t* window = nullptr) {
     const int64_t step = p.step_dev ? *p.step_dev : p.step;
-    const int64_t hi = step - 1;  // inclusive upper candidate
-    const int64_t lo = p.low[e];
+    int64_t hi = step - 1;  // inclusive upper candidate
+    int64_t lo = p.low[e];
+    if (p.crange) {
+        lo = p.crange[3 * (int64_t)e];
+        const int64_t chi = p.crange[3 * (int64_t)e + 1];
+        hi = chi < hi ? chi : hi;
+    }
     int total = 0;
     int64_t new_low = lo;
     bool blocked = false;
     // pending slot of j0 (= j0 mod P) and ring slot of this env's first commit, kept
     // incrementally: no 64-bit division inside the loop
-    int64_t r0 = lo % p.P;
+    int64_t r0 = lo <= hi ? lo % p.P : 0;
     const int64_t s0 = write ? (cursor + base) % p.capacity : 0;
     for (int64_t j0 = lo; j0 <= hi; j0 += 32) {
         const int64_t j = j0 + lane;
@@ -127,6 +136,7 @@ __device__ __forceinline__ int commit_env(const CommitParams& p, int e, int lane
         }
     }
     if (write && lane == 0) {
+        if (p.crange) new_low = p.crange[3 * (int64_t)e + 2];  // the oldest request still in flight
         p.low[e] = new_low;
         if (step + 1 - new_low >= p.P && atomicCAS(&p.status[0], 0, BE_ECAPACITY) == 0) p.status[1] = e;
         if (window) *window = step + 1 - new_low;
@@ -720,6 +730,7 @@ struct be_learner {
     int64_t* gate;     // DP update gate (be_train_iteration use_gate)
     // tensor-core router (be_train_iteration router = BE_ROUTER_TC): packed weight image
     // (rebuilt every iteration: the weights change with every update) and statistics
+    int64_t* crange;    // [E][3] completion id range of the step + oldest in flight (commits)
     void* tc_img;       // NULL when the network shape is outside route_tc's support
     int64_t* tc_stats;  // [2] states routed, fp64 re-evaluations
 };
@@ -729,7 +740,7 @@ static void learner_free(be_learner* L) {
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
                     L->preward, L->low, L->status, L->wl_state,
                     L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket,
-                    L->tc_img, L->tc_stats};
+                    L->tc_img, L->tc_stats, L->crange};
     for (void* p : ptrs) cudaFree(p);
     for (int r = 0; r < XMAX_RANKS; ++r)
         if (L->x_opened[r]) cudaIpcCloseMemHandle(L->x_opened[r]);
@@ -780,7 +791,8 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->status, 64},
         {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
         {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64},
-        {(void**)&L->scan, ((E + CENVS - 1) / CENVS) * 8}, {(void**)&L->ticket, 64}};
+        {(void**)&L->scan, ((E + CENVS - 1) / CENVS) * 8}, {(void**)&L->ticket, 64},
+        {(void**)&L->crange, E * 3 * 8}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -893,9 +905,11 @@ int32_t be_learner_workload(be_learner* L, uint64_t seed, int64_t step, double* 
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "workload launch");
 }
 
-static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cudaStream_t st) {
+static int commit_impl(be_learner* L, int64_t step, const int64_t* step_dev, cudaStream_t st,
+                       const int64_t* crange = nullptr) {
     CommitParams p{};
     p.step_dev = step_dev;
+    p.crange = crange;
     p.E = L->cfg.n_envs;
     p.D = L->D;
     p.P = L->cfg.pending_capacity;
@@ -1168,13 +1182,14 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,
-                                     reinterpret_cast<float*>(L->tc_img));
+                                     reinterpret_cast<float*>(L->tc_img), L->crange);
         } else if (c->router == BE_ROUTER_TC) {
             // > 16 replicas per env: observe + encode (pending slot) -> the batched
             // tcgen05 router on the E states -> submit
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
-                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 1);
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 1,
+                                     nullptr, L->crange);
             if (rc) return rc;
             rc = launch_route_tc_dev(&W, cf.n_tasks, M, L->px, E, c->policy_seed, it, c->epsilon_start,
                                      c->epsilon_end, c->epsilon_decay_steps, cf.pending_capacity, L->pa,
@@ -1182,14 +1197,16 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
             if (rc) return rc;
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
-                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2);
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2,
+                                     nullptr, L->crange);
         } else {
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
-                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl);
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,
+                                     nullptr, L->crange);
         }
         if (rc) return rc;
-        rc = commit_impl(L, 0, it, st);
+        rc = commit_impl(L, 0, it, st, L->crange);
         if (rc) return rc;
     }
     const int ups = c->updates_per_step;

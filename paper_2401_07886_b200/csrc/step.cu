@@ -92,7 +92,35 @@ struct StepParams {
     // (TcLayout, rebuilt by prep_kernel every iteration) and the TMEM columns to allocate
     const float* tc_img;
     int32_t tc_ncols;
+    // training commits (be_train_iteration): per env {lowest, highest request id completed
+    // in this step's advance, oldest request still in flight after the submit} (nullable)
+    int64_t* crange;
 };
+
+// request id of pending slot s (= id mod P) among the ids <= t
+__device__ __forceinline__ int64_t id_of_slot(int64_t t, uint32_t s, int32_t P) {
+    int64_t d = t % P - (int64_t)s;
+    if (d < 0) d += P;
+    return t - d;
+}
+template <int LPE>
+__device__ __forceinline__ int64_t group_min64(int64_t v) {
+#pragma unroll
+    for (int off = LPE / 2; off > 0; off >>= 1) {
+        const int64_t o = __shfl_xor_sync(FULL, v, off);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+template <int LPE>
+__device__ __forceinline__ int64_t group_max64(int64_t v) {
+#pragma unroll
+    for (int off = LPE / 2; off > 0; off >>= 1) {
+        const int64_t o = __shfl_xor_sync(FULL, v, off);
+        v = o > v ? o : v;
+    }
+    return v;
+}
 
 // Per-CTA tensor-core decision context of env_step_tc_kernel (shared memory + TMEM).
 struct TcStepCtx {
@@ -451,6 +479,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         }
         if (al) reps_of(p.state, e, p.R)[gl] = r;
         if (live && gl == 0) es->next_id = id2 + 1;
+        if (p.crange) {  // oldest request in flight (FIFO heads), for the commit's overflow check
+            const int64_t oh = group_min64<LPE>((al && r.count > 0) ? id_of_slot(id2, r.h_idtask & 0xffffffu, p.pending_P)
+                                                                   : INT64_MAX);
+            if (live && gl == 0) p.crange[3 * (int64_t)e + 2] = oh;
+        }
         const bool all_ok2 = (__ballot_sync(FULL, !ok) & gmask) == 0;
         if (live && gl == 0 && (bad2 || !all_ok2)) {
             if (atomicCAS(&p.status[0], 0, bad2 ? BE_EINVAL : BE_ECAPACITY) == 0) p.status[1] = e;
@@ -461,7 +494,30 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     int task = live ? p.task[e] : 0;
     const bool bad_task = live && task >= T;  // encode raises (policy.py:57-58)
     if (task >= T) task = 0;
+    const uint32_t cr_h0 = r.head, cr_idt0 = r.h_idtask;
+    const int cr_c0 = r.count;
     if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out);
+    if (p.crange) {
+        // the requests this advance completed are the popped FIFO prefix of every replica
+        // (ids increase along a FIFO): the env's lowest / highest completed id of this
+        // step bound the commit scan (be_train_iteration), instead of the whole window of
+        // unresolved decisions
+        const int popped = al ? cr_c0 - r.count : 0;
+        const int64_t t1 = es->next_id - 1;
+        int64_t jlo = INT64_MAX, jhi = -1;
+        if (popped > 0) {
+            const uint32_t s_first = cr_idt0 & 0xffffffu;
+            const uint32_t s_last = popped == 1 ? s_first : ring[(cr_h0 + popped - 1) & mask].idtask & 0xffffffu;
+            jlo = id_of_slot(t1, s_first, p.pending_P);
+            jhi = id_of_slot(t1, s_last, p.pending_P);
+        }
+        jlo = group_min64<LPE>(jlo);
+        jhi = group_max64<LPE>(jhi);
+        if (live && gl == 0) {
+            p.crange[3 * (int64_t)e] = jlo;
+            p.crange[3 * (int64_t)e + 1] = jhi;
+        }
+    }
     Estimator est;
 #pragma unroll
     for (int k = 0; k < 5; ++k) est.w[k] = es->w[k];
@@ -547,6 +603,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
     }
     if (al) reps_of(p.state, e, p.R)[gl] = r;
+    if (p.crange && p.phase == 0) {  // oldest request in flight after the submit
+        const int64_t oh = group_min64<LPE>((al && r.count > 0) ? id_of_slot(id, r.h_idtask & 0xffffffu, p.pending_P)
+                                                               : INT64_MAX);
+        if (live && gl == 0) p.crange[3 * (int64_t)e + 2] = oh;
+    }
     if (live && gl == 0) {
         if (p.rate_out) p.rate_out[e] = rate;
         if (action_out && p.phase == 0) action_out[e] = (uint8_t)tier;
@@ -720,9 +781,11 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
-                        double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase, float* tc_img) {
+                        double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase, float* tc_img,
+                        int64_t* crange) {
     StepParams p = base_params(env, rec_ld, rec);
     p.phase = phase;
+    p.crange = crange;
     p.tc_img = tc_img;
     p.tc_ncols = W->hidden <= 32 ? 32 : W->hidden <= 64 ? 64 : W->hidden <= 128 ? 128 : 256;
     p.arrival = arrival;
