@@ -30,3 +30,5 @@ def test_struct_sizes_match_c():
     assert ctypes.sizeof(_lib.BeQWeights) == 8 + 4 * 8
     assert ctypes.sizeof(_lib.BeRecords) == 6 * 8
     assert ctypes.sizeof(_lib.BeGenCfg) == 128
+    assert ctypes.sizeof(_lib.BeThresholds) == 8 + 8 * _lib.MAX_THETA  # be_thresholds, by value
+    assert ctypes.sizeof(_lib.BeTrainIterCfg) == 3 * 8 + 2 * 8 + 8 + 6 * 4  # ... use_gate, router, _pad

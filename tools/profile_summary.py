@@ -41,6 +41,8 @@ def main():
         rep = os.path.join(ROOT, "gpurun_out", f"prof_{name}_{tag}.ncu-rep")
         if not os.path.exists(rep):
             continue
+        # the report itself is kept beside its summary (tracked; .gpurunignore keeps it off the box)
+        shutil.copyfile(rep, os.path.join(out_dir, f"{tag}_prof_{name}.ncu-rep"))
         d = ncu_summary.summary(rep)[0]
         unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
         def nbytes(k):
@@ -59,7 +61,7 @@ def main():
             tensor_pipe_pct=metric(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
             warps_active=metric(d, "sm__warps_active.avg.per_cycle_active"),
             registers=metric(d, "launch__registers_per_thread"),
-            source=f"ncu --set full --clock-control none, report gpurun_out/prof_{name}_{tag}.ncu-rep")
+            source=f"ncu --set full --clock-control none, report profiles/{tag}_prof_{name}.ncu-rep")
         raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                              text=True).stdout
         rows = list(csv.reader(io.StringIO(raw)))
