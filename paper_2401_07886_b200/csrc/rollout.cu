@@ -29,6 +29,9 @@
 // table in shared memory, 0.84e9 at 3 CTAs/SM), so it keeps 2 CTAs/SM and stages the
 // skip table; the true-rate variant runs 3 CTAs/SM and reads it through L1 when the
 // batch fills them (config 4), else 2 CTAs/SM (config 1: 18 envs, latency-bound).
+#ifndef BE_RING_PER_GROUP
+#define BE_RING_PER_GROUP 1
+#endif
 #ifndef BE_TRACE_EVICT_FIRST
 #define BE_TRACE_EVICT_FIRST 1
 #endif
@@ -97,6 +100,7 @@ struct RolloutParams {
     int32_t screen;      // 1 = certified fp32 decision screen (qnet_screen) + fp64 fallback
     double inv_scale[BE_MAX_TIERS];  // 1 / batch_scales[m] (host IEEE division)
     double inv_rate_scale;           // 1 / rate_scale
+    int32_t ring_per_group;  // 1: replica rings indexed by the persistent group, else by env
     int32_t exact_mul;   // 1 = obs * (1/s) == obs / s for every reachable obs and tier
                          // (be_env.exact_mul; always so for power-of-two scales); the
                          // throughput variant (OCC = 1) is launched only then
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
     const int gl = lane & (LPE - 1);       // lane within the env group
     const int grp = LPE == 32 ? 0 : lane / LPE;
     const int g0 = grp * LPE;              // first lane of the group
+    const int my_group = (int)((blockIdx.x * blockDim.x + threadIdx.x) / LPE);  // persistent group id
     const unsigned gmask = LPE == 32 ? FULL : (0xffffu << g0);
     const TierC tc = lane_tier(p.cfg, gl, skip_tab);
     const bool active_lane = tc.tier >= 0;
@@ -228,7 +233,8 @@ __global__ void __launch_bounds__(BE_ROLLOUT_THREADS, OCC ? BE_ROLLOUT_MINB : BE
                 seg_end = p.seg_off[env + 1];
                 next_seg = seg_mark(seg);
                 cur_xr = __longlong_as_double(0x7ff8000000000000LL);  // NaN until a mark applies
-                ring = p.rings + ((size_t)env * p.R + (active_lane ? gl : 0)) * ((size_t)mask + 1);
+                ring = p.rings + ((size_t)(p.ring_per_group ? my_group : env) * p.R + (active_lane ? gl : 0)) *
+                                     ((size_t)mask + 1);
                 rep_reset(r);
                 r.head = 0;
                 est.n = 0;
@@ -402,7 +408,12 @@ static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st
     const long long max_blocks = (p.E + groups_per_block - 1) / groups_per_block;
     if (blocks > max_blocks) blocks = max_blocks;
     if (blocks < 1) blocks = 1;
-    kern<<<(unsigned)blocks, threads, smem, st>>>(p);
+    RolloutParams q = p;
+    // FIFO rings per persistent group when every group id indexes the allocation (the
+    // next env of a group reuses its predecessor's L1/L2-warm ring lines; rings by env
+    // id touch cold lines at every env start and leave dead dirty lines to be evicted)
+    q.ring_per_group = BE_RING_PER_GROUP && blocks * groups_per_block <= (long long)p.E;
+    kern<<<(unsigned)blocks, threads, smem, st>>>(q);
     e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "rollout launch");
     const int32_t pl[8] = {M, LPE, p.cfg.estimator_true_rate ? 1 : 0,
