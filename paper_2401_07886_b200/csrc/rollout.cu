@@ -15,6 +15,7 @@
 #include <stdint.h>
 #include <climits>
 #include <math.h>
+#include <stdlib.h>
 
 #include "be_env.cuh"
 #include "be_internal.h"
@@ -101,6 +102,7 @@ struct RolloutParams {
     double inv_scale[BE_MAX_TIERS];  // 1 / batch_scales[m] (host IEEE division)
     double inv_rate_scale;           // 1 / rate_scale
     int32_t ring_per_group;  // 1: replica rings indexed by the persistent group, else by env
+    int32_t throughput;      // 1: the throughput variant (3 CTAs/SM) — set by launch_rollout
     int32_t exact_mul;   // 1 = obs * (1/s) == obs / s for every reachable obs and tier
                          // (be_env.exact_mul; always so for power-of-two scales); the
                          // throughput variant (OCC = 1) is launched only then
@@ -388,9 +390,7 @@ size_t rollout_smem_bytes(int T, int M, int H, bool policy, int skip_rows, bool 
 
 template <int M, int LPE>
 static int launch_rollout_m(const RolloutParams& p, size_t smem, cudaStream_t st, int sms, int32_t* plan) {
-    // the throughput variant once the batch fills BE_ROLLOUT_MINB CTAs on every SM
-    const bool many = (long long)p.E >= (long long)sms * BE_ROLLOUT_MINB * (BE_ROLLOUT_THREADS / LPE) &&
-                      p.exact_mul;
+    const bool many = p.throughput != 0;  // chosen by launch_rollout
     auto kern = !p.cfg.estimator_true_rate ? rollout_kernel<M, LPE, 0, 0>
                 : many                     ? rollout_kernel<M, LPE, 1, 1>
                                            : rollout_kernel<M, LPE, 1, 0>;
@@ -486,9 +486,20 @@ int launch_rollout(be_env* env, const be_trace_soa* tr, const be_qweights* W, in
     }
     p.skip = env->d_skip;
     p.skip_rows = env->skip_rows;
-    // stage the skip table while two 256-thread CTAs still fit per SM (else read it via L1)
-    const bool many = (long long)p.E >= (long long)env->sms * BE_ROLLOUT_MINB *
-                                           (BE_ROLLOUT_THREADS / (env->R <= 16 ? 16 : 32));
+    // True rate: the variant with the shortest expected makespan.  One wave of the
+    // latency variant (2 CTAs/SM, 128 registers, the skip table staged in shared memory)
+    // beats everything; then one wave of the throughput variant (3 CTAs/SM, 80 registers,
+    // the skip table through L1); up to two waves of the latency variant still beat a
+    // throughput wave plus a partial second one (measured, tools/probe_occ.py: 8,192 envs
+    // — config 4's shard on 8 GPUs — 57.6 vs 67.2 ms); beyond, the throughput variant.
+    const long long gpb = BE_ROLLOUT_THREADS / (env->R <= 16 ? 16 : 32);
+    const long long g_lat = (long long)env->sms * BE_ROLLOUT_MINB_EST * gpb;
+    const long long g_many = (long long)env->sms * BE_ROLLOUT_MINB * gpb;
+    const long long E64 = p.E;
+    bool many = env->cfg.estimator_true_rate && env->exact_mul && !(E64 <= g_lat || (E64 > g_many && E64 <= 2 * g_lat));
+    if (const char* f = getenv("BE_ROLLOUT_FORCE_OCC"))  // probes (tools/probe_occ.py)
+        many = env->cfg.estimator_true_rate && env->exact_mul && atoi(f) != 0;
+    p.throughput = many ? 1 : 0;
     p.skip_smem = p.skip && rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_rows, p.screen) <=
                               (size_t)(env->cfg.estimator_true_rate && many ? BE_SKIP_SMEM_MAX : BE_SKIP_SMEM_MAX_EST);
     size_t smem = rollout_smem_bytes(T, M, policy ? p.H : 0, policy, p.skip_smem ? p.skip_rows : 0, p.screen);

@@ -42,11 +42,12 @@ def _check(tb, o, rw, rows, kw):
 
 
 def test_headline_variant_bench_workload(cuda):
-    """Config 4's kernel: 8,192 true-rate envs (>= SMs x 3 CTAs x 16 groups) at load
-    1x-10x, the reference-trained policy -> rollout_kernel<3, 16, TR=1, OCC=1>, skip
-    table through L1, certified screen; 40 strided envs (first, last and between,
-    i.e. envs pulled early and late from the dynamic env counter) vs the oracle."""
-    E, N = 8192, 2000
+    """Config 4's kernel: 10,000 true-rate envs (more than two waves of the latency
+    variant) at load 1x-10x, the reference-trained policy -> rollout_kernel<3, 16,
+    TR=1, OCC=1>, skip table through L1, certified screen; 40 strided envs (first, last
+    and between, i.e. envs pulled early and late from the dynamic env counter) vs the
+    oracle."""
+    E, N = 10000, 2000
     rates = [3.0 * (1 + (g % 10)) for g in range(E)]
     tb = TraceBatch.generate_stable(rates, N, 4, 2401, device=cuda, buckets=[g % 10 for g in range(E)])
     rw = RewardSpec.default()
@@ -60,14 +61,16 @@ def test_headline_variant_bench_workload(cuda):
 
 def test_headline_variant_offset_envs(cuda):
     """A GPU's shard of the sharded config 4 (global ids 57,344..65,535 on rank 7
-    of 8): traces keyed by global id, same kernel variant, oracle parity."""
+    of 8): traces keyed by global id; at 8,192 envs two waves of the latency variant
+    (2 CTAs/SM, skip table in shared memory) are the shorter makespan; oracle parity."""
     E, N, off = 8192, 1500, 57344
     gids = range(off, off + E)
     tb = TraceBatch.generate_stable([3.0 * (1 + (g % 10)) for g in gids], N, 4, 2401, device=cuda,
                                     env_offset=off)
     rw = RewardSpec.default()
     ro, o, kw = _run(tb, rw, "true-rate", want_realized=False)
-    assert ro.env.rollout_plan()["throughput_variant"] == 1
+    plan = ro.env.rollout_plan()
+    assert plan["throughput_variant"] == 0 and plan["true_rate"] == 1, plan
     _check(tb, o, rw, _strided(E, 24), kw)
 
 
