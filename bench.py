@@ -275,7 +275,21 @@ def training_probe(dev, world):
     if world > 1:
         from paper_2401_07886_b200 import sharding
         s = sharding.max_over_ranks(s, dev)
-    return dict(workload="config3: 4096 envs (TrainingWorkload, Philox), replay 1,048,576, batch 512, "
+    kernels = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        kt = json.load(open(prof)).get("kernels", {}).get("_train")
+        if kt:
+            try:
+                hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+            except (OSError, KeyError, ValueError):
+                hbm = 6650.0
+            # per-launch ncu figures (cold caches, serialised): HBM GB/s of every training-loop
+            # kernel against the measured copy peak, and the tensor-pipe activity of the
+            # tcgen05 env step (router="tc")
+            kernels = {k: dict(v, hbm_frac=v["hbm_gbs"] / hbm) for k, v in kt.items()}
+    return dict(kernels_ncu=kernels,
+                workload="config3: 4096 envs (TrainingWorkload, Philox), replay 1,048,576, batch 512, "
                          "Q-MLP 8-256-3 fp64, Adam lr 1e-4, Huber, target sync 500, epsilon 1.0->0.05",
                 iterations=its, updates=res.updates, updates_per_step=1,
                 iterations_per_s=its / s, updates_per_s=res.updates / s,

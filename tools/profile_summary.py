@@ -80,6 +80,32 @@ def main():
             f.write("\n# hot source lines (tools/ncu_lines.py): share of warp-stall samples and of "
                     "executed instructions\n")
             f.write(lines)
+    # training-loop kernels (prof_train_TAG / prof_step_tc_TAG: several kernels per report):
+    # per-launch DRAM bytes, time, HBM GB/s, issue and pipe activity (read by bench.py)
+    for rep_name in ("train", "step_tc"):
+        rep = os.path.join(ROOT, "gpurun_out", f"prof_{rep_name}_{tag}.ncu-rep")
+        if not os.path.exists(rep):
+            rep = os.path.join(out_dir, f"{tag}_prof_{rep_name}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        for d in ncu_summary.summary(rep):
+            kname = d["kernel"].split("(")[0].replace("void ", "").split("<")[0].strip()
+            if kname in summ["kernels"].get("_train", {}):
+                continue  # first launch of each kernel
+            unit = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+            def nb(k, d=d):
+                v = d.get(k)
+                return None if v is None else float(v[0].replace(",", "")) * unit.get(v[1], 1.0)
+            t = metric(d, "gpu__time_duration.sum")
+            t_us = t * (1e3 if d["gpu__time_duration.sum"][1] == "ms" else 1.0)
+            b = (nb("dram__bytes_read.sum") or 0) + (nb("dram__bytes_write.sum") or 0)
+            summ["kernels"].setdefault("_train", {})[kname] = dict(
+                tag=tag, time_us=t_us, dram_bytes=b, hbm_gbs=b / (t_us * 1e-6) / 1e9,
+                issue_active_pct=metric(d, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                tensor_pipe_pct=metric(d, "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+                fp64_pipe_pct=metric(d, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                source=f"ncu --set full --clock-control none, report profiles/{tag}_prof_{rep_name}.ncu-rep "
+                       "(config 3: 4,096 envs, batch 512)")
     launches = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(launches):
         shutil.copy(launches, os.path.join(out_dir, f"{tag}_launches.csv"))
