@@ -37,7 +37,10 @@ def make_case(E, ld, seed, ragged=True, n_buckets=3):
 
 
 @pytest.mark.parametrize("E,ld,ragged", [(1, 10000, False), (77, 1000, True), (1000, 333, True),
-                                         (64, 4096, False), (33, 25, True)])
+                                         (64, 4096, False), (33, 25, True),
+                                         # >= one CTA of 4 warps x 2 groups per SM: the big-batch tile
+                                         # shape (256-byte bursts, two 32-env groups per warp)
+                                         (40000, 70, True), (38000, 96, False)])
 def test_reduce_matches_oracle(cuda, E, ld, ragged):
     n, reward, flags, ss, sr, sb = make_case(E, ld, seed=E + ld, ragged=ragged)
     th = (1.0, 0.99, 0.98, 0.96, 0.94, 0.90)
