@@ -155,6 +155,10 @@ size_t be_env_device_bytes(const be_env* env);
 int32_t be_env_reset(be_env* env, const uint8_t* mask, void* stream);
 /* Sync `stream` and report latched device errors (ring overflow, ...). */
 int32_t be_env_check(be_env* env, void* stream);
+/* The latched device status {code, env} copied to dst (host pinned or device int32[2])
+ * in stream order, without a synchronisation: a pipelined caller (StreamingEvaluator)
+ * reads it with the batch's results and calls be_env_check only when it is nonzero. */
+int32_t be_env_status_async(be_env* env, int32_t* dst, void* stream);
 /* Counters of the certified fp32 decision screen of be_rollout_greedy, summed
  * over all rollouts since the last reset: out[0] = screened decisions,
  * out[1] = decisions that fell back to fp64.  Synchronises the device. */

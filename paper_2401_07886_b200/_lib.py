@@ -134,6 +134,7 @@ SIGNATURES = {
     "be_env_device_bytes": (_SZ, [_P]),
     "be_env_reset": (_I32, [_P, _P, _P]),
     "be_env_check": (_I32, [_P, _P]),
+    "be_env_status_async": (_I32, [_P, _P, _P]),
     "be_env_screen_stats": (_I32, [_P, _P, _I32]),
     "be_env_rollout_plan": (_I32, [_P, _P]),
     "be_env_step": (_I32, [_P, _P, _P, _P, _P, ctypes.POINTER(BeQWeights), _I32, _D, _U64, _U64,

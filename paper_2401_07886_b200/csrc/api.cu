@@ -242,6 +242,12 @@ int32_t be_env_reset(be_env* env, const uint8_t* mask, void* stream) {
     return launch_env_reset(env, mask, (cudaStream_t)stream);
 }
 
+int32_t be_env_status_async(be_env* env, int32_t* dst, void* stream) {
+    if (!env || !dst) return set_error(BE_EINVAL, "NULL argument");
+    cudaError_t e = cudaMemcpyAsync(dst, env->d_status, 2 * sizeof(int32_t), cudaMemcpyDefault, (cudaStream_t)stream);
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "be_env_status_async");
+}
+
 int32_t be_env_check(be_env* env, void* stream) {
     if (!env) return set_error(BE_EINVAL, "env is NULL");
     cudaError_t e = cudaStreamSynchronize((cudaStream_t)stream);
@@ -258,7 +264,7 @@ int32_t be_env_check(be_env* env, void* stream) {
                  "overflow; recreate the env with a larger ring_capacity",
                  st[1], 1 << env->cap_log2);
     else if (st[0] == BE_EINVAL)
-        snprintf(msg, sizeof(msg), "env %d: action / tier out of range", st[1]);
+        snprintf(msg, sizeof(msg), "env %d: action / tier or task id out of range", st[1]);
     else if (st[0] == BE_ENONFINITE)
         snprintf(msg, sizeof(msg), "env %d: non-finite network input", st[1]);
     else if (st[0] == BE_ECUDA)

@@ -427,7 +427,12 @@ class StreamingEvaluator:
             self._freed[slot].record(ks)
             host_stats = self._stats_buffer(red)
             for k, t in host_stats.items():
-                t.copy_(getattr(red, k), non_blocking=True)
+                if k != "status":
+                    t.copy_(getattr(red, k), non_blocking=True)
+            # the env's latched status rides with the statistics: result() needs no
+            # stream-wide synchronisation (which would also wait for the next batch)
+            _lib.check(self.ro.env._L.be_env_status_async(self.ro.env.handle, host_stats["status"].data_ptr(),
+                                                           _lib.stream_ptr(ks)))
             done = torch.cuda.Event()
             done.record(ks)
         self.d2h_bytes = sum(t.numel() * t.element_size() for t in host_stats.values())
@@ -440,8 +445,9 @@ class StreamingEvaluator:
         shapes = tuple((tuple(getattr(red, k).shape), getattr(red, k).dtype) for k in self._STATS)
         if shapes != self._stat_shapes:
             self._stat_shapes = shapes
-            self._stat_pool = [{k: torch.empty(sh, dtype=dt, pin_memory=True)
-                                for k, (sh, dt) in zip(self._STATS, shapes)}
+            self._stat_pool = [dict({k: torch.empty(sh, dtype=dt, pin_memory=True)
+                                     for k, (sh, dt) in zip(self._STATS, shapes)},
+                                    status=torch.zeros(2, dtype=torch.int32, pin_memory=True))
                                for _ in range(self.max_outstanding)]
         if not self._stat_pool:
             raise RuntimeError(f"more than {self.max_outstanding} submits await result()")
@@ -450,7 +456,9 @@ class StreamingEvaluator:
     def result(self, handle) -> ReduceResult:
         done, hs = handle
         done.synchronize()
-        self.ro.env.check(self.compute_stream)
+        if int(hs["status"][0]) != 0:  # raise with the library's message (syncs, error path only)
+            self._stat_pool.append(hs)
+            self.ro.env.check(self.compute_stream)
         out = ReduceResult(self.thresholds, *(hs[k].clone() for k in self._STATS))
         self._stat_pool.append(hs)
         return out

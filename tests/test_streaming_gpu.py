@@ -57,3 +57,18 @@ def test_streamed_rows_that_never_arrive_fail_loudly(cuda):
     ro.launch(tb, net, ready=(flags, 16, 7))
     with pytest.raises(CudaError, match="never became ready"):
         ro.env.check()
+
+
+def test_streaming_overflow_raises_at_result(cuda):
+    """A ring overflow inside a pipelined batch surfaces at that batch's result()
+    (the device status travels with the statistics; no stream-wide sync per batch)."""
+    from paper_2401_07886_b200 import CapacityError
+    E, N = 64, 3000
+    tiers, rw = default_tiers(), RewardSpec.default()
+    enc = StateEncoding(4, tuple(float(t.max_batch) for t in tiers))
+    tb = TraceBatch.generate_stable([30.0] * E, N, 4, 2, device=cuda)  # 10x load: queues grow
+    se = StreamingEvaluator(2, tiers, rw, E, N, enc, estimator_mode="true-rate", ring_capacity=8,
+                            device=cuda)  # static large tier floods its 4 replicas
+    h = se.submit(pin_trace(tb))
+    with pytest.raises(CapacityError):
+        se.result(h)

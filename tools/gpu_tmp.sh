@@ -1,2 +1,4 @@
-timeout 900 python -m pytest -q -x tests/test_reduce_gpu.py tests/test_rollout_gpu.py tests/test_streaming_gpu.py tests/test_bench_gpu.py tests/test_acceptance_gpu.py > gpurun_out/r2w_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2w_pytest.log; tail -2 gpurun_out/r2w_pytest.log
-for i in 1 2; do timeout 300 python tools/probe_reduce.py 2>&1 | tail -1 | cut -c1-130; timeout 300 python tools/probe_reduce.py 4096 10000 2>&1 | tail -1 | cut -c1-130; done
+timeout 900 python -m pytest -q -x tests/test_streaming_gpu.py tests/test_bench_gpu.py > gpurun_out/r2y_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2y_pytest.log; tail -3 gpurun_out/r2y_pytest.log
+timeout 900 python bench.py --steps 20 --warmup 5 --no-training --no-cpu-baseline > gpurun_out/r2y_bench.json 2> gpurun_out/r2y_bench.err
+python -c "
+import json; d=json.loads(open('gpurun_out/r2y_bench.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['e2e']['value']/d['value'], d['reducer_roofline']['frac'])"
