@@ -1,4 +1,6 @@
-timeout 900 python -m pytest -q -x tests/test_streaming_gpu.py tests/test_bench_gpu.py > gpurun_out/r2y_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2y_pytest.log; tail -3 gpurun_out/r2y_pytest.log
-timeout 900 python bench.py --steps 20 --warmup 5 --no-training --no-cpu-baseline > gpurun_out/r2y_bench.json 2> gpurun_out/r2y_bench.err
-python -c "
-import json; d=json.loads(open('gpurun_out/r2y_bench.json').read().strip().splitlines()[-1]); print(d['value'], d['e2e']['value'], d['e2e']['value']/d['value'], d['reducer_roofline']['frac'])"
+rm -f gpurun_out/ab.txt
+bash tools/gpu_ab.sh na ef2 na ef2
+cat gpurun_out/ab.txt
+for v in ef2; do
+BE200_LIB=$PWD/paper_2401_07886_b200/libbe200_$v.so timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:rollout_kernel -s 1 -c 1 --csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-training 2>/dev/null | grep -E "dram__" | awk -F'","' -v v=$v '{print v, $(NF-2), $NF}'
+done
