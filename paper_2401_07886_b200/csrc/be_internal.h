@@ -92,12 +92,28 @@ int launch_env_step(be_env* env, const double* arrival, const uint8_t* task,
                     uint8_t* action_out, double* q_out, double* x_out, cudaStream_t st);
 int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st,
                      const uint8_t* mask = nullptr, int new_segment = 0);
+// be_train_iteration with the fp64 router: the replay commit (ReplayBuffer
+// resolve_reward / resolve_next_state -> push, trainer.py:143-156) fused into the env
+// step — the step's completed transitions go straight into the ring (same slots as
+// commit_fused_kernel: env-id order, request-id order within an env)
+struct StepCommitArgs {
+    int64_t capacity;
+    double *rs, *rs2, *rr, *rc;  // ring states / next states / rewards / continue flags
+    uint8_t* ra;                 // ring actions
+    int64_t* low;                // [E] oldest request still in flight
+    int64_t* ring_state;         // cursor, size, total, last count, in-flight high-water mark
+    int32_t* status;             // learner status (pending-store overflow)
+    unsigned long long* scan;    // [ceil(E / 16)] decoupled look-back state
+    unsigned* epoch;             // scan epoch (advanced by the last block)
+};
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
                         double* x_base, cudaStream_t st, const struct WorkloadArgs* wl = nullptr,
-                        int phase = 0, float* tc_img = nullptr, int64_t* crange = nullptr);
+                        int phase = 0, float* tc_img = nullptr, int64_t* crange = nullptr,
+                        const StepCommitArgs* commit = nullptr);
+bool env_step_commit_supported(const be_env* env);
 // the training step with the decision on the tensor cores (tc_img != NULL above):
 // shared-memory size and the kernel attribute (set before any graph capture)
 size_t step_tc_smem_bytes(int H);

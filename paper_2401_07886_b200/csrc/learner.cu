@@ -720,7 +720,8 @@ struct be_learner {
     double* it_rate;
     unsigned* done;    // fused-update CTA arrival counter
     unsigned long long* scan;  // commit look-back state [(E + 7) / 8]
-    unsigned* ticket;          // commit ticket / epoch
+    unsigned* ticket;          // commit ticket / epoch; [2] the fused step+commit's scan epoch
+    unsigned long long* scan16;  // fused step+commit look-back state [(E + 15) / 16]
     // peer exchange (phase 4): one allocation = [2][nparam + 2] doubles + the epoch flag
     void* xmem;
     int32_t x_world, x_rank;
@@ -740,7 +741,7 @@ static void learner_free(be_learner* L) {
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
                     L->preward, L->low, L->status, L->wl_state,
                     L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket,
-                    L->tc_img, L->tc_stats, L->crange};
+                    L->tc_img, L->tc_stats, L->crange, L->scan16};
     for (void* p : ptrs) cudaFree(p);
     for (int r = 0; r < XMAX_RANKS; ++r)
         if (L->x_opened[r]) cudaIpcCloseMemHandle(L->x_opened[r]);
@@ -792,7 +793,7 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
         {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64},
         {(void**)&L->scan, ((E + CENVS - 1) / CENVS) * 8}, {(void**)&L->ticket, 64},
-        {(void**)&L->crange, E * 3 * 8}};
+        {(void**)&L->crange, E * 3 * 8}, {(void**)&L->scan16, ((E + 15) / 16) * 8}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -1175,6 +1176,7 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         be_records rec{};
         rec.flags = L->pflags;
         rec.reward = L->preward;
+        bool fused_commit = false;
         if (c->router == BE_ROUTER_TC && env->R <= 16) {
             // the decision on the tensor cores inside the env step: prep_kernel also packs
             // the router image; env_step_tc_kernel runs layer 1 of 16 envs per CTA as one
@@ -1199,6 +1201,16 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2,
                                      nullptr, L->crange);
+        } else if (env_step_commit_supported(env)) {
+            // the replay commit fused into the env step: one launch, no flag scan
+            StepCommitArgs cm{cf.replay_capacity, L->rs, L->rs2, L->rr, L->rc, L->ra, L->low,
+                              L->ring_state, L->status, L->scan16, L->ticket + 2};
+            rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
+                                     c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
+                                     cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,
+                                     nullptr, nullptr, &cm);
+            if (rc) return rc;
+            fused_commit = true;
         } else {
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
@@ -1206,8 +1218,10 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                      nullptr, L->crange);
         }
         if (rc) return rc;
-        rc = commit_impl(L, 0, it, st, L->crange);
-        if (rc) return rc;
+        if (!fused_commit) {
+            rc = commit_impl(L, 0, it, st, L->crange);
+            if (rc) return rc;
+        }
     }
     const int ups = c->updates_per_step;
     if (c->phase == 0) {

@@ -95,7 +95,160 @@ struct StepParams {
     // training commits (be_train_iteration): per env {lowest, highest request id completed
     // in this step's advance, oldest request still in flight after the submit} (nullable)
     int64_t* crange;
+    // fused replay commit (env_step_commit_kernel; fuse_commit = 1)
+    StepCommitArgs cm;
+    int32_t fuse_commit;
 };
+
+// Shared state of one env_step_commit_kernel CTA round.
+constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
+constexpr int SC_PASS = 256;  // request ids of an env's completed range per list pass
+struct CommitShared {
+    long long cursor, agg, excl;
+    long long pre[SC_ENVS];  // exclusive prefix of the counts within the block
+    int cnt[SC_ENVS];
+    unsigned long long ep;   // scan epoch << 40
+    unsigned long long wmax;
+    uint32_t list[SC_ENVS][SC_PASS];  // pending slots of an env's committable transitions, id order
+};
+
+// What one env's step hands the fused commit: the id range this step's advance
+// completed (every request in it is committable now: its next state x_{j+1}
+// exists) and the oldest request still in flight after the submit.  The step also
+// publishes the block's commit count as soon as the advance is done (commit_publish),
+// so the cross-block scan overlaps the Q forward and the submit.
+struct StepOut {
+    int64_t jlo, jhi, oldest;
+    CommitShared* cs;
+    int vb, le;
+    bool live;
+};
+
+// One pass of an env's completed id range (ids [b0, b0 + SC_PASS) of it, 16 per lane,
+// independent flag loads): the committable ones (reward written: flag 0x40) -> their
+// pending slots into `list` in id order.  Returns how many (group-uniform).
+template <bool FIRST>
+__device__ __forceinline__ int commit_list_pass(const StepParams& p, uint32_t* list, int e, int P, int64_t r0,
+                                                int64_t b0, int64_t L, int gl, unsigned gmask) {
+    const int64_t sbase = (r0 + b0 + gl * 16) % P;
+    unsigned bits = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        int64_t sj = sbase + k;
+        if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
+        if (b0 + gl * 16 + k < L && (p.rec.flags[(int64_t)e * P + sj] & 0x40)) bits |= 1u << k;
+    }
+    const int cnt = __popc(bits);
+    int inc = cnt;
+#pragma unroll
+    for (int off = 1; off < 16; off <<= 1) {
+        const int v = __shfl_up_sync(gmask, inc, off, 16);
+        if (gl >= off) inc += v;
+    }
+    int r = inc - cnt;
+    while (bits) {
+        int64_t sj = sbase + __ffs(bits) - 1;
+        if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
+        list[r++] = (uint32_t)sj;
+        bits &= bits - 1;
+    }
+    __syncwarp(gmask);
+    return __shfl_sync(gmask, inc, 15, 16);
+}
+
+__device__ __forceinline__ int64_t wrap_slot(int64_t s, int64_t cap) {
+    while (s >= cap) s -= cap;
+    return s;
+}
+
+// Transition (x_j, a_j, r_j, x_{j+1}) of pending slot sj: elements [d0, d0 + min(n, W))
+// of the two states, all loads issued before any store (the ring may alias nothing,
+// but the compiler cannot know).
+template <int W>
+__device__ __forceinline__ void commit_load(const StepParams& p, int e, int n, int P, int64_t sj, double (&xa)[W],
+                                            double (&xb)[W], uint8_t& a, double& r, int d0 = 0, int D = -1) {
+    if (D < 0) D = n;
+    const int64_t sj1 = sj + 1 == P ? 0 : sj + 1;
+    const double* pa = p.x_out + (sj * p.E + e) * D + d0;
+    const double* pb = p.x_out + (sj1 * p.E + e) * D + d0;
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+        if (k < n) {
+            xa[k] = pa[k];
+            xb[k] = pb[k];
+        }
+    a = p.action_out[sj * p.E + e];
+    r = p.rec.reward[(int64_t)e * P + sj];
+}
+template <int W>
+__device__ __forceinline__ void commit_store(const StepParams& p, const StepCommitArgs& c, int e, int n, int P, int64_t sj,
+                                             int64_t slot, const double (&xa)[W], const double (&xb)[W], uint8_t a,
+                                             double r, int d0 = 0, int D = -1, bool scalars = true) {
+    if (D < 0) D = n;
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+        if (k < n) {
+            c.rs[slot * D + d0 + k] = xa[k];
+            c.rs2[slot * D + d0 + k] = xb[k];
+        }
+    if (scalars) {
+        c.ra[slot] = a;
+        c.rr[slot] = r;
+        c.rc[slot] = 1.0;
+        p.rec.flags[(int64_t)e * P + sj] = 0x20;
+    }
+}
+
+#ifdef BE_STEPC_TIMING
+__device__ unsigned long long g_stepc_t[1024 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define STEPC_T(k) \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_stepc_t[blockIdx.x * 8 + (k)] = gtimer();
+#else
+#define STEPC_T(k)
+#endif
+
+// scan words: epoch << 40 | flag << 38 | value (flag 1 = block aggregate, 2 = inclusive prefix)
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+// release: this thread's earlier reads of the ring cursor / scan epoch are ordered
+// before the publication the last block waits for before it changes them
+__device__ __forceinline__ void st_release_u64(unsigned long long* a, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+
+// Block-wide (every thread of the CTA calls it once per round): the counts of the
+// block's 16 envs -> exclusive prefixes within the block, and the block aggregate
+// published to the look-back array (block 0: directly as its inclusive prefix).
+__device__ __forceinline__ void commit_publish(const StepParams& p, const StepOut& so, int count) {
+    CommitShared& cs = *so.cs;
+    if ((threadIdx.x & 15) == 0) cs.cnt[so.le] = so.live ? count : 0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const long long own = lane < SC_ENVS ? cs.cnt[lane] : 0;
+        long long inc = own;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long v = __shfl_up_sync(FULL, inc, off);
+            if (lane >= off) inc += v;
+        }
+        if (lane < SC_ENVS) cs.pre[lane] = inc - own;
+        const long long agg = __shfl_sync(FULL, inc, 31);
+        if (lane == 0) {
+            cs.agg = agg;
+            STEPC_T(1)
+            st_release_u64(&p.cm.scan[so.vb], cs.ep | ((so.vb == 0 ? 2ull : 1ull) << 38) | (unsigned long long)agg);
+        }
+    }
+}
 
 // request id of pending slot s (= id mod P) among the ids <= t
 __device__ __forceinline__ int64_t id_of_slot(int64_t t, uint32_t s, int32_t P) {
@@ -137,7 +290,8 @@ struct TcStepCtx {
 
 template <int M, int LPE, bool TCQ = false>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
-                                         bool policy, int T, int H, int D, TcStepCtx* tcx = nullptr);
+                                         bool policy, int T, int H, int D, TcStepCtx* tcx = nullptr,
+                                         StepOut* so = nullptr);
 
 // LPE lanes per env: 16 (two envs per warp) when the cluster has <= 16 replicas and
 // the encoded state fits 16 lanes, else 32
@@ -161,6 +315,174 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
         step_env<M, LPE>(p, e < p.E ? e : p.E - 1, e < p.E, sc, p.qpack, policy, T, H, D);
     }
     pdl_trigger();  // this CTA is done: the next kernel may start filling the SM
+}
+
+// The training env step (be_train_iteration, fp64 router) with the replay commit
+// fused in: commit_fused_kernel's slots and arithmetic without its launch, its ticket
+// or its flag scan.  Each CTA round steps 16 envs (two per warp); every request the
+// step's advance completed is committable now (its reward was just written, its next
+// state x_{j+1} exists: j <= it - 1), so the env's count is the number of FIFO entries
+// its replicas popped.  The counts are scanned across rounds by decoupled look-back
+// (virtual block = round x grid + CTA; the grid is one resident wave, so every
+// predecessor is running or done), then each env writes its transitions — request-id
+// order within the env, env-id order across envs, exactly commit_fused_kernel's slots.
+
+template <int M>
+__global__ void __launch_bounds__(256) env_step_commit_kernel(const StepParams p) {
+    STEPC_T(0)
+    pdl_wait();  // the previous kernel has completed and its writes are visible
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Score& sc = *reinterpret_cast<Score*>(smem_raw);
+    __shared__ CommitShared cs;
+    const StepCommitArgs& c = p.cm;
+    const int T = p.cfg.n_tasks, H = p.H, D = T + M + 1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = lane >> 4, gl = lane & 15;
+    const unsigned gmask = 0xffffu << (grp * 16);
+    if (threadIdx.x == 0) {
+        // cursor and scan epoch before this step's commits: read before this CTA
+        // publishes anything (the last block changes both only after every block has)
+        cs.cursor = __ldcg(c.ring_state);
+        cs.ep = (unsigned long long)(__ldcg(c.epoch) & 0xffffffu) << 40;
+        cs.wmax = 0ull;
+    }
+    if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
+    __syncthreads();
+    const int64_t it = *p.iter_dev;
+    const int P = p.pending_P;
+    const int nvb = (p.E + SC_ENVS - 1) / SC_ENVS;
+    for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {  // CTA-uniform rounds
+        const int le = warp * 2 + grp;
+        const int e = vb * SC_ENVS + le;
+        const bool live = e < p.E;
+        StepOut so;
+        so.cs = &cs;
+        so.vb = vb;
+        so.le = le;
+        so.live = live;
+        step_env<M, 16>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
+        STEPC_T(2)
+        // ---- this env's transitions, part 1 (independent of the cross-block prefix, so
+        // it overlaps warp 0's look-back): the flags of the completed id range, 16 ids
+        // per lane (independent loads) -> the env's committable pending slots in id
+        // order (shared list); the group's first 16 transitions loaded into registers
+        // (lane t holds transition t)
+        const int64_t L = (live && so.jlo <= so.jhi) ? so.jhi - so.jlo + 1 : 0;
+        const int64_t r0 = L ? so.jlo % P : 0;
+        const bool fast = D <= 8;
+        int gtot = L ? commit_list_pass<true>(p, cs.list[le], e, P, r0, 0, L, gl, gmask) : 0;
+        double xa[8], xb[8], rv = 0.0;
+        uint8_t av = 0;
+        int64_t sj0 = 0;
+        if (fast && gl < gtot) {
+            sj0 = cs.list[le][gl];
+            commit_load<8>(p, e, D, P, sj0, xa, xb, av, rv);
+        }
+#ifndef BE_STEPC_NOLB
+        if (warp == 0 && vb > 0) {
+#else
+        if (false) {
+#endif
+            // the block's exclusive prefix: look back over windows of 256 predecessors
+            // (8 per lane, nearest first), summing aggregates up to the nearest
+            // inclusive prefix; the aggregates were published right after each
+            // block's advance, so one window usually completes the scan
+            long long excl = 0;
+            for (int j = vb - 1;; j -= 256) {
+                unsigned long long v[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int idx = j - lane * 8 - k;
+                    v[k] = idx >= 0 ? ld_relaxed_u64(&c.scan[idx]) : (2ull << 38);
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const int idx = j - lane * 8 - k;
+                    while (idx >= 0 && ((v[k] >> 40) != (cs.ep >> 40) || ((v[k] >> 38) & 3ull) == 0))
+                        v[k] = ld_relaxed_u64(&c.scan[idx]);
+                }
+                int kstop = 8;  // this lane's nearest inclusive prefix
+#pragma unroll
+                for (int k = 7; k >= 0; --k)
+                    if (((v[k] >> 38) & 3ull) == 2ull) kstop = k;
+                const unsigned pb = __ballot_sync(FULL, kstop < 8);
+                const int stop = pb ? __ffs(pb) - 1 : 32;  // lanes < stop: all 8; lane stop: k <= kstop
+                long long val = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (lane < stop || (lane == stop && k <= kstop)) val += (long long)(v[k] & ((1ull << 38) - 1));
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) val += __shfl_xor_sync(FULL, val, off);
+                excl += val;
+                if (pb) break;
+            }
+            if (lane == 0) {
+                cs.excl = excl;
+                // acquire what the observed publications released (their cursor reads)
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                st_release_u64(&c.scan[vb], cs.ep | (2ull << 38) | (unsigned long long)(excl + cs.agg));
+            }
+        } else if (warp == 0 && lane == 0) {
+            cs.excl = 0;
+        }
+        if (warp == 0 && lane == 0 && vb == nvb - 1) {  // commits this step: advance the ring
+            const long long n = cs.excl + cs.agg;
+            c.ring_state[3] = n;
+            c.ring_state[0] = (cs.cursor + n) % c.capacity;
+            c.ring_state[1] = c.ring_state[1] + n < c.capacity ? c.ring_state[1] + n : c.capacity;
+            c.ring_state[2] += n;
+            *c.epoch = *c.epoch + 1u;
+        }
+        STEPC_T(3)
+        __syncthreads();
+        STEPC_T(4)
+#ifndef BE_STEPC_NOWR
+        if (live) {
+#else
+        if (false) {
+#endif
+            // ---- part 2: the stores (ReplayBuffer.push, trainer.py:123-133) from the
+            // env's slot base, request-id order; transitions past the first 16 go one
+            // round trip per 16, ids past the first SC_PASS of the range one pass each
+            const int64_t s0 = (cs.cursor + cs.excl + cs.pre[le]) % c.capacity;
+            if (fast && gl < gtot) commit_store<8>(p, c, e, D, P, sj0, wrap_slot(s0 + gl, c.capacity), xa, xb, av, rv);
+            int64_t total = 0;
+            for (int64_t b0 = 0; b0 < L; b0 += SC_PASS) {
+                if (b0 > 0) {
+                    __syncwarp(gmask);  // the list is rewritten
+                    gtot = commit_list_pass<false>(p, cs.list[le], e, P, r0, b0, L, gl, gmask);
+                }
+                for (int t = (b0 == 0 && fast) ? gl + 16 : gl; t < gtot; t += 16) {
+                    const int64_t sj = cs.list[le][t];
+                    const int64_t slot = wrap_slot(s0 + total + t, c.capacity);
+                    for (int d0 = 0; d0 < D; d0 += 8) {  // D > 8: several element chunks
+                        double ya[8], yb[8], r;
+                        uint8_t a;
+                        commit_load<8>(p, e, D - d0, P, sj, ya, yb, a, r, d0, D);
+                        commit_store<8>(p, c, e, D - d0, P, sj, slot, ya, yb, a, r, d0, D, d0 == 0);
+                    }
+                }
+                total += gtot;
+            }
+#ifdef BE_STEPC_TIMING
+            if (gl == 0 && blockIdx.x < 1024) {
+                atomicMax(&g_stepc_t[blockIdx.x * 8 + 7], ((unsigned long long)L << 32) | (unsigned)gtot);
+            }
+#endif
+            if (gl == 0) {
+                c.low[e] = so.oldest;
+                const int64_t win = it + 1 - so.oldest;
+                if (win >= P && atomicCAS(&c.status[0], 0, BE_ECAPACITY) == 0) c.status[1] = e;
+                if (win > 0) atomicMax(&cs.wmax, (unsigned long long)win);
+            }
+        }
+        STEPC_T(5)
+        __syncthreads();  // cs is reused by the next round
+        STEPC_T(6)
+    }
+    // high-water mark of in-flight decisions per env (ring_state[4])
+    if (threadIdx.x == 0 && cs.wmax > (unsigned long long)__ldcg(c.ring_state + 4))
+        atomicMax(reinterpret_cast<unsigned long long*>(c.ring_state + 4), cs.wmax);
+    pdl_trigger();
 }
 
 // The greedy decision of one env on the tensor cores, inside the env step (every
@@ -428,7 +750,7 @@ void step_tc_prepare(int M, int H) {
 // reductions are warp-wide); `live` = false for a padding group past the last env.
 template <int M, int LPE, bool TCQ>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
-                                         bool policy, int T, int H, int D, TcStepCtx* tcx) {
+                                         bool policy, int T, int H, int D, TcStepCtx* tcx, StepOut* so) {
     const int lane = threadIdx.x & 31;
     const int gl = lane & (LPE - 1), grp = LPE == 32 ? 0 : lane / LPE;
     const unsigned gmask = LPE == 32 ? FULL : (0xffffu << (grp * LPE));
@@ -497,7 +819,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     const uint32_t cr_h0 = r.head, cr_idt0 = r.h_idtask;
     const int cr_c0 = r.count;
     if (al) ok = advance_lane(r, tc, U, ring, mask, sc, out);
-    if (p.crange) {
+    if (p.crange || so) {
         // the requests this advance completed are the popped FIFO prefix of every replica
         // (ids increase along a FIFO): the env's lowest / highest completed id of this
         // step bound the commit scan (be_train_iteration), instead of the whole window of
@@ -513,7 +835,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         }
         jlo = group_min64<LPE>(jlo);
         jhi = group_max64<LPE>(jhi);
-        if (live && gl == 0) {
+        if (so) {
+            so->jlo = jlo;
+            so->jhi = jhi;
+            commit_publish(p, *so, (int)group_sum<LPE>((unsigned)popped, grp));
+        } else if (live && gl == 0) {
             p.crange[3 * (int64_t)e] = jlo;
             p.crange[3 * (int64_t)e + 1] = jhi;
         }
@@ -603,10 +929,11 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         ok &= submit_lane(r, tc, U, rid | ((uint32_t)task << 24), ring, mask);
     }
     if (al) reps_of(p.state, e, p.R)[gl] = r;
-    if (p.crange && p.phase == 0) {  // oldest request in flight after the submit
+    if ((p.crange || so) && p.phase == 0) {  // oldest request in flight after the submit
         const int64_t oh = group_min64<LPE>((al && r.count > 0) ? id_of_slot(id, r.h_idtask & 0xffffffu, p.pending_P)
                                                                : INT64_MAX);
-        if (live && gl == 0) p.crange[3 * (int64_t)e + 2] = oh;
+        if (so) so->oldest = oh;
+        else if (live && gl == 0) p.crange[3 * (int64_t)e + 2] = oh;
     }
     if (live && gl == 0) {
         if (p.rate_out) p.rate_out[e] = rate;
@@ -680,6 +1007,19 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
                                        step_tc_smem_bytes(p.H), st, p);
             return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step (tensor cores) launch");
         }
+    }
+    if (p.fuse_commit) {  // the training step + replay commit (two envs per warp)
+        if (!two) return set_error(BE_EINVAL, "fused commit needs <= 16 replicas and input dim <= 16");
+        int per_sm = 0, dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_commit_kernel<M>, 256, smem);
+        if (per_sm < 1) per_sm = 1;
+        // one resident wave (the look-back needs every predecessor running or done)
+        long long blocks = ((long long)p.E + SC_ENVS - 1) / SC_ENVS;
+        if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
+        cudaError_t e = launch_pdl(env_step_commit_kernel<M>, dim3((unsigned)blocks), dim3(256), smem, st, p);
+        return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step + commit launch");
     }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -782,10 +1122,17 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const int64_t* iter_dev, double eps_start, double eps_end, int64_t eps_decay,
                         int32_t pending_P, int64_t rec_ld, const be_records* rec, uint8_t* action_base,
                         double* x_base, cudaStream_t st, const WorkloadArgs* wl, int phase, float* tc_img,
-                        int64_t* crange) {
+                        int64_t* crange, const StepCommitArgs* commit) {
     StepParams p = base_params(env, rec_ld, rec);
     p.phase = phase;
     p.crange = crange;
+    if (commit) {
+        if (phase != 0 || tc_img || rec_ld != pending_P)
+            return set_error(BE_EINVAL, "the fused commit is the fp64-router training step");
+        p.cm = *commit;
+        p.fuse_commit = 1;
+        p.crange = nullptr;
+    }
     p.tc_img = tc_img;
     p.tc_ncols = W->hidden <= 32 ? 32 : W->hidden <= 64 ? 64 : W->hidden <= 128 ? 128 : 256;
     p.arrival = arrival;
@@ -808,6 +1155,10 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     return dispatch_step(p, step_smem_bytes(), st, wl);
 }
 
+bool env_step_commit_supported(const be_env* env) {
+    return env->R <= 16 && env->cfg.n_tasks + env->cfg.n_tiers + 1 <= 16;
+}
+
 int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStream_t st,
                      const uint8_t* mask, int new_segment) {
     StepParams p = base_params(env, rec_ld, rec);
@@ -818,3 +1169,9 @@ int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStr
 }
 
 }  // namespace be
+
+#ifdef BE_STEPC_TIMING
+extern "C" int be_debug_stepc_times(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, be::g_stepc_t, (size_t)n * sizeof(unsigned long long));
+}
+#endif

@@ -190,3 +190,23 @@ def test_training_modes_bit_identical(cuda):
             assert np.array_equal(a, b), mode
         assert [(x.step, x.loss, x.mean_recent_reward, x.epsilon) for x in r.log] == \
                [(x.step, x.loss, x.mean_recent_reward, x.epsilon) for x in ref.log], mode
+
+
+def test_training_modes_bit_identical_multi_round(cuda):
+    """The fused env step + replay commit over more envs than one resident wave of
+    CTAs (several look-back rounds per step) and a ring that wraps several times:
+    the device loop still equals the host-driven loop (env step, then the separate
+    commit kernel) bit for bit."""
+    tiers, rw = default_tiers(), RewardSpec.default()
+    cfg = TrainConfig(batch_size=128, buffer_capacity=50_000, warmup=1000, total_iterations=60,
+                      log_every=20, seed=11, target_sync_every=5)
+    out = {}
+    for mode in ("host", "device"):
+        out[mode] = run_training(tiers, rw, cfg, n_envs=6000, updates_per_step=1, mode=mode)
+    ref, r = out["host"], out["device"]
+    assert ref.transitions > 5 * cfg.buffer_capacity
+    assert r.updates == ref.updates and r.transitions == ref.transitions and r.max_inflight == ref.max_inflight
+    for a, b in zip(r.net.params(), ref.net.params()):
+        assert np.array_equal(a, b)
+    assert [(x.step, x.loss, x.mean_recent_reward) for x in r.log] == \
+           [(x.step, x.loss, x.mean_recent_reward) for x in ref.log]

@@ -43,7 +43,9 @@ def sass_lines(obj, kernel_sub):
 def main():
     rep, obj, ksub = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--print-source", "sass", "--csv"],
+    # one kernel of a multi-kernel report: filter on import, first matching launch
+    raw = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{ksub}", "-c", "1", "--page", "source",
+                          "--print-source", "sass", "--csv"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr_i = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
