@@ -28,6 +28,18 @@
 
 namespace be {
 
+#ifdef BE_LT_TIMING
+__device__ unsigned long long g_lt_t[512 * 16];
+#define LT_T(k)                                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 512) {                                         \
+        unsigned long long t_;                                                          \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+        g_lt_t[blockIdx.x * 16 + (k)] = t_;                                             \
+    }
+#else
+#define LT_T(k)
+#endif
+
 constexpr int LROWS = 4;       // rows per learner CTA (B = 512 -> 128 CTAs: latency, not work, bounds an update)
 constexpr int UTHREADS = 256;  // learner_update_kernel: 32 parameters x 8 tile slices per CTA
 constexpr int LTHREADS = 256;  // one thread per hidden unit (looping for H > 256)
@@ -258,6 +270,13 @@ struct LearnParams {
     const int64_t* iter_dev;
     int32_t ups, uidx;
     const int64_t* gate;  // non-NULL: update iff *gate != 0 (DP learner, all-reduced readiness)
+    // fused update (learner_tail): the last TAIL_CTAS tiles to finish reduce the tile
+    // partials of one hidden-unit slice each, apply the optimizer and repack the env
+    // step's weights; no second launch
+    int32_t tail;
+    unsigned long long* tick;  // [0] tile arrivals, [1] slice completions (monotonic)
+    double* qpack;             // the env step's packed weights (QLayout), or NULL
+    int32_t T;                 // tasks (packing)
 };
 
 __device__ __forceinline__ double relu_d(double x) {
@@ -265,37 +284,87 @@ __device__ __forceinline__ double relu_d(double x) {
     return __longlong_as_double(b & ~(b >> 63));
 }
 
-// Forward of LROWS rows through (W1,b1,W2,b2) into h (smem [LROWS][H]) and q
-// (smem [LROWS][M]); block-wide, fixed reduction order.
-// DM: compile-time upper bound of D (register-resident weight column).
+// The learner's three forwards in one pass (trainer.py:240-244): online(s'), target(s')
+// and online(s) for the tile's LROWS rows — the hidden layers of all three in one loop
+// over the hidden units (12 independent FMA chains per thread), then all 3 LROWS M
+// outputs with several (row, tier) pairs per warp in flight.  Fixed arithmetic per
+// output: h = relu((sum_d x_d W1[d][j], FMA chain in d order) + b1[j]); q = (lane-strided
+// FMA chains over j, xor-butterfly tree) + b2[m] — identical on every execution path.
+// w1 column j = threadIdx.x (wo, wt, bo, bt) arrives preloaded (the loads overlapped the
+// batch gather); W2 / b2 of both networks are staged in shared memory (sw2 = [2][H][M],
+// sb2 = [2][M]).
 template <int DM>
-__device__ void forward_rows(const double* x, int D, int H, int M, const double* w1,
-                             const double* b1, const double* w2, const double* b2, double* h,
-                             double* q) {
-    for (int j = threadIdx.x; j < H; j += blockDim.x) {
-        const double bj = b1[j];
-        double wcol[DM];
+__device__ __forceinline__ void load_w1_col(const double* w1, const double* b1, const double* tw1, const double* tb1,
+                                            int D, int H, int j, double (&wo)[DM], double (&wt)[DM], double& bo,
+                                            double& bt) {
+    bo = b1[j];
+    bt = tb1[j];
 #pragma unroll
-        for (int d = 0; d < DM; ++d) wcol[d] = d < D ? w1[d * H + j] : 0.0;
+    for (int d = 0; d < DM; ++d) {
+        wo[d] = d < D ? w1[d * H + j] : 0.0;
+        wt[d] = d < D ? tw1[d * H + j] : 0.0;
+    }
+}
+
+template <int DM>
+__device__ void forward3_rows(const double* xs2, const double* xs, int D, int H, int M, const double* w1,
+                              const double* b1, const double* tw1, const double* tb1, double (&wo)[DM],
+                              double (&wt)[DM], double bo, double bt, const double* sw2, const double* sb2,
+                              double* h2o, double* h2t, double* hs, double* q2, double* q2t, double* q) {
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        if (j != (int)threadIdx.x) load_w1_col<DM>(w1, b1, tw1, tb1, D, H, j, wo, wt, bo, bt);
 #pragma unroll
         for (int row = 0; row < LROWS; ++row) {
-            double acc = 0.0;
+            double a2o = 0.0, a2t = 0.0, ao = 0.0;
 #pragma unroll
             for (int d = 0; d < DM; ++d)
-                if (d < D) acc = __fma_rn(x[row * D + d], wcol[d], acc);
-            h[row * H + j] = relu_d(__dadd_rn(acc, bj));
+                if (d < D) {
+                    a2o = __fma_rn(xs2[row * D + d], wo[d], a2o);
+                    a2t = __fma_rn(xs2[row * D + d], wt[d], a2t);
+                    ao = __fma_rn(xs[row * D + d], wo[d], ao);
+                }
+            h2o[row * H + j] = relu_d(__dadd_rn(a2o, bo));
+            h2t[row * H + j] = relu_d(__dadd_rn(a2t, bt));
+            hs[row * H + j] = relu_d(__dadd_rn(ao, bo));
         }
     }
     __syncthreads();
-    // q[row][m] = sum_j h[row][j] w2[j][m]: warp w handles pairs w, w + 8, ...
+    constexpr int PW = 4;  // pairs per warp in flight
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
-    for (int pair = warp; pair < LROWS * M; pair += nw) {
-        const int row = pair / M, m = pair % M;
-        double acc = 0.0;
-        for (int j = lane; j < H; j += 32) acc = __fma_rn(h[row * H + j], w2[j * M + m], acc);
-        for (int off = 16; off > 0; off >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
-        if (lane == 0) q[pair] = __dadd_rn(acc, b2[m]);
+    const int npair = LROWS * M;
+    for (int pb = warp * PW; pb < 3 * npair; pb += nw * PW) {
+        const double* hp[PW];
+        const double* wp[PW];
+        int mm[PW];
+        double acc[PW];
+#pragma unroll
+        for (int i = 0; i < PW; ++i) {
+            const int id = pb + i < 3 * npair ? pb + i : 3 * npair - 1;
+            const int set = id / npair, pair = id % npair, row = pair / M;
+            mm[i] = pair % M;
+            hp[i] = (set == 0 ? h2o : set == 1 ? h2t : hs) + row * H;
+            wp[i] = sw2 + (set == 1 ? H * M : 0);
+            acc[i] = 0.0;
+        }
+        for (int j = lane; j < H; j += 32) {
+#pragma unroll
+            for (int i = 0; i < PW; ++i) acc[i] = __fma_rn(hp[i][j], wp[i][j * M + mm[i]], acc[i]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int i = 0; i < PW; ++i) acc[i] = __dadd_rn(acc[i], __shfl_xor_sync(0xffffffffu, acc[i], off));
+        }
+        if (lane < PW && pb + lane < 3 * npair) {
+            double v = acc[0];
+#pragma unroll
+            for (int i = 1; i < PW; ++i)
+                if (lane == i) v = acc[i];
+            const int id = pb + lane, set = id / npair, pair = id % npair;
+            const double* bb = sb2 + (set == 1 ? M : 0);
+            (set == 0 ? q2 : set == 1 ? q2t : q)[pair] = __dadd_rn(v, bb[pair % M]);
+        }
     }
     __syncthreads();
 }
@@ -356,6 +425,24 @@ __device__ __forceinline__ void apply_elem(const ApplyParams& p, const AdamCoef&
     if (a.sync) p.target[k] = w;
 }
 
+// apply_elem with w, m, v already loaded (the fused update prefetches them)
+__device__ __forceinline__ void apply_elem_pre(const ApplyParams& p, const AdamCoef& a, int k, double gk, double w,
+                                               double mk0, double vk0) {
+    if (p.adam) {
+        double mk = __dadd_rn(__dmul_rn(mk0, p.beta1), __dmul_rn(1.0 - p.beta1, gk));
+        double vk = __dadd_rn(__dmul_rn(vk0, p.beta2), __dmul_rn(__dmul_rn(1.0 - p.beta2, gk), gk));
+        p.m[k] = mk;
+        p.v[k] = vk;
+        const double num = __dmul_rn(p.lr, __ddiv_rn(mk, a.bc0));
+        const double den = __dadd_rn(__dsqrt_rn(__ddiv_rn(vk, a.bc1)), p.eps);
+        w = __dsub_rn(w, __ddiv_rn(num, den));
+    } else {
+        w = __dsub_rn(w, __dmul_rn(p.lr, gk));
+    }
+    p.params[k] = w;
+    if (a.sync) p.target[k] = w;
+}
+
 __device__ __forceinline__ void apply_finish(const ApplyParams& p) {
     p.counters[0] += 1;
     p.counters[1] += 1;
@@ -365,6 +452,28 @@ __device__ __forceinline__ void apply_finish(const ApplyParams& p) {
 
 __device__ __forceinline__ bool update_gated(const ApplyParams& p) {
     return p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size);
+}
+
+// Tile partial sums are stored hidden-unit-major: position j (D + 1 + M) + r holds
+// hidden unit j's r-th parameter (r < D: W1[r][j]; r == D: b1[j]; else W2[j][r - D - 1]),
+// then b2 and the loss — so the fused update's slice of hidden units reads one
+// contiguous run.  pos_of / param_of convert between that and the parameter index
+// (w1 | b1 | w2 | b2, the network's flat layout); the loss is nparam in both.
+__device__ __forceinline__ int pos_of(int k, int D, int H, int M) {
+    const int PU = D + 1 + M;
+    if (k < D * H) return (k % H) * PU + k / H;
+    if (k < D * H + H) return (k - D * H) * PU + D;
+    if (k < D * H + H + H * M) {
+        const int i = k - D * H - H;
+        return (i / M) * PU + D + 1 + i % M;
+    }
+    return H * PU + (k - D * H - H - H * M);
+}
+__device__ __forceinline__ int param_of(int q, int D, int H, int M) {
+    const int PU = D + 1 + M;
+    if (q >= H * PU) return D * H + H + H * M + (q - H * PU);
+    const int j = q / PU, r = q % PU;
+    return r < D ? r * H + j : r == D ? D * H + j : D * H + H + j * M + (r - D - 1);
 }
 
 // Everything after the row tiles.  A CTA owns 32 consecutive parameters
@@ -378,6 +487,7 @@ __device__ __forceinline__ bool update_gated(const ApplyParams& p) {
 // all-reduce well defined); the iteration counter still advances.
 struct UpdateParams {
     int32_t n_tiles, B, reduce, apply;
+    int32_t D, H, M;        // network shape (partial layout: pos_of)
     const double* partial;  // [n_tiles][nparam + 1]
     unsigned* done;         // CTA arrival counter (reset by the last CTA)
     ApplyParams ap;
@@ -408,7 +518,7 @@ __global__ void __launch_bounds__(UTHREADS) learner_update_kernel(const UpdatePa
         double s = 0.0;
         if (k <= p.nparam) {
             const size_t ld = (size_t)p.nparam + 1;
-            const double* src = u.partial + k;
+            const double* src = u.partial + pos_of(k, u.D, u.H, u.M);
 #pragma unroll 8
             for (int t = t0; t < t1; ++t) s = __dadd_rn(s, __ldcg(src + (size_t)t * ld));
         }
@@ -498,7 +608,7 @@ __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateP
         const int t0 = warp * per, t1 = min(u.n_tiles, t0 + per);
         double sum = 0.0;
         if (k <= p.nparam) {
-            const double* src = u.partial + k;
+            const double* src = u.partial + pos_of(k, u.D, u.H, u.M);
             const size_t pld = (size_t)p.nparam + 1;
 #pragma unroll 8
             for (int t = t0; t < t1; ++t) sum = __dadd_rn(sum, __ldcg(src + (size_t)t * pld));
@@ -564,30 +674,193 @@ __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateP
     }
 }
 
+// ------------------------------------------- fused update (learner_partial_kernel tail)
+// The TD/Huber backward and the optimizer step in ONE launch: every tile CTA takes a
+// ticket after writing its partial sums; the last TAIL_CTAS to arrive (all other tiles
+// have arrived or are running, so waiting is safe at any grid size) wait for the
+// remaining tiles, then each reduces the partials of one slice of hidden units — w1[:, j],
+// b1[j], w2[j, :] for j in the slice (slice 0 also b2 and the loss) — with exactly
+// learner_update_kernel's fixed tree (8 tile slices summed in tile order, then in slice
+// order), applies Adam / SGD (apply_elem) and repacks those units' entries of the env
+// step's weight layout (QLayout, stage_qnet's values).  The last slice to finish advances
+// the counters (apply_finish).  Bit-identical to partial + learner_update_kernel.
+constexpr int TAIL_CTAS = 64;
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* a) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// partial-sum position (pos_of) of item i of a slice of hidden units [j0, j0 + nj):
+// the slice's contiguous run, then (slice 0) b2 and the loss; -1 past the end
+__device__ __forceinline__ int tail_pos(int i, int j0, int nj, int D, int H, int M, bool extras) {
+    const int PU = D + 1 + M;
+    if (i < nj * PU) return j0 * PU + i;
+    i -= nj * PU;
+    if (extras && i <= M) return H * PU + i;  // b2[i], i == M: the loss
+    return -1;
+}
+
+__device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int nparam) {
+    __shared__ unsigned long long rank_sh;
+    __shared__ double part[2][UTHREADS / 32][32];
+    __syncthreads();  // every thread's partial sums are written
+    if (threadIdx.x == 0) {
+        __threadfence();
+        rank_sh = atomicAdd(p.tick, 1ull);
+    }
+    __syncthreads();
+    LT_T(4)
+    const unsigned long long nt = gridDim.x, v = rank_sh;
+    const int NS = (int)(nt < TAIL_CTAS ? nt : TAIL_CTAS);
+    const unsigned long long rank = v % nt;
+    if (rank < nt - NS) return;
+    const int slice = (int)(rank - (nt - NS));
+    const AdamCoef a = adam_coef(ap);  // (overlaps the wait)
+    if (threadIdx.x == 0) {
+        const unsigned long long target = (v / nt + 1) * nt;
+        while (ld_acquire_gpu(p.tick) < target) __nanosleep(32);
+    }
+    __syncthreads();
+    LT_T(5)
+    const int D = p.D, H = p.H, M = p.M;
+    const int U = (H + NS - 1) / NS;
+    const int j0 = slice * U, nj = j0 < H ? min(U, H - j0) : 0;
+    const bool extras = slice == 0;
+    const int n_items = nj * (D + 1 + M) + (extras ? M + 1 : 0);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    constexpr int NSUB = UTHREADS / 32;
+    const int n_tiles = (int)nt;
+    const int per = (n_tiles + NSUB - 1) / NSUB;
+    const int t0 = w * per, t1 = min(n_tiles, t0 + per);
+    const size_t ld = (size_t)nparam + 1;
+    for (int c0 = 0; c0 < n_items; c0 += 64) {  // two rounds of 32 items, loads of both in flight
+        // the optimizer state of this thread's item (threads < 64), in flight with the sums
+        const int qme = threadIdx.x < 64 ? tail_pos(c0 + threadIdx.x, j0, nj, D, H, M, extras) : -1;
+        const int kme = qme >= 0 ? param_of(qme, D, H, M) : -1;
+        double wme = 0.0, mme = 0.0, vme = 0.0;
+        if (kme >= 0 && kme < nparam) {
+            wme = ap.params[kme];
+            if (ap.adam) {
+                mme = ap.m[kme];
+                vme = ap.v[kme];
+            }
+        }
+        double sum[2] = {0.0, 0.0};
+        int k2[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) k2[r] = tail_pos(c0 + r * 32 + lane, j0, nj, D, H, M, extras);
+        for (int tb = t0; tb < t1; tb += 16) {  // 16 tiles' loads in flight, then the in-order sum
+            double x[2][16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    x[r][i] = (tb + i < t1 && k2[r] >= 0) ? __ldcg(p.partial + (size_t)(tb + i) * ld + k2[r]) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                    if (tb + i < t1) sum[r] = __dadd_rn(sum[r], x[r][i]);
+        }
+        LT_T(8)
+        part[0][w][lane] = sum[0];
+        part[1][w][lane] = sum[1];
+        __syncthreads();
+        LT_T(9)
+        if (kme >= 0) {
+            const int r = threadIdx.x >> 5;
+            double g = part[r][0][lane];
+#pragma unroll
+            for (int q = 1; q < NSUB; ++q) g = __dadd_rn(g, part[r][q][lane]);
+            if (kme < nparam) {
+                ap.grad[kme] = g;
+                apply_elem_pre(ap, a, kme, g, wme, mme, vme);
+            } else {
+                *ap.loss = __ddiv_rn(g, (double)p.B);
+            }
+        }
+        LT_T(10)
+        __syncthreads();
+    }
+    LT_T(6)
+    // the env step's packed weights for this slice's hidden units (stage_qnet's values):
+    // task rows W1[t][j] + b1[j], pairs / odd entries W1[T + v][j] (v <= M) and W2[j][v - M - 1]
+    if (p.qpack) {
+        const int T = p.T, NV = 2 * M + 1, NP = M;
+        const double* w1 = ap.params;
+        const double* b1 = ap.params + D * H;
+        const double* w2 = ap.params + D * H + H;
+        for (int i = threadIdx.x; i < nj * (T + NV); i += blockDim.x) {
+            const int u = i / (T + NV), r = i % (T + NV), j = j0 + u;
+            if (r < T) {
+                p.qpack[(size_t)r * H + j] = __dadd_rn(w1[(size_t)r * H + j], b1[j]);
+            } else {
+                const int vv = r - T;
+                const double x = vv <= M ? w1[(size_t)(T + vv) * H + j] : w2[(size_t)j * M + (vv - M - 1)];
+                double* pairs = p.qpack + (size_t)T * H;
+                if (vv < 2 * NP) pairs[((size_t)(vv >> 1) * H + j) * 2 + (vv & 1)] = x;
+                else pairs[(size_t)2 * NP * H + j] = x;
+            }
+        }
+        if (extras && threadIdx.x < M) p.qpack[(size_t)(T + NV) * H + threadIdx.x] = ap.params[D * H + H + H * M + threadIdx.x];
+    }
+    __syncthreads();
+    LT_T(7)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.tick + 1, 1ull) % (unsigned long long)NS == (unsigned long long)(NS - 1)) {
+            __threadfence();
+            apply_finish(ap);
+            if (ap.advance) ap.counters[3] += 1;
+        }
+    }
+}
+
 template <int DM>
-__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p) {
+__global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p, const ApplyParams ap) {
     pdl_wait();     // the previous one has completed and its writes are visible
+    LT_T(0)
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
     double* xs = lsm;                    // [LROWS][D]
     double* xs2 = xs + LROWS * D;        // [LROWS][D]
     double* hh = xs2 + LROWS * D;        // [LROWS][H]  online h(s)
-    double* ht = hh + LROWS * H;         // [LROWS][H]  scratch h(s')
-    double* q = ht + LROWS * H;          // [LROWS][M]
+    double* ht = hh + LROWS * H;         // [LROWS][H]  online h(s')
+    double* ht2 = ht + LROWS * H;        // [LROWS][H]  target h(s')
+    double* q = ht2 + LROWS * H;         // [LROWS][M]
     double* q2 = q + LROWS * M;          // [LROWS][M]
     double* q2t = q2 + LROWS * M;        // [LROWS][M]
     double* g = q2t + LROWS * M;         // [LROWS][M]  dL/dq
     double* rw = g + LROWS * M;          // [LROWS]
     double* cc = rw + LROWS;             // [LROWS]
     double* lrow = cc + LROWS;           // [LROWS] per-row loss
-    int* act = reinterpret_cast<int*>(lrow + LROWS);  // [LROWS]
+    double* sw2 = lrow + LROWS;          // [2][H][M] W2 online, target
+    double* sb2 = sw2 + 2 * H * M;       // [2][M]    b2 online, target
+    int* act = reinterpret_cast<int*>(sb2 + 2 * M);  // [LROWS]
     const int row0 = blockIdx.x * LROWS;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) return;  // warm-up: no update
+    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) {  // warm-up: no update
+        // (fused update: the iteration still advances; nothing in this launch reads it)
+        if (p.tail && ap.advance && blockIdx.x == 0 && threadIdx.x == 0) ap.counters[3] += 1;
+        return;
+    }
     const uint64_t counter = p.iter_dev ? (uint64_t)(*p.iter_dev) * (uint64_t)p.ups + (uint64_t)p.uidx
                                         : p.counter;
 
+    // ---- the weights the forwards read (independent of the batch: in flight during the gather)
+    double wo[DM], wt[DM], bo = 0.0, bt = 0.0;
+    if ((int)threadIdx.x < H) load_w1_col<DM>(p.w1, p.b1, p.tw1, p.tb1, D, H, threadIdx.x, wo, wt, bo, bt);
+    for (int k = threadIdx.x; k < H * M; k += blockDim.x) {
+        sw2[k] = p.w2[k];
+        sw2[H * M + k] = p.tw2[k];
+    }
+    if ((int)threadIdx.x < M) {
+        sb2[threadIdx.x] = p.b2[threadIdx.x];
+        sb2[M + threadIdx.x] = p.tb2[threadIdx.x];
+    }
     // ---- gather the batch rows (ReplayBuffer.sample: rng.integers(0, size, B))
     for (int k = threadIdx.x; k < LROWS; k += blockDim.x) {
         const int b = row0 + k;
@@ -608,10 +881,10 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         }
     }
     __syncthreads();
+    LT_T(1)
     // ---- Double-Q targets (trainer.py:240-243)
-    forward_rows<DM>(xs2, D, H, M, p.w1, p.b1, p.w2, p.b2, ht, q2);
-    forward_rows<DM>(xs2, D, H, M, p.tw1, p.tb1, p.tw2, p.tb2, ht, q2t);
-    forward_rows<DM>(xs, D, H, M, p.w1, p.b1, p.w2, p.b2, hh, q);
+    forward3_rows<DM>(xs2, xs, D, H, M, p.w1, p.b1, p.tw1, p.tb1, wo, wt, bo, bt, sw2, sb2, ht, ht2, hh, q2,
+                      q2t, q);
     for (int k = threadIdx.x; k < LROWS; k += blockDim.x) {
         const bool valid = row0 + k < p.B;
         int best = 0;
@@ -637,13 +910,14 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         for (int m = 0; m < M; ++m) g[k * M + m] = (valid && m == act[k]) ? dq : 0.0;
     }
     __syncthreads();
+    LT_T(2)
     // ---- backward over this tile's rows (trainer.py:256-263)
     for (int j = threadIdx.x; j < H; j += blockDim.x) {
         double dw2[BE_MAX_TIERS], db1 = 0.0, dw1[DM], w2j[BE_MAX_TIERS];
 #pragma unroll
         for (int m = 0; m < BE_MAX_TIERS; ++m) {
             dw2[m] = 0.0;
-            w2j[m] = m < M ? p.w2[j * M + m] : 0.0;
+            w2j[m] = m < M ? sw2[j * M + m] : 0.0;
         }
 #pragma unroll
         for (int d = 0; d < DM; ++d) dw1[d] = 0.0;
@@ -665,24 +939,27 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
             for (int d = 0; d < DM; ++d)
                 if (d < D) dw1[d] = __fma_rn(xs[row * D + d], dh, dw1[d]);
         }
+        double* oj = out + j * (D + 1 + M);  // hidden-unit-major (pos_of)
 #pragma unroll
         for (int d = 0; d < DM; ++d)
-            if (d < D) out[d * H + j] = dw1[d];
-        out[D * H + j] = db1;
+            if (d < D) oj[d] = dw1[d];
+        oj[D] = db1;
 #pragma unroll
         for (int m = 0; m < BE_MAX_TIERS; ++m)
-            if (m < M) out[D * H + H + j * M + m] = dw2[m];
+            if (m < M) oj[D + 1 + m] = dw2[m];
     }
     if (threadIdx.x < M) {
         double s = 0.0;
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, g[row * M + threadIdx.x]);
-        out[D * H + H + H * M + threadIdx.x] = s;
+        out[H * (D + 1 + M) + threadIdx.x] = s;
     }
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, lrow[row]);
         out[nparam] = s;
     }
+    LT_T(3)
+    if (p.tail) learner_tail(p, ap, nparam);
     pdl_trigger();
 }
 
@@ -722,6 +999,7 @@ struct be_learner {
     unsigned long long* scan;  // commit look-back state [(E + 7) / 8]
     unsigned* ticket;          // commit ticket / epoch; [2] the fused step+commit's scan epoch
     unsigned long long* scan16;  // fused step+commit look-back state [(E + 15) / 16]
+    unsigned long long* tick;    // fused learner update tickets (learner_tail)
     // peer exchange (phase 4): one allocation = [2][nparam + 2] doubles + the epoch flag
     void* xmem;
     int32_t x_world, x_rank;
@@ -741,7 +1019,7 @@ static void learner_free(be_learner* L) {
                     L->rs, L->rs2, L->rr, L->rc, L->ra, L->ring_state, L->px, L->pa, L->pflags,
                     L->preward, L->low, L->status, L->wl_state,
                     L->it_arrival, L->it_task, L->it_rate, L->done, L->gate, L->scan, L->ticket,
-                    L->tc_img, L->tc_stats, L->crange, L->scan16};
+                    L->tc_img, L->tc_stats, L->crange, L->scan16, L->tick};
     for (void* p : ptrs) cudaFree(p);
     for (int r = 0; r < XMAX_RANKS; ++r)
         if (L->x_opened[r]) cudaIpcCloseMemHandle(L->x_opened[r]);
@@ -793,7 +1071,8 @@ int32_t be_learner_create(const be_learner_cfg* c, int32_t device, be_learner** 
         {(void**)&L->wl_state, E * 3 * 8}, {(void**)&L->it_arrival, E * 8},
         {(void**)&L->it_task, E}, {(void**)&L->it_rate, E * 8}, {(void**)&L->done, 64}, {(void**)&L->gate, 64},
         {(void**)&L->scan, ((E + CENVS - 1) / CENVS) * 8}, {(void**)&L->ticket, 64},
-        {(void**)&L->crange, E * 3 * 8}, {(void**)&L->scan16, ((E + 15) / 16) * 8}};
+        {(void**)&L->crange, E * 3 * 8}, {(void**)&L->scan16, ((E + 15) / 16) * 8},
+        {(void**)&L->tick, 64}};
     for (auto& a : allocs) {
         e = cudaMalloc(a.p, a.n);
         if (e != cudaSuccess) {
@@ -946,6 +1225,9 @@ static int launch_update(be_learner* L, int reduce, int apply, ApplyParams ap, c
     UpdateParams u{};
     u.n_tiles = L->n_tiles;
     u.B = L->cfg.batch;
+    u.D = L->D;
+    u.H = L->cfg.hidden;
+    u.M = L->cfg.n_tiers;
     u.reduce = reduce;
     u.apply = apply;
     u.partial = L->partial;
@@ -961,6 +1243,9 @@ static int launch_xupdate(be_learner* L, int32_t advance, cudaStream_t st) {
     UpdateParams u{};
     u.n_tiles = L->n_tiles;
     u.B = L->cfg.batch;
+    u.D = L->D;
+    u.H = L->cfg.hidden;
+    u.M = L->cfg.n_tiers;
     u.reduce = 1;
     u.apply = 1;
     u.partial = L->partial;
@@ -987,7 +1272,8 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
                                  uint64_t counter, int64_t* sample_idx, cudaStream_t st,
                                  const int64_t* iter_dev = nullptr, int32_t ups = 1, int32_t uidx = 0,
                                  int32_t fused = 0, int32_t advance = 0,
-                                 const int64_t* gate = nullptr, int32_t partials_only = 0) {
+                                 const int64_t* gate = nullptr, int32_t partials_only = 0,
+                                 int32_t tail = 0, double* qpack = nullptr) {
     const be_learner_cfg& cf = L->cfg;
     if (B != cf.batch) return set_error(BE_EINVAL, "batch size differs from the learner config");
     LearnParams p{};
@@ -1023,16 +1309,25 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     p.ups = ups;
     p.uidx = uidx;
     p.gate = gate;
-    const size_t smem = sizeof(double) * (2 * LROWS * D + 2 * LROWS * H + 4 * LROWS * M + 3 * LROWS) +
+    const size_t smem = sizeof(double) * (2 * LROWS * D + 3 * LROWS * H + 4 * LROWS * M + 3 * LROWS + 2 * H * M + 2 * M) +
                         sizeof(int) * LROWS;
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "hidden too large for the learner tile");
-    if (D <= 8) learner_partial_kernel<8><<<L->n_tiles, LTHREADS, smem, st>>>(p);
-    else if (D <= 16) learner_partial_kernel<16><<<L->n_tiles, LTHREADS, smem, st>>>(p);
-    else learner_partial_kernel<32><<<L->n_tiles, LTHREADS, smem, st>>>(p);
+    ApplyParams ap{};
+    if (tail) {  // backward + optimizer in this one launch (learner_tail)
+        ap = apply_params(L, sampling ? 0 : 1, advance);
+        ap.gate = gate;
+        p.tail = 1;
+        p.tick = L->tick;
+        p.qpack = qpack;
+        p.T = cf.n_tasks;
+    }
+    if (D <= 8) learner_partial_kernel<8><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
+    else if (D <= 16) learner_partial_kernel<16><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
+    else learner_partial_kernel<32><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
     // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "learner launch");
-    if (partials_only) return BE_OK;
+    if (partials_only || tail) return BE_OK;
     return launch_update(L, 1, fused, apply_params(L, sampling ? 0 : 1, fused ? advance : 0), gate, st);
 }
 
@@ -1227,7 +1522,8 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
     if (c->phase == 0) {
         for (int u = 0; u < ups; ++u) {
             rc = learner_backward_impl(L, nullptr, nullptr, nullptr, nullptr, nullptr, cf.batch,
-                                       c->sample_seed, 0, nullptr, st, it, ups, u, 1, u == ups - 1);
+                                       c->sample_seed, 0, nullptr, st, it, ups, u, 1, u == ups - 1, nullptr, 0,
+                                       /*tail=*/1, env->d_qpack);
             if (rc) return rc;
         }
         if (ups == 0) {  // no learner: still advance the iteration
@@ -1281,3 +1577,9 @@ int32_t be_learner_check(be_learner* L, void* stream) {
 }
 
 }  // extern "C"
+
+#ifdef BE_LT_TIMING
+extern "C" int be_debug_lt_times(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, be::g_lt_t, (size_t)n * sizeof(unsigned long long));
+}
+#endif

@@ -102,14 +102,20 @@ struct StepParams {
 
 // Shared state of one env_step_commit_kernel CTA round.
 constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
-constexpr int SC_PASS = 256;  // request ids of an env's completed range per list pass
+#ifndef BE_CW
+#define BE_CW 4
+#endif
+constexpr int SC_LIST = 4096;  // block-wide transition list (ring-slot order); overflow: per env
 struct CommitShared {
     long long cursor, agg, excl;
     long long pre[SC_ENVS];  // exclusive prefix of the counts within the block
     int cnt[SC_ENVS];
     unsigned long long ep;   // scan epoch << 40
     unsigned long long wmax;
-    uint32_t list[SC_ENVS][SC_PASS];  // pending slots of an env's committable transitions, id order
+    // the block's committable transitions in ring-slot order (env order, then request-id
+    // order): pending slot and env of entry i, whose ring slot is the block's base + i
+    uint32_t sj[SC_LIST];
+    uint8_t le[SC_LIST];
 };
 
 // What one env's step hands the fused commit: the id range this step's advance
@@ -124,78 +130,92 @@ struct StepOut {
     bool live;
 };
 
-// One pass of an env's completed id range (ids [b0, b0 + SC_PASS) of it, 16 per lane,
-// independent flag loads): the committable ones (reward written: flag 0x40) -> their
-// pending slots into `list` in id order.  Returns how many (group-uniform).
-template <bool FIRST>
-__device__ __forceinline__ int commit_list_pass(const StepParams& p, uint32_t* list, int e, int P, int64_t r0,
-                                                int64_t b0, int64_t L, int gl, unsigned gmask) {
-    const int64_t sbase = (r0 + b0 + gl * 16) % P;
-    unsigned bits = 0;
+// An env's committable transitions into the block list: its completed id range
+// [jlo, jlo + L) is scanned 256 ids per pass (16 per lane, independent flag loads);
+// the ready ones (reward written: flag 0x40) take list entries base, base + 1, ... in
+// id order.  Entries past SC_LIST are left to commit_copy_overflow.  Group-wide.
+__device__ __forceinline__ void commit_list(const StepParams& p, CommitShared& cs, int e, int le, int P, int64_t jlo,
+                                            int64_t L, long long base, int gl, unsigned gmask) {
+    const int64_t r0 = jlo % P;
+    for (int64_t b0 = 0; b0 < L; b0 += 256) {
+        const int64_t sbase = (r0 + b0 + gl * 16) % P;
+        unsigned bits = 0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        int64_t sj = sbase + k;
-        if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
-        if (b0 + gl * 16 + k < L && (p.rec.flags[(int64_t)e * P + sj] & 0x40)) bits |= 1u << k;
-    }
-    const int cnt = __popc(bits);
-    int inc = cnt;
+        for (int k = 0; k < 16; ++k) {
+            int64_t sj = sbase + k;
+            if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
+            if (b0 + gl * 16 + k < L && (p.rec.flags[(int64_t)e * P + sj] & 0x40)) bits |= 1u << k;
+        }
+        const int cnt = __popc(bits);
+        int inc = cnt;
 #pragma unroll
-    for (int off = 1; off < 16; off <<= 1) {
-        const int v = __shfl_up_sync(gmask, inc, off, 16);
-        if (gl >= off) inc += v;
+        for (int off = 1; off < 16; off <<= 1) {
+            const int v = __shfl_up_sync(gmask, inc, off, 16);
+            if (gl >= off) inc += v;
+        }
+        long long r = base + inc - cnt;
+        while (bits) {
+            int64_t sj = sbase + __ffs(bits) - 1;
+            if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
+            if (r < SC_LIST) {
+                cs.sj[r] = (uint32_t)sj;
+                cs.le[r] = (uint8_t)le;
+            }
+            ++r;
+            bits &= bits - 1;
+        }
+        base += __shfl_sync(gmask, inc, 15, 16);
     }
-    int r = inc - cnt;
-    while (bits) {
-        int64_t sj = sbase + __ffs(bits) - 1;
-        if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
-        list[r++] = (uint32_t)sj;
-        bits &= bits - 1;
-    }
-    __syncwarp(gmask);
-    return __shfl_sync(gmask, inc, 15, 16);
 }
 
-__device__ __forceinline__ int64_t wrap_slot(int64_t s, int64_t cap) {
-    while (s >= cap) s -= cap;
-    return s;
-}
-
-// Transition (x_j, a_j, r_j, x_{j+1}) of pending slot sj: elements [d0, d0 + min(n, W))
-// of the two states, all loads issued before any store (the ring may alias nothing,
-// but the compiler cannot know).
-template <int W>
-__device__ __forceinline__ void commit_load(const StepParams& p, int e, int n, int P, int64_t sj, double (&xa)[W],
-                                            double (&xb)[W], uint8_t& a, double& r, int d0 = 0, int D = -1) {
-    if (D < 0) D = n;
+// One transition (x_j, a_j, r_j, x_{j+1}) of env e, pending slot sj, into ring slot
+// `slot` (ReplayBuffer.push, trainer.py:123-133): every load issued before any store.
+template <int CW>
+__device__ __forceinline__ void commit_copy(const StepParams& p, const StepCommitArgs& c, int e, int D, int P,
+                                            int64_t sj, int64_t slot) {
     const int64_t sj1 = sj + 1 == P ? 0 : sj + 1;
-    const double* pa = p.x_out + (sj * p.E + e) * D + d0;
-    const double* pb = p.x_out + (sj1 * p.E + e) * D + d0;
+    const double* pa = p.x_out + (sj * p.E + e) * D;
+    const double* pb = p.x_out + (sj1 * p.E + e) * D;
+    const uint8_t a = p.action_out[sj * p.E + e];
+    const double r = p.rec.reward[(int64_t)e * P + sj];
+    for (int d0 = 0; d0 < D; d0 += CW) {
+        double xa[CW], xb[CW];
 #pragma unroll
-    for (int k = 0; k < W; ++k)
-        if (k < n) {
-            xa[k] = pa[k];
-            xb[k] = pb[k];
-        }
-    a = p.action_out[sj * p.E + e];
-    r = p.rec.reward[(int64_t)e * P + sj];
+        for (int k = 0; k < CW; ++k)
+            if (d0 + k < D) {
+                xa[k] = pa[d0 + k];
+                xb[k] = pb[d0 + k];
+            }
+#pragma unroll
+        for (int k = 0; k < CW; ++k)
+            if (d0 + k < D) {
+                c.rs[slot * D + d0 + k] = xa[k];
+                c.rs2[slot * D + d0 + k] = xb[k];
+            }
+    }
+    c.ra[slot] = a;
+    c.rr[slot] = r;
+    c.rc[slot] = 1.0;
+    p.rec.flags[(int64_t)e * P + sj] = 0x20;
 }
-template <int W>
-__device__ __forceinline__ void commit_store(const StepParams& p, const StepCommitArgs& c, int e, int n, int P, int64_t sj,
-                                             int64_t slot, const double (&xa)[W], const double (&xb)[W], uint8_t a,
-                                             double r, int d0 = 0, int D = -1, bool scalars = true) {
-    if (D < 0) D = n;
-#pragma unroll
-    for (int k = 0; k < W; ++k)
-        if (k < n) {
-            c.rs[slot * D + d0 + k] = xa[k];
-            c.rs2[slot * D + d0 + k] = xb[k];
+
+// The block list overflowed (more than SC_LIST transitions in one block and step):
+// the owning env group rescans its range and copies its entries at list index >= SC_LIST.
+__device__ __forceinline__ void commit_copy_overflow(const StepParams& p, const StepCommitArgs& c, int e, int D, int P,
+                                                     int64_t jlo, int64_t L, long long base, int64_t s0, int gl,
+                                                     unsigned gmask) {
+    const int64_t r0 = jlo % P;
+    for (int64_t b0 = 0; b0 < L; b0 += 16) {
+        int64_t sj = (r0 + b0 + gl) % P;
+        const bool ready = b0 + gl < L && (p.rec.flags[(int64_t)e * P + sj] & 0x40);
+        const unsigned rb = __ballot_sync(gmask, ready);
+        const long long idx = base + __popc(rb & ((1u << (threadIdx.x & 31)) - 1u));
+        if (ready && idx >= SC_LIST) {
+            int64_t slot = s0 + idx;
+            while (slot >= c.capacity) slot -= c.capacity;
+            commit_copy<4>(p, c, e, D, P, sj, slot);
         }
-    if (scalars) {
-        c.ra[slot] = a;
-        c.rr[slot] = r;
-        c.rc[slot] = 1.0;
-        p.rec.flags[(int64_t)e * P + sj] = 0x20;
+        base += __popc(rb);
     }
 }
 
@@ -328,7 +348,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
 // order within the env, env-id order across envs, exactly commit_fused_kernel's slots.
 
 template <int M>
-__global__ void __launch_bounds__(256) env_step_commit_kernel(const StepParams p) {
+__global__ void __launch_bounds__(256, 2) env_step_commit_kernel(const StepParams p) {
     STEPC_T(0)
     pdl_wait();  // the previous kernel has completed and its writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -361,22 +381,10 @@ __global__ void __launch_bounds__(256) env_step_commit_kernel(const StepParams p
         so.live = live;
         step_env<M, 16>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
         STEPC_T(2)
-        // ---- this env's transitions, part 1 (independent of the cross-block prefix, so
-        // it overlaps warp 0's look-back): the flags of the completed id range, 16 ids
-        // per lane (independent loads) -> the env's committable pending slots in id
-        // order (shared list); the group's first 16 transitions loaded into registers
-        // (lane t holds transition t)
+        // ---- this env's transitions into the block list (independent of the cross-block
+        // prefix, so it overlaps warp 0's look-back)
         const int64_t L = (live && so.jlo <= so.jhi) ? so.jhi - so.jlo + 1 : 0;
-        const int64_t r0 = L ? so.jlo % P : 0;
-        const bool fast = D <= 8;
-        int gtot = L ? commit_list_pass<true>(p, cs.list[le], e, P, r0, 0, L, gl, gmask) : 0;
-        double xa[8], xb[8], rv = 0.0;
-        uint8_t av = 0;
-        int64_t sj0 = 0;
-        if (fast && gl < gtot) {
-            sj0 = cs.list[le][gl];
-            commit_load<8>(p, e, D, P, sj0, xa, xb, av, rv);
-        }
+        if (L) commit_list(p, cs, e, le, P, so.jlo, L, cs.pre[le], gl, gmask);
 #ifndef BE_STEPC_NOLB
         if (warp == 0 && vb > 0) {
 #else
@@ -435,37 +443,22 @@ __global__ void __launch_bounds__(256) env_step_commit_kernel(const StepParams p
         STEPC_T(3)
         __syncthreads();
         STEPC_T(4)
+        // ---- the block's transitions, one per thread: ring slot = block base + list index
+        const long long n_blk = cs.agg;
+        const int64_t s0 = (cs.cursor + cs.excl) % c.capacity;
 #ifndef BE_STEPC_NOWR
-        if (live) {
-#else
-        if (false) {
+        for (long long i = threadIdx.x; i < (n_blk < SC_LIST ? n_blk : SC_LIST); i += blockDim.x) {
+            const int lei = cs.le[i];
+            int64_t slot = s0 + i;
+            while (slot >= c.capacity) slot -= c.capacity;
+            commit_copy<BE_CW>(p, c, vb * SC_ENVS + lei, D, P, cs.sj[i], slot);
+        }
 #endif
-            // ---- part 2: the stores (ReplayBuffer.push, trainer.py:123-133) from the
-            // env's slot base, request-id order; transitions past the first 16 go one
-            // round trip per 16, ids past the first SC_PASS of the range one pass each
-            const int64_t s0 = (cs.cursor + cs.excl + cs.pre[le]) % c.capacity;
-            if (fast && gl < gtot) commit_store<8>(p, c, e, D, P, sj0, wrap_slot(s0 + gl, c.capacity), xa, xb, av, rv);
-            int64_t total = 0;
-            for (int64_t b0 = 0; b0 < L; b0 += SC_PASS) {
-                if (b0 > 0) {
-                    __syncwarp(gmask);  // the list is rewritten
-                    gtot = commit_list_pass<false>(p, cs.list[le], e, P, r0, b0, L, gl, gmask);
-                }
-                for (int t = (b0 == 0 && fast) ? gl + 16 : gl; t < gtot; t += 16) {
-                    const int64_t sj = cs.list[le][t];
-                    const int64_t slot = wrap_slot(s0 + total + t, c.capacity);
-                    for (int d0 = 0; d0 < D; d0 += 8) {  // D > 8: several element chunks
-                        double ya[8], yb[8], r;
-                        uint8_t a;
-                        commit_load<8>(p, e, D - d0, P, sj, ya, yb, a, r, d0, D);
-                        commit_store<8>(p, c, e, D - d0, P, sj, slot, ya, yb, a, r, d0, D, d0 == 0);
-                    }
-                }
-                total += gtot;
-            }
+        if (live) {
+            if (n_blk > SC_LIST && L) commit_copy_overflow(p, c, e, D, P, so.jlo, L, cs.pre[le], s0, gl, gmask);
 #ifdef BE_STEPC_TIMING
             if (gl == 0 && blockIdx.x < 1024) {
-                atomicMax(&g_stepc_t[blockIdx.x * 8 + 7], ((unsigned long long)L << 32) | (unsigned)gtot);
+                atomicMax(&g_stepc_t[blockIdx.x * 8 + 7], ((unsigned long long)L << 32) | (unsigned)cs.cnt[le]);
             }
 #endif
             if (gl == 0) {
