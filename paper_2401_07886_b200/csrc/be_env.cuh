@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(256) stage_qpack_kernel(const double* w1, cons
 }
 constexpr int QPACK_CTAS = 16;
 
-template <int M, int LPE>
+template <int M, int LPE, int UNROLL = 8>
 __device__ __forceinline__ void qnet_group(const double* __restrict__ sw, int T, int H, int task,
                                            const double (&xt)[M], double xr, double (&q)[M]) {
     constexpr int NV = QLayout<M>::NV, NP = QLayout<M>::NP;
@@ -452,7 +452,7 @@ __device__ __forceinline__ void qnet_group(const double* __restrict__ sw, int T,
     double a[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) a[m] = 0.0;
-#pragma unroll 8
+#pragma unroll UNROLL
     for (int j = g; j < H; j += LPE) {
         double v[NV];
 #pragma unroll

@@ -114,6 +114,8 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         int phase = 0, float* tc_img = nullptr, int64_t* crange = nullptr,
                         const StepCommitArgs* commit = nullptr);
 bool env_step_commit_supported(const be_env* env);
+// pack W into env->d_qpack (QLayout) for the env step's fp64 decision
+int launch_stage_qpack(be_env* env, const be_qweights* W, cudaStream_t st);
 // the training step with the decision on the tensor cores (tc_img != NULL above):
 // shared-memory size and the kernel attribute (set before any graph capture)
 size_t step_tc_smem_bytes(int H);

@@ -25,7 +25,11 @@ struct WorkloadArgs {
     const int64_t* step_dev;  // be_train_iteration: iteration index on device (else `step`)
 };
 
-__device__ __forceinline__ void train_workload_env(const WorkloadArgs& w, int e) {
+// Next arrival of env e: (arrival time, task, regime rate); `store` = write the state
+// and the outputs (the fused training step computes it on every lane of the env's
+// group and lets one lane store).
+__device__ __forceinline__ void train_workload_next(const WorkloadArgs& w, int e, bool store, double& t_out,
+                                                    int& task_out, double& rate_out) {
     const uint64_t step = w.step_dev ? (uint64_t)*w.step_dev : w.step;
     double t = w.state[3 * e], rate = w.state[3 * e + 1], left = w.state[3 * e + 2];
     P4 a = philox4x32_10(step * 2, (uint64_t)e, w.seed);
@@ -41,12 +45,24 @@ __device__ __forceinline__ void train_workload_env(const WorkloadArgs& w, int e)
     P4 b = philox4x32_10(step * 2 + 1, (uint64_t)e, w.seed);
     const double gap = -log1p(-u01(b.x[0], b.x[1])) * (1000.0 / rate);
     t = t + gap;
-    w.state[3 * e] = t;
-    w.state[3 * e + 1] = rate;
-    w.state[3 * e + 2] = left;
-    w.arrival[e] = t;
-    w.task[e] = (uint8_t)below(b.x[2], (uint32_t)w.n_tasks);
-    w.rate_out[e] = rate;
+    const int task = (int)below(b.x[2], (uint32_t)w.n_tasks);
+    if (store) {
+        w.state[3 * e] = t;
+        w.state[3 * e + 1] = rate;
+        w.state[3 * e + 2] = left;
+        w.arrival[e] = t;
+        w.task[e] = (uint8_t)task;
+        w.rate_out[e] = rate;
+    }
+    t_out = t;
+    task_out = task;
+    rate_out = rate;
+}
+
+__device__ __forceinline__ void train_workload_env(const WorkloadArgs& w, int e) {
+    double t, rate;
+    int task;
+    train_workload_next(w, e, true, t, task, rate);
 }
 
 }  // namespace be

@@ -1000,6 +1000,9 @@ struct be_learner {
     unsigned* ticket;          // commit ticket / epoch; [2] the fused step+commit's scan epoch
     unsigned long long* scan16;  // fused step+commit look-back state [(E + 15) / 16]
     unsigned long long* tick;    // fused learner update tickets (learner_tail)
+    // the env whose packed step weights (d_qpack) hold the current parameters: the fused
+    // update (learner_tail) repacks them, every other parameter write clears this
+    const be_env* qpack_env;
     // peer exchange (phase 4): one allocation = [2][nparam + 2] doubles + the epoch flag
     void* xmem;
     int32_t x_world, x_rank;
@@ -1132,6 +1135,7 @@ int32_t be_learner_set_params(be_learner* L, const double* w1, const double* b1,
     cudaMemsetAsync(L->v, 0, (size_t)L->nparam * 8, st);
     cudaMemsetAsync(L->counters, 0, 64, st);
     cudaMemsetAsync(L->xmem, 0, xmem_bytes(L), st);  // peer-exchange epochs restart with the counters
+    L->qpack_env = nullptr;
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "set_params");
 }
@@ -1235,6 +1239,7 @@ static int launch_update(be_learner* L, int reduce, int apply, ApplyParams ap, c
     ap.gate = gate;
     u.ap = ap;
     const int blocks = (reduce || apply) ? (L->nparam + 32) / 32 : 1;  // 32 parameters (+ the loss) per CTA
+    if (apply) L->qpack_env = nullptr;
     cudaError_t e = launch_pdl(learner_update_kernel, dim3(blocks), dim3(UTHREADS), 0, st, u);
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "learner update launch");
 }
@@ -1251,6 +1256,7 @@ static int launch_xupdate(be_learner* L, int32_t advance, cudaStream_t st) {
     u.partial = L->partial;
     u.done = L->done;
     u.ap = apply_params(L, 0, advance);
+    L->qpack_env = nullptr;
     XParams x{};
     x.world = L->x_world;
     x.rank = L->x_rank;
@@ -1497,7 +1503,14 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2,
                                      nullptr, L->crange);
         } else if (env_step_commit_supported(env)) {
-            // the replay commit fused into the env step: one launch, no flag scan
+            // the replay commit fused into the env step: one launch, no flag scan; the
+            // step generates the arrivals itself and reads the weights the learner's
+            // fused update packed (packed here once if anything else wrote them)
+            if (L->qpack_env != env) {
+                rc = launch_stage_qpack(env, &W, st);
+                if (rc) return rc;
+                L->qpack_env = env;
+            }
             StepCommitArgs cm{cf.replay_capacity, L->rs, L->rs2, L->rr, L->rc, L->ra, L->low,
                               L->ring_state, L->status, L->scan16, L->ticket + 2};
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,

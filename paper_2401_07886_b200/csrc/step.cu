@@ -98,12 +98,21 @@ struct StepParams {
     // fused replay commit (env_step_commit_kernel; fuse_commit = 1)
     StepCommitArgs cm;
     int32_t fuse_commit;
+    // env_step_commit_kernel generates the iteration's arrivals itself (TrainingWorkload)
+    int32_t gen_workload;
+    WorkloadArgs wl;
 };
 
 // Shared state of one env_step_commit_kernel CTA round.
 constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
 #ifndef BE_CW
-#define BE_CW 4
+#define BE_CW 2  // doubles per load batch of a transition copy (register-bound: 2 spills least)
+#endif
+#ifndef BE_STEPC_MINB
+#define BE_STEPC_MINB 2  // 2 CTAs per SM: one resident wave of 296 CTAs (4736 envs)
+#endif
+#ifndef BE_STEPC_QU
+#define BE_STEPC_QU 4  // Q-forward unroll of the fused training step (8: register-bound, slower)
 #endif
 constexpr int SC_LIST = 4096;  // block-wide transition list (ring-slot order); overflow: per env
 struct CommitShared {
@@ -128,6 +137,9 @@ struct StepOut {
     CommitShared* cs;
     int vb, le;
     bool live;
+    bool has_wl;  // arrival / task / true rate below instead of p.arrival / p.task / p.true_rate
+    int task;
+    double U, rate;
 };
 
 // An env's committable transitions into the block list: its completed id range
@@ -308,7 +320,7 @@ struct TcStepCtx {
     bool img_ready;
 };
 
-template <int M, int LPE, bool TCQ = false>
+template <int M, int LPE, bool TCQ = false, int QU = 8>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
                                          bool policy, int T, int H, int D, TcStepCtx* tcx = nullptr,
                                          StepOut* so = nullptr);
@@ -348,7 +360,7 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
 // order within the env, env-id order across envs, exactly commit_fused_kernel's slots.
 
 template <int M>
-__global__ void __launch_bounds__(256, 2) env_step_commit_kernel(const StepParams p) {
+__global__ void __launch_bounds__(256, BE_STEPC_MINB) env_step_commit_kernel(const StepParams p) {
     STEPC_T(0)
     pdl_wait();  // the previous kernel has completed and its writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -379,7 +391,12 @@ __global__ void __launch_bounds__(256, 2) env_step_commit_kernel(const StepParam
         so.vb = vb;
         so.le = le;
         so.live = live;
-        step_env<M, 16>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
+        so.has_wl = false;
+        if (p.gen_workload) {  // TrainingWorkload.next_arrival (trainer.py:304-316), lane 0 stores
+            train_workload_next(p.wl, live ? e : p.E - 1, live && gl == 0, so.U, so.task, so.rate);
+            so.has_wl = true;
+        }
+        step_env<M, 16, false, BE_STEPC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
         STEPC_T(2)
         // ---- this env's transitions into the block list (independent of the cross-block
         // prefix, so it overlaps warp 0's look-back)
@@ -741,7 +758,7 @@ void step_tc_prepare(int M, int H) {
 
 // One env per LPE-lane group (all 32 lanes of the warp call it: the group
 // reductions are warp-wide); `live` = false for a padding group past the last env.
-template <int M, int LPE, bool TCQ>
+template <int M, int LPE, bool TCQ, int QU>
 __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, const Score& sc, const double* sw,
                                          bool policy, int T, int H, int D, TcStepCtx* tcx, StepOut* so) {
     const int lane = threadIdx.x & 31;
@@ -805,8 +822,9 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
         }
         return;
     }
-    const double U = p.arrival[e];
-    int task = live ? p.task[e] : 0;
+    const bool wl_in = so != nullptr && so->has_wl;
+    const double U = wl_in ? so->U : p.arrival[e];
+    int task = live ? (wl_in ? so->task : (int)p.task[e]) : 0;
     const bool bad_task = live && task >= T;  // encode raises (policy.py:57-58)
     if (task >= T) task = 0;
     const uint32_t cr_h0 = r.head, cr_idt0 = r.h_idtask;
@@ -842,7 +860,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
     for (int k = 0; k < 5; ++k) est.w[k] = es->w[k];
     est.n = es->n;
     const int64_t id = es->next_id;
-    const double cur = p.true_rate ? p.true_rate[e] : 0.0;
+    const double cur = wl_in ? so->rate : p.true_rate ? p.true_rate[e] : 0.0;
     const double rate = estimator_observe(est, U, p.cfg.estimator_true_rate != 0, cur, p.cfg.prior_rate);
     int obs[M];
 #pragma unroll
@@ -883,7 +901,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
                                          (threadIdx.x >> 5) * 2 + grp, gl);
             if (!explore) tier = dec;
         } else {
-            qnet_group<M, LPE>(sw, T, H, task, xt, xr, q);
+            qnet_group<M, LPE, QU>(sw, T, H, task, xt, xr, q);
             if (!explore) tier = argmax_first<M>(q);
         }
     }
@@ -978,7 +996,8 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
     const bool two = p.R <= 16 && p.cfg.n_tasks + M + 1 <= 16;
     auto kern = two ? env_step_kernel<M, 16> : env_step_kernel<M, 32>;
     float* tc_img = const_cast<float*>(p.tc_img);
-    if (p.qpack && wl) {  // pack the weights (+ the tensor-core image) + the training workload, one launch
+    if (p.fuse_commit && p.gen_workload) {  // the step generates the workload; the learner keeps qpack packed
+    } else if (p.qpack && wl) {  // pack the weights (+ the tensor-core image) + the training workload, one launch
         const int ntc = tc_img ? TCPACK_CTAS : 0;
         cudaError_t e = launch_pdl(prep_kernel<M>, dim3(QPACK_CTAS + ntc + (wl->E + 255) / 256), dim3(256), 0, st,
                                    p.w1, p.b1, p.w2, p.b2, p.cfg.n_tasks, p.H, const_cast<double*>(p.qpack), *wl,
@@ -1125,6 +1144,12 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
         p.cm = *commit;
         p.fuse_commit = 1;
         p.crange = nullptr;
+#ifndef BE_STEPC_PREPWL
+        if (wl) {
+            p.gen_workload = 1;
+            p.wl = *wl;
+        }
+#endif
     }
     p.tc_img = tc_img;
     p.tc_ncols = W->hidden <= 32 ? 32 : W->hidden <= 64 ? 64 : W->hidden <= 128 ? 128 : 256;
@@ -1146,6 +1171,22 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     p.b2 = W->b2;
     p.qpack = phase == 2 ? nullptr : env->d_qpack;  // submit: no weights needed
     return dispatch_step(p, step_smem_bytes(), st, wl);
+}
+
+int launch_stage_qpack(be_env* env, const be_qweights* W, cudaStream_t st) {
+    const int T = env->cfg.n_tasks;
+    cudaError_t e = cudaSuccess;
+    switch (env->cfg.n_tiers) {
+#define BE_QP(MM)                                                                                             \
+    case MM:                                                                                                  \
+        e = launch_pdl(stage_qpack_kernel<MM>, dim3(QPACK_CTAS), dim3(256), 0, st, W->w1, W->b1, W->w2, W->b2, T, \
+                       W->hidden, env->d_qpack);                                                              \
+        break;
+        BE_QP(1) BE_QP(2) BE_QP(3) BE_QP(4) BE_QP(5) BE_QP(6) BE_QP(7) BE_QP(8)
+#undef BE_QP
+        default: return set_error(BE_EINVAL, "n_tiers out of range");
+    }
+    return e == cudaSuccess ? BE_OK : set_cuda_error(e, "stage_qpack launch");
 }
 
 bool env_step_commit_supported(const be_env* env) {
