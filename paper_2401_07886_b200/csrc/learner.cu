@@ -28,18 +28,6 @@
 
 namespace be {
 
-#ifdef BE_LT_TIMING
-__device__ unsigned long long g_lt_t[512 * 16];
-#define LT_T(k)                                                                         \
-    if (threadIdx.x == 0 && blockIdx.x < 512) {                                         \
-        unsigned long long t_;                                                          \
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-        g_lt_t[blockIdx.x * 16 + (k)] = t_;                                             \
-    }
-#else
-#define LT_T(k)
-#endif
-
 constexpr int LROWS = 4;       // rows per learner CTA (B = 512 -> 128 CTAs: latency, not work, bounds an update)
 constexpr int UTHREADS = 256;  // learner_update_kernel: 32 parameters x 8 tile slices per CTA
 constexpr int LTHREADS = 256;  // one thread per hidden unit (looping for H > 256)
@@ -277,6 +265,7 @@ struct LearnParams {
     unsigned long long* tick;  // [0] tile arrivals, [1] slice completions (monotonic)
     double* qpack;             // the env step's packed weights (QLayout), or NULL
     int32_t T;                 // tasks (packing)
+    int32_t stage_out;         // tile partials staged in shared memory, copied out coalesced
 };
 
 __device__ __forceinline__ double relu_d(double x) {
@@ -711,7 +700,6 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
         rank_sh = atomicAdd(p.tick, 1ull);
     }
     __syncthreads();
-    LT_T(4)
     const unsigned long long nt = gridDim.x, v = rank_sh;
     const int NS = (int)(nt < TAIL_CTAS ? nt : TAIL_CTAS);
     const unsigned long long rank = v % nt;
@@ -723,7 +711,6 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
         while (ld_acquire_gpu(p.tick) < target) __nanosleep(32);
     }
     __syncthreads();
-    LT_T(5)
     const int D = p.D, H = p.H, M = p.M;
     const int U = (H + NS - 1) / NS;
     const int j0 = slice * U, nj = j0 < H ? min(U, H - j0) : 0;
@@ -764,11 +751,9 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
                 for (int r = 0; r < 2; ++r)
                     if (tb + i < t1) sum[r] = __dadd_rn(sum[r], x[r][i]);
         }
-        LT_T(8)
         part[0][w][lane] = sum[0];
         part[1][w][lane] = sum[1];
         __syncthreads();
-        LT_T(9)
         if (kme >= 0) {
             const int r = threadIdx.x >> 5;
             double g = part[r][0][lane];
@@ -781,10 +766,8 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
                 *ap.loss = __ddiv_rn(g, (double)p.B);
             }
         }
-        LT_T(10)
         __syncthreads();
     }
-    LT_T(6)
     // the env step's packed weights for this slice's hidden units (stage_qnet's values):
     // task rows W1[t][j] + b1[j], pairs / odd entries W1[T + v][j] (v <= M) and W2[j][v - M - 1]
     if (p.qpack) {
@@ -807,7 +790,6 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
         if (extras && threadIdx.x < M) p.qpack[(size_t)(T + NV) * H + threadIdx.x] = ap.params[D * H + H + H * M + threadIdx.x];
     }
     __syncthreads();
-    LT_T(7)
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(p.tick + 1, 1ull) % (unsigned long long)NS == (unsigned long long)(NS - 1)) {
@@ -820,8 +802,6 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
 
 template <int DM>
 __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnParams p, const ApplyParams ap) {
-    pdl_wait();     // the previous one has completed and its writes are visible
-    LT_T(0)
     extern __shared__ __align__(16) double lsm[];
     const int D = p.D, H = p.H, M = p.M;
     double* xs = lsm;                    // [LROWS][D]
@@ -840,17 +820,14 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     double* sb2 = sw2 + 2 * H * M;       // [2][M]    b2 online, target
     int* act = reinterpret_cast<int*>(sb2 + 2 * M);  // [LROWS]
     const int row0 = blockIdx.x * LROWS;
+    const int nparam_ = D * H + H + H * M + M;
+    // the tile's partial sums, staged for one coalesced copy out (when they fit)
+    double* so = p.stage_out ? reinterpret_cast<double*>(act + ((LROWS + 1) & ~1)) : nullptr;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) {  // warm-up: no update
-        // (fused update: the iteration still advances; nothing in this launch reads it)
-        if (p.tail && ap.advance && blockIdx.x == 0 && threadIdx.x == 0) ap.counters[3] += 1;
-        return;
-    }
-    const uint64_t counter = p.iter_dev ? (uint64_t)(*p.iter_dev) * (uint64_t)p.ups + (uint64_t)p.uidx
-                                        : p.counter;
-
-    // ---- the weights the forwards read (independent of the batch: in flight during the gather)
+    // ---- the weights the forwards read (in flight during the batch gather).  Measured:
+    // a programmatic launch behind the env step (this prologue overlapping the step's
+    // tail) is slower — the early CTAs compete with the step's last CTAs
     double wo[DM], wt[DM], bo = 0.0, bt = 0.0;
     if ((int)threadIdx.x < H) load_w1_col<DM>(p.w1, p.b1, p.tw1, p.tb1, D, H, threadIdx.x, wo, wt, bo, bt);
     for (int k = threadIdx.x; k < H * M; k += blockDim.x) {
@@ -861,6 +838,15 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         sb2[threadIdx.x] = p.b2[threadIdx.x];
         sb2[M + threadIdx.x] = p.tb2[threadIdx.x];
     }
+    pdl_wait();  // the previous kernel has completed and its writes are visible
+    if (p.gate ? *p.gate == 0 : (p.sampling && p.ring_state[1] < p.min_size)) {  // warm-up: no update
+        // (fused update: the iteration still advances; nothing in this launch reads it)
+        if (p.tail && ap.advance && blockIdx.x == 0 && threadIdx.x == 0) ap.counters[3] += 1;
+        return;
+    }
+    const uint64_t counter = p.iter_dev ? (uint64_t)(*p.iter_dev) * (uint64_t)p.ups + (uint64_t)p.uidx
+                                        : p.counter;
+
     // ---- gather the batch rows (ReplayBuffer.sample: rng.integers(0, size, B))
     for (int k = threadIdx.x; k < LROWS; k += blockDim.x) {
         const int b = row0 + k;
@@ -881,7 +867,6 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         }
     }
     __syncthreads();
-    LT_T(1)
     // ---- Double-Q targets (trainer.py:240-243)
     forward3_rows<DM>(xs2, xs, D, H, M, p.w1, p.b1, p.tw1, p.tb1, wo, wt, bo, bt, sw2, sb2, ht, ht2, hh, q2,
                       q2t, q);
@@ -910,7 +895,6 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
         for (int m = 0; m < M; ++m) g[k * M + m] = (valid && m == act[k]) ? dq : 0.0;
     }
     __syncthreads();
-    LT_T(2)
     // ---- backward over this tile's rows (trainer.py:256-263)
     for (int j = threadIdx.x; j < H; j += blockDim.x) {
         double dw2[BE_MAX_TIERS], db1 = 0.0, dw1[DM], w2j[BE_MAX_TIERS];
@@ -939,7 +923,7 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
             for (int d = 0; d < DM; ++d)
                 if (d < D) dw1[d] = __fma_rn(xs[row * D + d], dh, dw1[d]);
         }
-        double* oj = out + j * (D + 1 + M);  // hidden-unit-major (pos_of)
+        double* oj = (so ? so : out) + j * (D + 1 + M);  // hidden-unit-major (pos_of)
 #pragma unroll
         for (int d = 0; d < DM; ++d)
             if (d < D) oj[d] = dw1[d];
@@ -951,14 +935,17 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     if (threadIdx.x < M) {
         double s = 0.0;
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, g[row * M + threadIdx.x]);
-        out[H * (D + 1 + M) + threadIdx.x] = s;
+        (so ? so : out)[H * (D + 1 + M) + threadIdx.x] = s;
     }
     if (threadIdx.x == 0) {
         double s = 0.0;
         for (int row = 0; row < LROWS; ++row) s = __dadd_rn(s, lrow[row]);
-        out[nparam] = s;
+        (so ? so : out)[nparam] = s;
     }
-    LT_T(3)
+    if (so) {
+        __syncthreads();
+        for (int i = threadIdx.x; i <= nparam_; i += blockDim.x) out[i] = so[i];
+    }
     if (p.tail) learner_tail(p, ap, nparam);
     pdl_trigger();
 }
@@ -1315,8 +1302,13 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     p.ups = ups;
     p.uidx = uidx;
     p.gate = gate;
-    const size_t smem = sizeof(double) * (2 * LROWS * D + 3 * LROWS * H + 4 * LROWS * M + 3 * LROWS + 2 * H * M + 2 * M) +
-                        sizeof(int) * LROWS;
+    size_t smem = sizeof(double) * (2 * LROWS * D + 3 * LROWS * H + 4 * LROWS * M + 3 * LROWS + 2 * H * M + 2 * M) +
+                  sizeof(int) * ((LROWS + 1) & ~1);
+    const size_t stage = sizeof(double) * ((size_t)L->nparam + 1);
+    if (smem + stage <= 200 * 1024) {
+        p.stage_out = 1;
+        smem += stage;
+    }
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "hidden too large for the learner tile");
     ApplyParams ap{};
     if (tail) {  // backward + optimizer in this one launch (learner_tail)
@@ -1327,9 +1319,8 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
         p.qpack = qpack;
         p.T = cf.n_tasks;
     }
-    if (D <= 8) learner_partial_kernel<8><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
-    else if (D <= 16) learner_partial_kernel<16><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
-    else learner_partial_kernel<32><<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
+    auto kern = D <= 8 ? learner_partial_kernel<8> : D <= 16 ? learner_partial_kernel<16> : learner_partial_kernel<32>;
+    kern<<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
     // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "learner launch");
@@ -1591,8 +1582,3 @@ int32_t be_learner_check(be_learner* L, void* stream) {
 
 }  // extern "C"
 
-#ifdef BE_LT_TIMING
-extern "C" int be_debug_lt_times(unsigned long long* out, int n) {
-    return (int)cudaMemcpyFromSymbol(out, be::g_lt_t, (size_t)n * sizeof(unsigned long long));
-}
-#endif

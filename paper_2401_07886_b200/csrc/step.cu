@@ -105,20 +105,13 @@ struct StepParams {
 
 // Shared state of one env_step_commit_kernel CTA round.
 constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
-#ifndef BE_CW
-#define BE_CW 2  // doubles per load batch of a transition copy (register-bound: 2 spills least)
-#endif
-#ifndef BE_STEPC_MINB
-#define BE_STEPC_MINB 2  // 2 CTAs per SM: one resident wave of 296 CTAs (4736 envs)
-#endif
-#ifndef BE_STEPC_QU
-#define BE_STEPC_QU 4  // Q-forward unroll of the fused training step (8: register-bound, slower)
-#endif
+constexpr int SC_CW = 2;    // doubles per load batch of a transition copy (register-bound: 2 spills least)
+constexpr int SC_MINB = 2;  // 2 CTAs per SM: one resident wave of 296 CTAs (4736 envs)
+constexpr int SC_QU = 4;    // Q-forward unroll of the fused training step (8: register-bound, slower)
 constexpr int SC_LIST = 4096;  // block-wide transition list (ring-slot order); overflow: per env
 struct CommitShared {
     long long cursor, agg, excl;
-    long long pre[SC_ENVS];  // exclusive prefix of the counts within the block
-    int cnt[SC_ENVS];
+    int cnt[SC_ENVS];        // commit counts of the block's envs
     unsigned long long ep;   // scan epoch << 40
     unsigned long long wmax;
     // the block's committable transitions in ring-slot order (env order, then request-id
@@ -231,18 +224,6 @@ __device__ __forceinline__ void commit_copy_overflow(const StepParams& p, const 
     }
 }
 
-#ifdef BE_STEPC_TIMING
-__device__ unsigned long long g_stepc_t[1024 * 8];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#define STEPC_T(k) \
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_stepc_t[blockIdx.x * 8 + (k)] = gtimer();
-#else
-#define STEPC_T(k)
-#endif
 
 // scan words: epoch << 40 | flag << 38 | value (flag 1 = block aggregate, 2 = inclusive prefix)
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* a) {
@@ -257,8 +238,8 @@ __device__ __forceinline__ void st_release_u64(unsigned long long* a, unsigned l
 }
 
 // Block-wide (every thread of the CTA calls it once per round): the counts of the
-// block's 16 envs -> exclusive prefixes within the block, and the block aggregate
-// published to the look-back array (block 0: directly as its inclusive prefix).
+// block's 16 envs into shared memory, and their sum published to the look-back array
+// (block 0: directly as its inclusive prefix).
 __device__ __forceinline__ void commit_publish(const StepParams& p, const StepOut& so, int count) {
     CommitShared& cs = *so.cs;
     if ((threadIdx.x & 15) == 0) cs.cnt[so.le] = so.live ? count : 0;
@@ -272,11 +253,9 @@ __device__ __forceinline__ void commit_publish(const StepParams& p, const StepOu
             const long long v = __shfl_up_sync(FULL, inc, off);
             if (lane >= off) inc += v;
         }
-        if (lane < SC_ENVS) cs.pre[lane] = inc - own;
         const long long agg = __shfl_sync(FULL, inc, 31);
         if (lane == 0) {
             cs.agg = agg;
-            STEPC_T(1)
             st_release_u64(&p.cm.scan[so.vb], cs.ep | ((so.vb == 0 ? 2ull : 1ull) << 38) | (unsigned long long)agg);
         }
     }
@@ -349,19 +328,26 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     pdl_trigger();  // this CTA is done: the next kernel may start filling the SM
 }
 
-// The training env step (be_train_iteration, fp64 router) with the replay commit
-// fused in: commit_fused_kernel's slots and arithmetic without its launch, its ticket
-// or its flag scan.  Each CTA round steps 16 envs (two per warp); every request the
-// step's advance completed is committable now (its reward was just written, its next
-// state x_{j+1} exists: j <= it - 1), so the env's count is the number of FIFO entries
-// its replicas popped.  The counts are scanned across rounds by decoupled look-back
-// (virtual block = round x grid + CTA; the grid is one resident wave, so every
-// predecessor is running or done), then each env writes its transitions — request-id
-// order within the env, env-id order across envs, exactly commit_fused_kernel's slots.
-
+// The training iteration's env step (be_train_iteration, fp64 router) with the
+// arrivals and the replay commit fused in — one launch where the reference runs
+// TrainingWorkload.next_arrival, ClusterSim.advance / observe / submit, select_action and
+// ReplayBuffer.resolve_* / push per env (trainer.py:374-395, :143-156).  Each CTA
+// round steps 16 envs (two per warp):
+//   * every lane of an env's group draws the env's next arrival (one lane stores the
+//     workload state), then the step runs (step_env);
+//   * every request the advance completed is committable at once (its reward was just
+//     written, its next state x_{j+1} exists: j <= it - 1), so an env's commit count is
+//     the number of FIFO entries its replicas popped; right after the advance the block
+//     publishes its total (commit_publish), so the cross-block scan — decoupled
+//     look-back over virtual blocks (round x grid + CTA; the grid is one resident wave,
+//     so every predecessor is running or done) — overlaps the Q forward and the submit;
+//   * each env lists its committable pending slots in shared memory (request-id order,
+//     after the block's earlier envs), then every thread copies one transition: ring
+//     slot = the block's prefix + list index — commit_fused_kernel's slots (env-id
+//     order, request-id order within an env), so the host-driven loop and this one
+//     fill the ring identically.
 template <int M>
-__global__ void __launch_bounds__(256, BE_STEPC_MINB) env_step_commit_kernel(const StepParams p) {
-    STEPC_T(0)
+__global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const StepParams p) {
     pdl_wait();  // the previous kernel has completed and its writes are visible
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
@@ -396,17 +382,16 @@ __global__ void __launch_bounds__(256, BE_STEPC_MINB) env_step_commit_kernel(con
             train_workload_next(p.wl, live ? e : p.E - 1, live && gl == 0, so.U, so.task, so.rate);
             so.has_wl = true;
         }
-        step_env<M, 16, false, BE_STEPC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
-        STEPC_T(2)
+        step_env<M, 16, false, SC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
         // ---- this env's transitions into the block list (independent of the cross-block
         // prefix, so it overlaps warp 0's look-back)
         const int64_t L = (live && so.jlo <= so.jhi) ? so.jhi - so.jlo + 1 : 0;
-        if (L) commit_list(p, cs, e, le, P, so.jlo, L, cs.pre[le], gl, gmask);
-#ifndef BE_STEPC_NOLB
+        // this env's first list entry: the counts of the block's earlier envs (cs.cnt is
+        // complete since commit_publish's barrier)
+        long long pre = 0;
+        for (int l = 0; l < le; ++l) pre += cs.cnt[l];
+        if (L) commit_list(p, cs, e, le, P, so.jlo, L, pre, gl, gmask);
         if (warp == 0 && vb > 0) {
-#else
-        if (false) {
-#endif
             // the block's exclusive prefix: look back over windows of 256 predecessors
             // (8 per lane, nearest first), summing aggregates up to the nearest
             // inclusive prefix; the aggregates were published right after each
@@ -457,27 +442,18 @@ __global__ void __launch_bounds__(256, BE_STEPC_MINB) env_step_commit_kernel(con
             c.ring_state[2] += n;
             *c.epoch = *c.epoch + 1u;
         }
-        STEPC_T(3)
         __syncthreads();
-        STEPC_T(4)
         // ---- the block's transitions, one per thread: ring slot = block base + list index
         const long long n_blk = cs.agg;
         const int64_t s0 = (cs.cursor + cs.excl) % c.capacity;
-#ifndef BE_STEPC_NOWR
         for (long long i = threadIdx.x; i < (n_blk < SC_LIST ? n_blk : SC_LIST); i += blockDim.x) {
             const int lei = cs.le[i];
             int64_t slot = s0 + i;
             while (slot >= c.capacity) slot -= c.capacity;
-            commit_copy<BE_CW>(p, c, vb * SC_ENVS + lei, D, P, cs.sj[i], slot);
+            commit_copy<SC_CW>(p, c, vb * SC_ENVS + lei, D, P, cs.sj[i], slot);
         }
-#endif
         if (live) {
-            if (n_blk > SC_LIST && L) commit_copy_overflow(p, c, e, D, P, so.jlo, L, cs.pre[le], s0, gl, gmask);
-#ifdef BE_STEPC_TIMING
-            if (gl == 0 && blockIdx.x < 1024) {
-                atomicMax(&g_stepc_t[blockIdx.x * 8 + 7], ((unsigned long long)L << 32) | (unsigned)cs.cnt[le]);
-            }
-#endif
+            if (n_blk > SC_LIST && L) commit_copy_overflow(p, c, e, D, P, so.jlo, L, pre, s0, gl, gmask);
             if (gl == 0) {
                 c.low[e] = so.oldest;
                 const int64_t win = it + 1 - so.oldest;
@@ -485,9 +461,7 @@ __global__ void __launch_bounds__(256, BE_STEPC_MINB) env_step_commit_kernel(con
                 if (win > 0) atomicMax(&cs.wmax, (unsigned long long)win);
             }
         }
-        STEPC_T(5)
         __syncthreads();  // cs is reused by the next round
-        STEPC_T(6)
     }
     // high-water mark of in-flight decisions per env (ring_state[4])
     if (threadIdx.x == 0 && cs.wmax > (unsigned long long)__ldcg(c.ring_state + 4))
@@ -1144,12 +1118,10 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
         p.cm = *commit;
         p.fuse_commit = 1;
         p.crange = nullptr;
-#ifndef BE_STEPC_PREPWL
         if (wl) {
             p.gen_workload = 1;
             p.wl = *wl;
         }
-#endif
     }
     p.tc_img = tc_img;
     p.tc_ncols = W->hidden <= 32 ? 32 : W->hidden <= 64 ? 64 : W->hidden <= 128 ? 128 : 256;
@@ -1204,8 +1176,3 @@ int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStr
 
 }  // namespace be
 
-#ifdef BE_STEPC_TIMING
-extern "C" int be_debug_stepc_times(unsigned long long* out, int n) {
-    return (int)cudaMemcpyFromSymbol(out, be::g_stepc_t, (size_t)n * sizeof(unsigned long long));
-}
-#endif
