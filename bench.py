@@ -297,10 +297,12 @@ def training_probe(dev, world):
                 final_loss=res.log[-1].loss if res.log else None, n_gpus=world,
                 mode=kw["mode"], exchange=kw.get("exchange") if world > 1 else None,
                 exchange_error=exchange_err,
-                note="whole job; device time of the training loop, max over ranks (be_train_iteration: "
-                     "workload, env step, single-pass commit, 128-tile learner + multi-CTA reduce/Adam; "
-                     "CUDA graph replay; W > 1: data-parallel learner, 4096 envs and a replay shard per "
-                     "rank, one update per iteration over the W x 512 sampled transitions)")
+                note="whole job; device time of the training loop, max over ranks (be_train_iteration, "
+                     "two launches per iteration at W = 1: env_step_commit_kernel = arrivals + env step + "
+                     "replay commit, learner_partial_kernel = 128-tile TD/Huber backward + fused "
+                     "reduce/Adam/weight repack; CUDA graph replay; W > 1: data-parallel learner, 4096 "
+                     "envs and a replay shard per rank, one update per iteration over the W x 512 sampled "
+                     "transitions)")
 
 
 

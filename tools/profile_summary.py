@@ -88,6 +88,8 @@ def main():
             rep = os.path.join(out_dir, f"{tag}_prof_{rep_name}.ncu-rep")
         if not os.path.exists(rep):
             continue
+        if rep_name == "train":
+            summ["kernels"]["_train"] = {}  # this report replaces the previous training kernels
         for d in ncu_summary.summary(rep):
             kname = d["kernel"].split("(")[0].replace("void ", "").split("<")[0].strip()
             if kname in summ["kernels"].get("_train", {}):
