@@ -1469,14 +1469,26 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         rec.flags = L->pflags;
         rec.reward = L->preward;
         bool fused_commit = false;
+        const bool fuse = env_step_commit_supported(env) && (c->router != BE_ROUTER_TC || env->R <= 16);
+        StepCommitArgs cm{cf.replay_capacity, L->rs, L->rs2, L->rr, L->rc, L->ra, L->low,
+                          L->ring_state, L->status, L->scan16, L->ticket + 2};
+        if (fuse && L->qpack_env != env) {
+            // the step reads the packed fp64 weights the learner's fused update keeps
+            // current; pack them here once if anything else wrote the parameters
+            rc = launch_stage_qpack(env, &W, st);
+            if (rc) return rc;
+            L->qpack_env = env;
+        }
         if (c->router == BE_ROUTER_TC && env->R <= 16) {
-            // the decision on the tensor cores inside the env step: prep_kernel also packs
-            // the router image; env_step_tc_kernel runs layer 1 of 16 envs per CTA as one
-            // tcgen05 tile (certified, fp64 fallback: the fp64 step's decisions)
+            // the decision on the tensor cores inside the env step (+ arrivals + replay
+            // commit): the router image is repacked, then env_step_commit_kernel<M, true>
+            // runs layer 1 of 16 envs per CTA as one tcgen05 tile (certified, fp64
+            // fallback: the fp64 step's decisions)
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,
-                                     reinterpret_cast<float*>(L->tc_img), L->crange);
+                                     reinterpret_cast<float*>(L->tc_img), nullptr, fuse ? &cm : nullptr);
+            fused_commit = fuse;
         } else if (c->router == BE_ROUTER_TC) {
             // > 16 replicas per env: observe + encode (pending slot) -> the batched
             // tcgen05 router on the E states -> submit
@@ -1493,17 +1505,9 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, nullptr, 2,
                                      nullptr, L->crange);
-        } else if (env_step_commit_supported(env)) {
+        } else if (fuse) {
             // the replay commit fused into the env step: one launch, no flag scan; the
-            // step generates the arrivals itself and reads the weights the learner's
-            // fused update packed (packed here once if anything else wrote them)
-            if (L->qpack_env != env) {
-                rc = launch_stage_qpack(env, &W, st);
-                if (rc) return rc;
-                L->qpack_env = env;
-            }
-            StepCommitArgs cm{cf.replay_capacity, L->rs, L->rs2, L->rr, L->rc, L->ra, L->low,
-                              L->ring_state, L->status, L->scan16, L->ticket + 2};
+            // step generates the arrivals itself
             rc = launch_env_step_dev(env, L->it_arrival, L->it_task, L->it_rate, &W, c->policy_seed, it,
                                      c->epsilon_start, c->epsilon_end, c->epsilon_decay_steps,
                                      cf.pending_capacity, cf.pending_capacity, &rec, L->pa, L->px, st, &wl, 0,

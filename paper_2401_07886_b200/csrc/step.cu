@@ -328,7 +328,23 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
     pdl_trigger();  // this CTA is done: the next kernel may start filling the SM
 }
 
-// The training iteration's env step (be_train_iteration, fp64 router) with the
+// Shared-memory layout of the tensor-core step kernels: Score, the packed router image,
+// the A operand (hi, lo), layer-2 partial sums, mbarriers.
+struct TcStepSmem {
+    size_t img, ah, al, part, bars, bytes;
+    __host__ __device__ static size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+    __host__ __device__ explicit TcStepSmem(int H) {
+        img = up(sizeof(Score), 128);
+        ah = up(img + (size_t)TcLayout{H}.bytes(), 128);
+        al = ah + sizeof(float) * 128 * TC_K;
+        part = al + sizeof(float) * 128 * TC_K;
+        bars = up(part + sizeof(float2) * 2 * 16 * 2 * TC_MP, 16);
+        bytes = bars + 2 * sizeof(uint64_t) + 16;
+    }
+};
+
+// The training iteration's env step (be_train_iteration; TCQ: the greedy decision on
+// the tensor cores, tc_decide, else the fp64 group forward) with the
 // arrivals and the replay commit fused in — one launch where the reference runs
 // TrainingWorkload.next_arrival, ClusterSim.advance / observe / submit, select_action and
 // ReplayBuffer.resolve_* / push per env (trainer.py:374-395, :143-156).  Each CTA
@@ -346,12 +362,36 @@ __global__ void __launch_bounds__(256) env_step_kernel(const StepParams p) {
 //     slot = the block's prefix + list index — commit_fused_kernel's slots (env-id
 //     order, request-id order within an env), so the host-driven loop and this one
 //     fill the ring identically.
-template <int M>
+template <int M, bool TCQ>
 __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const StepParams p) {
     pdl_wait();  // the previous kernel has completed and its writes are visible
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     __shared__ CommitShared cs;
+    // TCQ: one TMEM allocation (H columns; two CTAs per SM) and one bulk copy of the
+    // packed router image per CTA, for all rounds (env_step_tc_kernel's setup)
+    TcStepCtx cx;
+    uint64_t* bars = nullptr;
+    if constexpr (TCQ) {
+        const TcStepSmem S(p.H);
+        cx.img = reinterpret_cast<const float*>(smem_raw + S.img);
+        cx.Ah = reinterpret_cast<float*>(smem_raw + S.ah);
+        cx.Al = reinterpret_cast<float*>(smem_raw + S.al);
+        cx.part = reinterpret_cast<float2*>(smem_raw + S.part);
+        bars = reinterpret_cast<uint64_t*>(smem_raw + S.bars);
+        cx.bar = &bars[1];
+        cx.img_bar = &bars[0];
+        cx.phase = 0;
+        cx.img_ready = false;
+        for (int k = threadIdx.x; k < 2 * 128 * TC_K; k += blockDim.x) cx.Ah[k] = 0.f;  // rows >= 16 stay 0
+        if (threadIdx.x == 0) {
+            tc::mbar_init(&bars[0], 1);
+            tc::mbar_init(&bars[1], 1);
+            tc::fence_mbar_init();
+        }
+        if ((threadIdx.x >> 5) == 0) tc::tmem_alloc(reinterpret_cast<uint32_t*>(bars + 2), (uint32_t)p.tc_ncols);
+        tc::fence_before_sync();
+    }
     const StepCommitArgs& c = p.cm;
     const int T = p.cfg.n_tasks, H = p.H, D = T + M + 1;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = lane >> 4, gl = lane & 15;
@@ -365,6 +405,15 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
     }
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     __syncthreads();
+    if constexpr (TCQ) {
+        tc::fence_after_sync();
+        cx.tmem = *reinterpret_cast<uint32_t*>(bars + 2);
+        if (threadIdx.x == 0) {
+            const uint32_t nb = (uint32_t)TcLayout{p.H}.bytes();
+            tc::mbar_expect_tx(&bars[0], nb);
+            tc::bulk_g2s(const_cast<float*>(cx.img), p.tc_img, nb, &bars[0]);
+        }
+    }
     const int64_t it = *p.iter_dev;
     const int P = p.pending_P;
     const int nvb = (p.E + SC_ENVS - 1) / SC_ENVS;
@@ -382,7 +431,8 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
             train_workload_next(p.wl, live ? e : p.E - 1, live && gl == 0, so.U, so.task, so.rate);
             so.has_wl = true;
         }
-        step_env<M, 16, false, SC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, nullptr, &so);
+        step_env<M, 16, TCQ, SC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, TCQ ? &cx : nullptr,
+                                    &so);
         // ---- this env's transitions into the block list (independent of the cross-block
         // prefix, so it overlaps warp 0's look-back)
         const int64_t L = (live && so.jlo <= so.jhi) ? so.jhi - so.jlo + 1 : 0;
@@ -466,6 +516,22 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
     // high-water mark of in-flight decisions per env (ring_state[4])
     if (threadIdx.x == 0 && cs.wmax > (unsigned long long)__ldcg(c.ring_state + 4))
         atomicMax(reinterpret_cast<unsigned long long*>(c.ring_state + 4), cs.wmax);
+    if constexpr (TCQ) {
+        tc::fence_before_sync();
+        __syncthreads();
+        if ((threadIdx.x >> 5) == 0) tc::tmem_dealloc(cx.tmem, (uint32_t)p.tc_ncols);
+    }
+    pdl_trigger();
+}
+
+// The tensor-core router image for the fused training step (the weights change every
+// update; the fp64 packed weights are kept current by the learner's fused update).
+template <int M>
+__global__ void __launch_bounds__(256) tc_image_kernel(const double* w1, const double* b1, const double* w2,
+                                                       const double* b2, int D, int H, float* img) {
+    pdl_wait();
+    if constexpr (M <= TC_MP) tc_pack_image<M>(w1, b1, w2, b2, D, H, img, blockIdx.x * blockDim.x + threadIdx.x,
+                                                 gridDim.x * blockDim.x);
     pdl_trigger();
 }
 
@@ -651,18 +717,6 @@ __device__ __forceinline__ int tc_decide(TcStepCtx& cx, bool live, bool explore,
 }
 
 // Shared-memory plan of env_step_tc_kernel: [Score | image | A hi | A lo | partials | barriers]
-struct TcStepSmem {
-    size_t img, ah, al, part, bars, bytes;
-    __host__ __device__ static size_t up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-    __host__ __device__ explicit TcStepSmem(int H) {
-        img = up(sizeof(Score), 128);
-        ah = up(img + (size_t)TcLayout{H}.bytes(), 128);
-        al = ah + sizeof(float) * 128 * TC_K;
-        part = al + sizeof(float) * 128 * TC_K;
-        bars = up(part + sizeof(float2) * 2 * 16 * 2 * TC_MP, 16);
-        bytes = bars + 2 * sizeof(uint64_t) + 16;
-    }
-};
 
 // The training env step with the greedy decision on the tensor cores (be_train_iteration,
 // router = BE_ROUTER_TC).  256 threads = 16 envs (16 lanes each) per CTA round, rounds
@@ -722,10 +776,13 @@ size_t step_tc_smem_bytes(int H) { return TcStepSmem(H).bytes; }
 void step_tc_prepare(int M, int H) {
     const int smem = (int)TcStepSmem(H).bytes;
     switch (M) {
-        case 1: cudaFuncSetAttribute(env_step_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 2: cudaFuncSetAttribute(env_step_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 3: cudaFuncSetAttribute(env_step_tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 4: cudaFuncSetAttribute(env_step_tc_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
+#define BE_TCP(MM)                                                                                          \
+    case MM:                                                                                                \
+        cudaFuncSetAttribute(env_step_tc_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
+        cudaFuncSetAttribute(env_step_commit_kernel<MM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        break;
+        BE_TCP(1) BE_TCP(2) BE_TCP(3) BE_TCP(4)
+#undef BE_TCP
         default: break;
     }
 }
@@ -983,6 +1040,19 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
         if (e != cudaSuccess) return set_cuda_error(e, "stage_qpack launch");
     }
     if constexpr (M <= TC_MP) {
+        if (tc_img && p.fuse_commit) {  // image, then step + arrivals + commit with tcgen05 decisions
+            cudaError_t e = launch_pdl(tc_image_kernel<M>, dim3(TCPACK_CTAS), dim3(256), 0, st, p.w1, p.b1, p.w2,
+                                       p.b2, p.cfg.n_tasks + M + 1, p.H, tc_img);
+            if (e != cudaSuccess) return set_cuda_error(e, "router image launch");
+            int dev = 0, sms = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            long long blocks = ((long long)p.E + SC_ENVS - 1) / SC_ENVS;
+            if (blocks > 2LL * sms) blocks = 2LL * sms;  // two CTAs per SM share its TMEM
+            e = launch_pdl(env_step_commit_kernel<M, true>, dim3((unsigned)blocks), dim3(256), step_tc_smem_bytes(p.H),
+                           st, p);
+            return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step + commit (tensor cores) launch");
+        }
         if (tc_img) {  // the decision on the tensor cores (attribute set by step_tc_prepare)
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
@@ -999,12 +1069,12 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_commit_kernel<M>, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_commit_kernel<M, false>, 256, smem);
         if (per_sm < 1) per_sm = 1;
         // one resident wave (the look-back needs every predecessor running or done)
         long long blocks = ((long long)p.E + SC_ENVS - 1) / SC_ENVS;
         if (blocks > (long long)sms * per_sm) blocks = (long long)sms * per_sm;
-        cudaError_t e = launch_pdl(env_step_commit_kernel<M>, dim3((unsigned)blocks), dim3(256), smem, st, p);
+        cudaError_t e = launch_pdl(env_step_commit_kernel<M, false>, dim3((unsigned)blocks), dim3(256), smem, st, p);
         return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step + commit launch");
     }
     if (smem > 48 * 1024) {
@@ -1113,8 +1183,7 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     p.phase = phase;
     p.crange = crange;
     if (commit) {
-        if (phase != 0 || tc_img || rec_ld != pending_P)
-            return set_error(BE_EINVAL, "the fused commit is the fp64-router training step");
+        if (phase != 0 || rec_ld != pending_P) return set_error(BE_EINVAL, "the fused commit is the training step");
         p.cm = *commit;
         p.fuse_commit = 1;
         p.crange = nullptr;
