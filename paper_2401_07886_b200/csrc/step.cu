@@ -14,6 +14,20 @@
 
 namespace be {
 
+// Development probe points (compiled out unless BE_PROBE_T is defined): thread 0 of
+// CTA b records %globaltimer into be_probe_t[b][k]; read back with be_debug_probe.
+#ifdef BE_PROBE_T
+__device__ unsigned long long be_probe_t[1024 * 16];
+#define BE_PROBE(k)                                                                   \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
+        unsigned long long t_;                                                        \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+        be_probe_t[blockIdx.x * 16 + (k)] = t_;                                       \
+    }
+#else
+#define BE_PROBE(k)
+#endif
+
 struct EnvState {
     double w[5];
     int32_t n;
@@ -102,6 +116,9 @@ struct StepParams {
     int32_t gen_workload;
     WorkloadArgs wl;
 };
+
+// dynamic shared memory of the step kernels starts with the reward tables (Score)
+__host__ __device__ constexpr size_t step_score_bytes() { return (sizeof(Score) + 15) & ~size_t(15); }
 
 // Shared state of one env_step_commit_kernel CTA round.
 constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
@@ -403,6 +420,20 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
         cs.ep = (unsigned long long)(__ldcg(c.epoch) & 0xffffffu) << 40;
         cs.wmax = 0ull;
     }
+    // fp64 decisions: the packed weights into shared memory (asynchronous copies,
+    // landing during the arrivals and the advance; read by every round's Q forward)
+    const double* sw = p.qpack;
+    if constexpr (!TCQ) {
+        double* swm = reinterpret_cast<double*>(smem_raw + step_score_bytes());
+        const int nd = (int)QLayout<M>::doubles(p.cfg.n_tasks, p.H);
+        for (int k = threadIdx.x; 2 * k < nd; k += blockDim.x) {
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(swm + 2 * k);
+            if (2 * k + 1 < nd) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(p.qpack + 2 * k));
+            else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(p.qpack + 2 * k));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        sw = swm;
+    }
     if (threadIdx.x < 32) load_score(sc, p.cfg, p.aux);
     __syncthreads();
     if constexpr (TCQ) {
@@ -427,20 +458,24 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
         so.le = le;
         so.live = live;
         so.has_wl = false;
+        BE_PROBE(0)
         if (p.gen_workload) {  // TrainingWorkload.next_arrival (trainer.py:304-316), lane 0 stores
             train_workload_next(p.wl, live ? e : p.E - 1, live && gl == 0, so.U, so.task, so.rate);
             so.has_wl = true;
         }
-        step_env<M, 16, TCQ, SC_QU>(p, live ? e : p.E - 1, live, sc, p.qpack, true, T, H, D, TCQ ? &cx : nullptr,
-                                    &so);
+        BE_PROBE(1)
+        if constexpr (!TCQ) asm volatile("cp.async.wait_all;\n" ::);  // visible to all after step_env's barrier
+        step_env<M, 16, TCQ, SC_QU>(p, live ? e : p.E - 1, live, sc, sw, true, T, H, D, TCQ ? &cx : nullptr, &so);
         // ---- this env's transitions into the block list (independent of the cross-block
         // prefix, so it overlaps warp 0's look-back)
+        BE_PROBE(3)
         const int64_t L = (live && so.jlo <= so.jhi) ? so.jhi - so.jlo + 1 : 0;
         // this env's first list entry: the counts of the block's earlier envs (cs.cnt is
         // complete since commit_publish's barrier)
         long long pre = 0;
         for (int l = 0; l < le; ++l) pre += cs.cnt[l];
         if (L) commit_list(p, cs, e, le, P, so.jlo, L, pre, gl, gmask);
+        BE_PROBE(4)
         if (warp == 0 && vb > 0) {
             // the block's exclusive prefix: look back over windows of 256 predecessors
             // (8 per lane, nearest first), summing aggregates up to the nearest
@@ -492,7 +527,9 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
             c.ring_state[2] += n;
             *c.epoch = *c.epoch + 1u;
         }
+        BE_PROBE(5)
         __syncthreads();
+        BE_PROBE(6)
         // ---- the block's transitions, one per thread: ring slot = block base + list index
         const long long n_blk = cs.agg;
         const int64_t s0 = (cs.cursor + cs.excl) % c.capacity;
@@ -511,7 +548,9 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
                 if (win > 0) atomicMax(&cs.wmax, (unsigned long long)win);
             }
         }
+        BE_PROBE(7)
         __syncthreads();  // cs is reused by the next round
+        BE_PROBE(8)
     }
     // high-water mark of in-flight decisions per env (ring_state[4])
     if (threadIdx.x == 0 && cs.wmax > (unsigned long long)__ldcg(c.ring_state + 4))
@@ -881,6 +920,7 @@ __device__ __forceinline__ void step_env(const StepParams& p, int e, bool live, 
             so->jlo = jlo;
             so->jhi = jhi;
             commit_publish(p, *so, (int)group_sum<LPE>((unsigned)popped, grp));
+            BE_PROBE(2)
         } else if (live && gl == 0) {
             p.crange[3 * (int64_t)e] = jlo;
             p.crange[3 * (int64_t)e + 1] = jhi;
@@ -1069,6 +1109,12 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
         int per_sm = 0, dev = 0, sms = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        smem = step_score_bytes() + QLayout<M>::doubles(p.cfg.n_tasks, p.H) * sizeof(double);  // + the weights
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(env_step_commit_kernel<M, false>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute");
+        }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_commit_kernel<M, false>, 256, smem);
         if (per_sm < 1) per_sm = 1;
         // one resident wave (the look-back needs every predecessor running or done)
@@ -1094,7 +1140,7 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
     return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step launch");
 }
 
-static size_t step_smem_bytes() { return (sizeof(Score) + 15) & ~size_t(15); }
+static size_t step_smem_bytes() { return step_score_bytes(); }
 
 static int dispatch_step(const StepParams& p, size_t smem, cudaStream_t st, const WorkloadArgs* wl = nullptr) {
     switch (p.cfg.n_tiers) {
@@ -1245,3 +1291,9 @@ int launch_env_drain(be_env* env, int64_t rec_ld, const be_records* rec, cudaStr
 
 }  // namespace be
 
+
+#ifdef BE_PROBE_T
+extern "C" int be_debug_probe(unsigned long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, be::be_probe_t, (size_t)n * sizeof(unsigned long long));
+}
+#endif
