@@ -266,6 +266,7 @@ struct LearnParams {
     double* qpack;             // the env step's packed weights (QLayout), or NULL
     int32_t T;                 // tasks (packing)
     int32_t stage_out;         // tile partials staged in shared memory, copied out coalesced
+    int32_t tail_ns;           // tail CTAs: min(TAIL_CTAS, tiles, resident CTAs - 1) (waiting is safe)
 };
 
 __device__ __forceinline__ double relu_d(double x) {
@@ -665,15 +666,15 @@ __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateP
 
 // ------------------------------------------- fused update (learner_partial_kernel tail)
 // The TD/Huber backward and the optimizer step in ONE launch: every tile CTA takes a
-// ticket after writing its partial sums; the last TAIL_CTAS to arrive (all other tiles
-// have arrived or are running, so waiting is safe at any grid size) wait for the
-// remaining tiles, then each reduces the partials of one slice of hidden units — w1[:, j],
+// ticket after writing its partial sums; the last tail_ns to arrive (at most TAIL_CTAS,
+// and fewer than the GPU holds at once, so the tiles they wait for always find a slot)
+// wait for the remaining tiles, then each reduces the partials of one slice of hidden units — w1[:, j],
 // b1[j], w2[j, :] for j in the slice (slice 0 also b2 and the loss) — with exactly
 // learner_update_kernel's fixed tree (8 tile slices summed in tile order, then in slice
 // order), applies Adam / SGD (apply_elem) and repacks those units' entries of the env
 // step's weight layout (QLayout, stage_qnet's values).  The last slice to finish advances
 // the counters (apply_finish).  Bit-identical to partial + learner_update_kernel.
-constexpr int TAIL_CTAS = 64;
+constexpr int TAIL_CTAS = 128;  // at most (measured: 128 > 64 > 32 at batch 512)
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* a) {
     unsigned long long v;
@@ -701,7 +702,7 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
     }
     __syncthreads();
     const unsigned long long nt = gridDim.x, v = rank_sh;
-    const int NS = (int)(nt < TAIL_CTAS ? nt : TAIL_CTAS);
+    const int NS = p.tail_ns;
     const unsigned long long rank = v % nt;
     if (rank < nt - NS) return;
     const int slice = (int)(rank - (nt - NS));
@@ -1311,7 +1312,18 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
     }
     if (smem > 200 * 1024) return set_error(BE_EINVAL, "hidden too large for the learner tile");
     ApplyParams ap{};
+    auto kern = D <= 8 ? learner_partial_kernel<8> : D <= 16 ? learner_partial_kernel<16> : learner_partial_kernel<32>;
     if (tail) {  // backward + optimizer in this one launch (learner_tail)
+        // the tail CTAs spin until every tile has arrived: fewer of them than the
+        // GPU holds at once, so the tiles they wait for always find a slot
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LTHREADS, smem);
+        int ns = TAIL_CTAS < L->n_tiles ? TAIL_CTAS : L->n_tiles;
+        if (ns > sms * per_sm - 1) ns = sms * per_sm - 1;
+        if (ns < 1) return set_error(BE_EINVAL, "learner tile does not fit the GPU");
+        p.tail_ns = ns;
         ap = apply_params(L, sampling ? 0 : 1, advance);
         ap.gate = gate;
         p.tail = 1;
@@ -1319,7 +1331,6 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
         p.qpack = qpack;
         p.T = cf.n_tasks;
     }
-    auto kern = D <= 8 ? learner_partial_kernel<8> : D <= 16 ? learner_partial_kernel<16> : learner_partial_kernel<32>;
     kern<<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
     // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
     cudaError_t e = cudaGetLastError();
