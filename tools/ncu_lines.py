@@ -44,7 +44,8 @@ def main():
     rep, obj, ksub = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     # one kernel of a multi-kernel report: filter on import, first matching launch
-    raw = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{ksub}", "-c", "1", "--page", "source",
+    kfilt = ksub.split("ILi")[0]  # a mangled template suffix selects SASS, not the ncu filter
+    raw = subprocess.run(["ncu", "-i", rep, "-k", f"regex:{kfilt}", "-c", "1", "--page", "source",
                           "--print-source", "sass", "--csv"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
