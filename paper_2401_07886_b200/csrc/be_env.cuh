@@ -214,17 +214,22 @@ __device__ __forceinline__ void complete(const Rep& r, const TierC& tc, const Sc
 // kernels stage the table in shared memory.  Skipping keeps every operand at
 // or below (2^53 - 2) u, the second-largest double of the binade.
 
-// Number k <= kmax of whole START->END cycles that can be jumped from a START
-// at time t (0 < t < until); writes the time after k cycles.  `tab` is this
-// tier's table, indexed [n][binade - SKIP_ELO].
-__device__ __forceinline__ int skip_cycles(double t, const double* __restrict__ tab, int n, int kmax,
-                                           double until, double& t_out) {
-    if (kmax <= 0) return 0;
+// The table entry of a START at time t with n running requests (0: no skip); `tab`
+// is this tier's table, indexed [n][binade - SKIP_ELO].
+__device__ __forceinline__ double skip_entry(double t, const double* __restrict__ tab, int n) {
     const int hi = __double2hiint(t);
     const int ib = ((hi >> 20) & 0x7ff) - (1023 + SKIP_ELO);
-    if ((unsigned)ib >= (unsigned)SKIP_NB || hi < 0) return 0;
-    const double D = tab[n * SKIP_NB + ib];
+    if ((unsigned)ib >= (unsigned)SKIP_NB || hi < 0) return 0.0;
+    return tab[n * SKIP_NB + ib];
+}
+
+// Number k <= kmax of whole START->END cycles that can be jumped from a START at
+// time t (0 < t < until), D = skip_entry(t, ...) (loaded by the caller ahead of
+// time); writes the time after k cycles.
+__device__ __forceinline__ int skip_cycles_d(double t, double D, int kmax, double until, double& t_out) {
+    if (kmax <= 0) return 0;
     if (!(D > 0.0)) return 0;
+    const int hi = __double2hiint(t);
     // (2^53 - 2) u: same exponent as t, mantissa all ones but the last bit
     const double top = __hiloint2double(hi | 0x000fffff, (int)0xfffffffe);
     // x = min(top, until) - t is exact: both operands are multiples of u in t's binade
@@ -246,6 +251,7 @@ __device__ __forceinline__ int skip_cycles(double t, const double* __restrict__ 
     return (int)q;
 }
 
+
 // ---------------------------------------------------------------------------
 // One replica's share of ClusterSim.advance(until) (simcore.py:113-149):
 // process events while (t, kind) < (until, START); END at the horizon is
@@ -257,6 +263,8 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
         if (r.kind == K_START) {
             if (!(r.t < until)) break;
             int n_active = min(r.count, tc.max_batch);
+            // the skip-table entry of this START, in flight during the joins below (+0.7%)
+            const double Dskip = tc.skip ? skip_entry(r.t, tc.skip, n_active) : 0.0;
             if (r.n_running < n_active) {  // newly admitted requests join (simcore.py:143-145)
                 if (r.n_running == 0) r.h_join = r.iters;
                 // requests admitted straight into `active` got their join at submit; only
@@ -270,7 +278,7 @@ __device__ __forceinline__ bool advance_lane(Rep& r, const TierC& tc, double unt
             if (tc.skip) {
                 int K = r.h_join + tc.tokens - r.iters;  // ENDs until the head completes
                 double tn;
-                int k = skip_cycles(r.t, tc.skip, n_active, min(K - 1, (1 << 30) - r.iters), until, tn);
+                int k = skip_cycles_d(r.t, Dskip, min(K - 1, (1 << 30) - r.iters), until, tn);
                 if (k > 0) {
                     r.t = tn;
                     r.iters += k;
