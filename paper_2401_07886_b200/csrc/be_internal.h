@@ -105,6 +105,7 @@ struct StepCommitArgs {
     int32_t* status;             // learner status (pending-store overflow)
     unsigned long long* scan;    // [ceil(E / 16)] decoupled look-back state
     unsigned* epoch;             // scan epoch (advanced by the last block)
+    int32_t list_cap;            // block transition-list entries used (<= SC_LIST; set at launch)
 };
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,

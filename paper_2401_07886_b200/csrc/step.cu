@@ -5,6 +5,7 @@
 // training loop, a custom router) between steps.  One warp per env.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "be_env.cuh"
 #include "be_internal.h"
@@ -155,9 +156,10 @@ struct StepOut {
 // An env's committable transitions into the block list: its completed id range
 // [jlo, jlo + L) is scanned 256 ids per pass (16 per lane, independent flag loads);
 // the ready ones (reward written: flag 0x40) take list entries base, base + 1, ... in
-// id order.  Entries past SC_LIST are left to commit_copy_overflow.  Group-wide.
+// id order.  Entries past the list capacity are left to commit_copy_overflow.  Group-wide.
 __device__ __forceinline__ void commit_list(const StepParams& p, CommitShared& cs, int e, int le, int P, int64_t jlo,
                                             int64_t L, long long base, int gl, unsigned gmask) {
+    const int cap = p.cm.list_cap;
     const int64_t r0 = jlo % P;
     for (int64_t b0 = 0; b0 < L; b0 += 256) {
         const int64_t sbase = (r0 + b0 + gl * 16) % P;
@@ -179,7 +181,7 @@ __device__ __forceinline__ void commit_list(const StepParams& p, CommitShared& c
         while (bits) {
             int64_t sj = sbase + __ffs(bits) - 1;
             if (sj >= P) sj = P >= 16 ? sj - P : sj % P;
-            if (r < SC_LIST) {
+            if (r < cap) {
                 cs.sj[r] = (uint32_t)sj;
                 cs.le[r] = (uint8_t)le;
             }
@@ -221,8 +223,8 @@ __device__ __forceinline__ void commit_copy(const StepParams& p, const StepCommi
     p.rec.flags[(int64_t)e * P + sj] = 0x20;
 }
 
-// The block list overflowed (more than SC_LIST transitions in one block and step):
-// the owning env group rescans its range and copies its entries at list index >= SC_LIST.
+// The block list overflowed (more transitions in one block and step than its capacity):
+// the owning env group rescans its range and copies its entries at list index >= cap.
 __device__ __forceinline__ void commit_copy_overflow(const StepParams& p, const StepCommitArgs& c, int e, int D, int P,
                                                      int64_t jlo, int64_t L, long long base, int64_t s0, int gl,
                                                      unsigned gmask) {
@@ -232,7 +234,7 @@ __device__ __forceinline__ void commit_copy_overflow(const StepParams& p, const 
         const bool ready = b0 + gl < L && (p.rec.flags[(int64_t)e * P + sj] & 0x40);
         const unsigned rb = __ballot_sync(gmask, ready);
         const long long idx = base + __popc(rb & ((1u << (threadIdx.x & 31)) - 1u));
-        if (ready && idx >= SC_LIST) {
+        if (ready && idx >= p.cm.list_cap) {
             int64_t slot = s0 + idx;
             while (slot >= c.capacity) slot -= c.capacity;
             commit_copy<4>(p, c, e, D, P, sj, slot);
@@ -533,14 +535,20 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
         // ---- the block's transitions, one per thread: ring slot = block base + list index
         const long long n_blk = cs.agg;
         const int64_t s0 = (cs.cursor + cs.excl) % c.capacity;
-        for (long long i = threadIdx.x; i < (n_blk < SC_LIST ? n_blk : SC_LIST); i += blockDim.x) {
+        const long long n_list = n_blk < c.list_cap ? n_blk : c.list_cap;
+        if (n_blk > c.list_cap) {  // (block-uniform) the list overflowed
+            // entries past the list, found by rescanning the ready flags — before any
+            // listed entry's flag is cleared below, so the ranks match the list's
+            if (live && L) commit_copy_overflow(p, c, e, D, P, so.jlo, L, pre, s0, gl, gmask);
+            __syncthreads();
+        }
+        for (long long i = threadIdx.x; i < n_list; i += blockDim.x) {
             const int lei = cs.le[i];
             int64_t slot = s0 + i;
             while (slot >= c.capacity) slot -= c.capacity;
             commit_copy<SC_CW>(p, c, vb * SC_ENVS + lei, D, P, cs.sj[i], slot);
         }
         if (live) {
-            if (n_blk > SC_LIST && L) commit_copy_overflow(p, c, e, D, P, so.jlo, L, pre, s0, gl, gmask);
             if (gl == 0) {
                 c.low[e] = so.oldest;
                 const int64_t win = it + 1 - so.oldest;
@@ -1231,6 +1239,12 @@ int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
     if (commit) {
         if (phase != 0 || rec_ld != pending_P) return set_error(BE_EINVAL, "the fused commit is the training step");
         p.cm = *commit;
+        // BE_COMMIT_LIST_CAP (tests only): a smaller block list, to exercise the overflow path
+        p.cm.list_cap = SC_LIST;
+        if (const char* lc = getenv("BE_COMMIT_LIST_CAP")) {
+            const int v = atoi(lc);
+            if (v >= 0 && v < SC_LIST) p.cm.list_cap = v;
+        }
         p.fuse_commit = 1;
         p.crange = nullptr;
         if (wl) {

@@ -240,3 +240,23 @@ def test_training_fused_iteration_edge_shapes(cuda, shape):
         for a, b in zip(r.net.params(), ref.net.params()):
             assert np.array_equal(a, b), m
         assert [(x.step, x.loss) for x in r.log] == [(x.step, x.loss) for x in ref.log], m
+
+
+@pytest.mark.parametrize("cap", ["0", "1", "5"])
+def test_training_fused_commit_list_overflow(cuda, monkeypatch, cap):
+    """The fused step's block transition list overflowing (BE_COMMIT_LIST_CAP shrinks
+    it from 4096 entries: 0 = every transition takes the per-env overflow copy, 1 / 5 =
+    an env's transitions split between the list and the overflow copy — the case a
+    rescan racing the listed copies' flag updates got wrong) still fills the ring
+    exactly as the host-driven loop."""
+    tiers, rw = default_tiers(), RewardSpec.default()
+    cfg = TrainConfig(batch_size=64, buffer_capacity=4_000, warmup=300, total_iterations=150, log_every=50,
+                      seed=19)
+    ref = run_training(tiers, rw, cfg, n_envs=40, updates_per_step=1, mode="host")
+    monkeypatch.setenv("BE_COMMIT_LIST_CAP", cap)
+    r = run_training(tiers, rw, cfg, n_envs=40, updates_per_step=1, mode="device")
+    assert r.updates == ref.updates and r.transitions == ref.transitions
+    for a, b in zip(r.net.params(), ref.net.params()):
+        assert np.array_equal(a, b)
+    assert [(x.step, x.loss, x.mean_recent_reward) for x in r.log] == \
+           [(x.step, x.loss, x.mean_recent_reward) for x in ref.log]
