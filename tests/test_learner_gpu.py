@@ -212,25 +212,32 @@ def test_training_modes_bit_identical_multi_round(cuda):
            [(x.step, x.loss, x.mean_recent_reward) for x in ref.log]
 
 
-@pytest.mark.parametrize("shape", ["odd_hidden_batch", "many_replicas"])
+@pytest.mark.parametrize("shape", ["odd_hidden_batch", "many_replicas", "wide_hidden_big_batch"])
 def test_training_fused_iteration_edge_shapes(cuda, shape):
     """The two-launch device iteration on shapes its fast paths special-case, against
     the host-driven loop (separate step, commit, tiles and update launches):
     odd_hidden_batch — hidden 100 (hidden-unit slices of unequal size, empty trailing
     slices), batch 50 (a partial last tile, fewer tiles than fused-update slices), three
     updates per iteration; many_replicas — 24 replicas per env (more than a 16-lane
-    group: the step + separate commit path)."""
+    group: the step + separate commit path); wide_hidden_big_batch — batch 1024 (tiles
+    that finish before the tail CTAs) and hidden 1024 (tile partials written directly,
+    not staged in shared memory)."""
     rw = RewardSpec.default()
     if shape == "odd_hidden_batch":
         tiers = default_tiers()
         cfg = TrainConfig(batch_size=50, buffer_capacity=5_000, warmup=300, total_iterations=120, log_every=40,
                           seed=13, hidden=100, target_sync_every=4)
         kw = dict(n_envs=21, updates_per_step=3)
-    else:
+    elif shape == "many_replicas":
         tiers = default_tiers(replicas=8)
         cfg = TrainConfig(batch_size=64, buffer_capacity=5_000, warmup=300, total_iterations=120, log_every=40,
                           seed=17)
         kw = dict(n_envs=19, updates_per_step=1)
+    else:  # 256 tiles (more than the fused update's tail CTAs); partials too big to stage
+        tiers = default_tiers()
+        cfg = TrainConfig(batch_size=1024, buffer_capacity=20_000, warmup=1_100, total_iterations=80, log_every=40,
+                          seed=23, hidden=1024)
+        kw = dict(n_envs=64, updates_per_step=1)
     out = {m: run_training(tiers, rw, cfg, mode=m, **kw) for m in ("host", "device", "graph")}
     ref = out["host"]
     assert ref.updates > 50
