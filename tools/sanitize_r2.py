@@ -1,6 +1,7 @@
 """Small workloads over the kernels added in round 2, for compute-sanitizer
-(memcheck / racecheck / synccheck): the training step with the decision fused
-onto tcgen05 (env_step_tc_kernel) and its split form (> 16 replicas), the
+(memcheck / racecheck / synccheck): the fused training iteration (arrivals + step +
+replay commit, fp64 and tcgen05 decisions, the commit list overflowing; backward +
+Adam in one launch), the split tensor-core form (> 16 replicas), the
 completion-range commit, the step split (observe / route_tc / submit), segment
 resets, the rollout's device-side task check and the by-value reducer thresholds."""
 import os
@@ -21,6 +22,10 @@ rw = RewardSpec.default()
 cfg = TrainConfig(batch_size=16, buffer_capacity=4096, warmup=16, total_iterations=10, log_every=5, seed=1)
 for router in ("fp64", "tc"):
     run_training(default_tiers(), rw, cfg, n_envs=40, mode="device", router=router, pending_capacity=256)
+# the fused step + commit with its block list overflowing (list entries + per-env rescan)
+os.environ["BE_COMMIT_LIST_CAP"] = "1"
+run_training(default_tiers(), rw, cfg, n_envs=40, mode="device", pending_capacity=256)
+del os.environ["BE_COMMIT_LIST_CAP"]
 wide = [ModelTierSpec(i, 6, t.alpha_ms, t.beta_ms, t.max_batch, t.tokens_per_request) for i, t in
         enumerate(default_tiers())]  # 18 replicas per env: the split tensor-core path
 run_training(wide, rw, cfg, StateEncoding(4, (128.0, 32.0, 8.0)), n_envs=24, mode="device", router="tc",
