@@ -420,8 +420,13 @@ int32_t be_learner_open_peers_ipc(be_learner* learner, int32_t world, int32_t ra
  *   pending slot it % P) -> commit(it) -> update(s) -> it += 1.
  * Bit-identical to driving be_learner_workload / be_env_step / be_learner_commit
  * / be_learner_backward / be_learner_apply from the host with the same seeds.
- * phase 0: whole iteration; each update = the row-tile kernel (Double-Q targets,
- *          Huber backward) + one tile-reduction/Adam kernel.
+ * phase 0: whole iteration in two launches when the env has <= 16 replicas and
+ *          input dim <= 16: the env step with the arrivals and the replay commit
+ *          fused in, then per update one kernel — row tiles (Double-Q targets, Huber
+ *          backward) whose last CTAs reduce the tiles, apply Adam and repack the
+ *          step's weights (else: separate step, commit and tile + reduce/Adam launches).
+ *          Weights written outside the learner (be_learner_set_params) are repacked
+ *          by the next phase-0 call.
  * phase 4: whole iteration with the peer-memory gradient exchange (data-parallel,
  *          be_learner_set_peers first): no host round trip, graph-capturable.
  * phase 3: the env part only (workload, env step, commits; with
@@ -441,8 +446,9 @@ typedef struct {
     int32_t update_index;
     int32_t use_gate;
     int32_t router;   /* BE_ROUTER_FP64: the decision inside the env step (fp64 Q);
-                         BE_ROUTER_TC: observe -> tensor-core router (be_qnet_route_tc,
-                         tcgen05, certified + fp64 fallback: the same decisions) -> submit */
+                         BE_ROUTER_TC: the decision on tcgen05 inside the env step
+                         (<= 16 replicas; else observe -> be_qnet_route_tc -> submit),
+                         certified + fp64 fallback: the same decisions */
     int32_t _pad;
 } be_train_iter_cfg;
 #define BE_ROUTER_FP64 0
