@@ -106,6 +106,10 @@ struct StepCommitArgs {
     unsigned long long* scan;    // [ceil(E / 16)] decoupled look-back state
     unsigned* epoch;             // scan epoch (advanced by the last block)
     int32_t list_cap;            // block transition-list entries used (<= SC_LIST; set at launch)
+    // virtual block ids from a ticket (when the grid may exceed the CTAs resident at once):
+    // [2] counters used by alternate launches (epoch parity), each reset one launch ahead
+    unsigned* vticket;
+    int32_t use_ticket;
 };
 int launch_env_step_dev(be_env* env, const double* arrival, const uint8_t* task,
                         const double* true_rate, const be_qweights* W, uint64_t seed,

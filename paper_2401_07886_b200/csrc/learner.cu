@@ -1482,7 +1482,7 @@ int32_t be_train_iteration(be_learner* L, be_env* env, const be_train_iter_cfg* 
         bool fused_commit = false;
         const bool fuse = env_step_commit_supported(env) && (c->router != BE_ROUTER_TC || env->R <= 16);
         StepCommitArgs cm{cf.replay_capacity, L->rs, L->rs2, L->rr, L->rc, L->ra, L->low,
-                          L->ring_state, L->status, L->scan16, L->ticket + 2};
+                          L->ring_state, L->status, L->scan16, L->ticket + 2, 0, L->ticket + 4, 0};
         if (fuse && L->qpack_env != env) {
             // the step reads the packed fp64 weights the learner's fused update keeps
             // current; pack them here once if anything else wrote the parameters

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <stdio.h>
 
 #include "be_env.cuh"
 #include "be_internal.h"
@@ -129,6 +130,7 @@ constexpr int SC_QU = 4;    // Q-forward unroll of the fused training step (8: r
 constexpr int SC_LIST = 4096;  // block-wide transition list (ring-slot order); overflow: per env
 struct CommitShared {
     long long cursor, agg, excl;
+    int vb;                  // this round's virtual block (ticket mode)
     int cnt[SC_ENVS];        // commit counts of the block's envs
     unsigned long long ep;   // scan epoch << 40
     unsigned long long wmax;
@@ -450,7 +452,19 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
     const int64_t it = *p.iter_dev;
     const int P = p.pending_P;
     const int nvb = (p.E + SC_ENVS - 1) / SC_ENVS;
-    for (int vb = blockIdx.x; vb < nvb; vb += gridDim.x) {  // CTA-uniform rounds
+    // CTA-uniform rounds.  Virtual blocks: blockIdx.x, + gridDim.x, ... when the whole grid
+    // is resident at once (every look-back predecessor is running or done); else taken
+    // from a ticket in start order, so a block only ever waits on blocks already handed
+    // to running CTAs
+    const unsigned ep_par = (unsigned)(cs.ep >> 40) & 1u;
+    for (int vb = blockIdx.x;; vb += gridDim.x) {
+        if (c.use_ticket) {
+            __syncthreads();  // the previous round's reads of cs.vb are done
+            if (threadIdx.x == 0) cs.vb = (int)atomicAdd(&c.vticket[ep_par], 1u);
+            __syncthreads();
+            vb = cs.vb;
+        }
+        if (vb >= nvb) break;
         const int le = warp * 2 + grp;
         const int e = vb * SC_ENVS + le;
         const bool live = e < p.E;
@@ -528,6 +542,7 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
             c.ring_state[1] = c.ring_state[1] + n < c.capacity ? c.ring_state[1] + n : c.capacity;
             c.ring_state[2] += n;
             *c.epoch = *c.epoch + 1u;
+            if (c.use_ticket) c.vticket[ep_par ^ 1u] = 0u;  // the next launch's counter
         }
         BE_PROBE(5)
         __syncthreads();
@@ -827,6 +842,8 @@ void step_tc_prepare(int M, int H) {
     case MM:                                                                                                \
         cudaFuncSetAttribute(env_step_tc_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
         cudaFuncSetAttribute(env_step_commit_kernel<MM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        cudaFuncSetAttribute(env_step_commit_kernel<MM, true>, cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                             (int)cudaSharedmemCarveoutMaxShared); /* two CTAs per SM (shared TMEM) */       \
         break;
         BE_TCP(1) BE_TCP(2) BE_TCP(3) BE_TCP(4)
 #undef BE_TCP
@@ -1095,10 +1112,18 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
             int dev = 0, sms = 0;
             cudaGetDevice(&dev);
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            // two CTAs per SM (they share its TMEM); when the occupancy calculator does not
+            // vouch for all of them being resident at once, virtual blocks come from a ticket
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, env_step_commit_kernel<M, true>, 256,
+                                                          step_tc_smem_bytes(p.H));
+            if (per_sm < 1) return set_error(BE_EINVAL, "tensor-core step does not fit an SM");
             long long blocks = ((long long)p.E + SC_ENVS - 1) / SC_ENVS;
-            if (blocks > 2LL * sms) blocks = 2LL * sms;  // two CTAs per SM share its TMEM
+            if (blocks > 2LL * sms) blocks = 2LL * sms;
+            StepParams q = p;
+            q.cm.use_ticket = blocks > (long long)per_sm * sms ? 1 : 0;
             e = launch_pdl(env_step_commit_kernel<M, true>, dim3((unsigned)blocks), dim3(256), step_tc_smem_bytes(p.H),
-                           st, p);
+                           st, q);
             return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step + commit (tensor cores) launch");
         }
         if (tc_img) {  // the decision on the tensor cores (attribute set by step_tc_prepare)

@@ -105,3 +105,17 @@ def test_training_tc_router_rejects_unsupported_width(cuda):
     cfg = TrainConfig(batch_size=8, buffer_capacity=64, warmup=8, total_iterations=4, hidden=48)
     with pytest.raises(ValueError):
         run_training(tiers, rw, cfg, n_envs=4, router="tc", mode="device")
+
+
+def test_training_tc_router_multi_round(cuda):
+    """The tensor-core step + commit over more envs than two CTAs per SM cover (several
+    rounds per CTA, virtual blocks from the start-order ticket): the same training as
+    the fp64 router."""
+    tiers, rw = default_tiers(), RewardSpec.default()
+    cfg = TrainConfig(batch_size=128, buffer_capacity=60_000, warmup=8_000, total_iterations=40, log_every=20,
+                      seed=29)
+    a = run_training(tiers, rw, cfg, n_envs=6000, updates_per_step=1, mode="device", router="fp64")
+    b = run_training(tiers, rw, cfg, n_envs=6000, updates_per_step=1, mode="device", router="tc")
+    assert a.updates > 10 and (a.updates, a.transitions) == (b.updates, b.transitions)
+    for x, y in zip(a.net.params(), b.net.params()):
+        assert np.array_equal(x, y)
