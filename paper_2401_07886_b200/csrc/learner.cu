@@ -676,6 +676,19 @@ __global__ void __launch_bounds__(UTHREADS) learner_xupdate_kernel(const UpdateP
 // the counters (apply_finish).  Bit-identical to partial + learner_update_kernel.
 constexpr int TAIL_CTAS = 128;  // at most (measured: 128 > 64 > 32 at batch 512)
 
+// fetch-add with release semantics at GPU scope: the CTA's writes this thread observed
+// through the preceding barrier are ordered before the ticket (cumulativity)
+__device__ __forceinline__ unsigned long long atom_add_release_gpu(unsigned long long* a, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long long* a, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.add.acq_rel.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(a), "l"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* a) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
@@ -696,10 +709,7 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
     __shared__ unsigned long long rank_sh;
     __shared__ double part[2][UTHREADS / 32][32];
     __syncthreads();  // every thread's partial sums are written
-    if (threadIdx.x == 0) {
-        __threadfence();
-        rank_sh = atomicAdd(p.tick, 1ull);
-    }
+    if (threadIdx.x == 0) rank_sh = atom_add_release_gpu(p.tick, 1ull);
     __syncthreads();
     const unsigned long long nt = gridDim.x, v = rank_sh;
     const int NS = p.tail_ns;
@@ -792,9 +802,9 @@ __device__ void learner_tail(const LearnParams& p, const ApplyParams& ap, int np
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(p.tick + 1, 1ull) % (unsigned long long)NS == (unsigned long long)(NS - 1)) {
-            __threadfence();
+        // acq_rel: this slice's counter reads are released before the ticket, and the
+        // last slice acquires every other slice's (they read counters[0..1] first)
+        if (atom_add_acq_rel_gpu(p.tick + 1, 1ull) % (unsigned long long)NS == (unsigned long long)(NS - 1)) {
             apply_finish(ap);
             if (ap.advance) ap.counters[3] += 1;
         }
