@@ -126,7 +126,7 @@ __host__ __device__ constexpr size_t step_score_bytes() { return (sizeof(Score) 
 constexpr int SC_ENVS = 16;  // envs per CTA round (8 warps x 2)
 constexpr int SC_CW = 2;    // doubles per load batch of a transition copy (register-bound: 2 spills least)
 constexpr int SC_MINB = 2;  // 2 CTAs per SM: one resident wave of 296 CTAs (4736 envs)
-constexpr int SC_QU = 4;    // Q-forward unroll of the fused training step (8: register-bound, slower)
+constexpr int SC_QU = 4;    // Q-forward unroll of the fused step (weights in shared memory: 2 / 4 / 8 measure alike)
 constexpr int SC_LIST = 4096;  // block-wide transition list (ring-slot order); overflow: per env
 struct CommitShared {
     long long cursor, agg, excl;
