@@ -6,7 +6,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
-#include <stdio.h>
 
 #include "be_env.cuh"
 #include "be_internal.h"
