@@ -2,7 +2,9 @@
 // be_env_drain.  Same device building blocks as the fused rollout
 // (be_env.cuh); the per-replica registers are loaded from and stored back to
 // HBM around every step, so the host can interleave its own logic (the
-// training loop, a custom router) between steps.  One warp per env.
+// training loop, a custom router) between steps.  One or two envs per warp.
+// Also the training iteration's env step (be_train_iteration): arrivals, step and
+// replay commit in one launch (env_step_commit_kernel), fp64 or tcgen05 decisions.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
