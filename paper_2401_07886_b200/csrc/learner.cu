@@ -1,11 +1,15 @@
 // learner.cu — DQN training on the device (K3 replay + K4 learner).
 //
-//   TrainingWorkload.next_arrival    trainer.py:293-316   -> train_workload_kernel
-//   ReplayBuffer pending store       trainer.py:93-156    -> pending ring [P][E] + commit kernels
+//   TrainingWorkload.next_arrival    trainer.py:293-316   -> train_workload_kernel (host-driven),
+//                                                             in the env step (be_train_iteration)
+//   ReplayBuffer pending store       trainer.py:93-156    -> pending ring [P][E] + commit_fused_kernel
+//                                                             (host-driven) / env_step_commit_kernel
 //   ReplayBuffer ring / sample       trainer.py:101-163   -> ring [C] + Philox sampling
-//   _StepKernel.compute              trainer.py:211-267   -> learner_partial_kernel (+ reduce)
+//   _StepKernel.compute              trainer.py:211-267   -> learner_partial_kernel
 //   td_targets_double_q              trainer.py:166-174
-//   Adam / SGD, target sync          trainer.py:177-208, :276-290 -> learner_update_kernel
+//   Adam / SGD, target sync          trainer.py:177-208, :276-290 -> learner_tail (fused into
+//                                                             learner_partial_kernel) / learner_update_kernel
+//                                                             (reduce-only / apply-only: NCCL DP, host API)
 //
 // All learner arithmetic is fp64 (an fp32 learner misses 1e-5 on
 // gradients by cancellation over the batch).  Gradients are reduced over row
