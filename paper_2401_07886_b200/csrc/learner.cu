@@ -840,9 +840,10 @@ __global__ void __launch_bounds__(LTHREADS) learner_partial_kernel(const LearnPa
     double* so = p.stage_out ? reinterpret_cast<double*>(act + ((LROWS + 1) & ~1)) : nullptr;
     const int nparam = D * H + H + H * M + M;
     double* out = p.partial + (size_t)blockIdx.x * (nparam + 1);
-    // ---- the weights the forwards read (in flight during the batch gather).  Measured:
-    // a programmatic launch behind the env step (this prologue overlapping the step's
-    // tail) is slower — the early CTAs compete with the step's last CTAs
+    // ---- the weights the forwards read (in flight during the batch gather), before the
+    // wait: behind a programmatic launch the predecessor is the env step, and everything
+    // this prologue reads was final before that step's own wait returned (measured: the
+    // step triggering at its top instead of its end is slower — early CTAs compete)
     double wo[DM], wt[DM], bo = 0.0, bt = 0.0;
     if ((int)threadIdx.x < H) load_w1_col<DM>(p.w1, p.b1, p.tw1, p.tb1, D, H, threadIdx.x, wo, wt, bo, bt);
     for (int k = threadIdx.x; k < H * M; k += blockDim.x) {
@@ -1344,6 +1345,14 @@ static int learner_backward_impl(be_learner* L, const double* s, const uint8_t* 
         p.tick = L->tick;
         p.qpack = qpack;
         p.T = cf.n_tasks;
+    }
+    if (tail && uidx == 0) {
+        // be_train_iteration's first update follows the env step, which triggers at its
+        // end: a programmatic launch hides this launch's latency (the weight prologue
+        // reads only what the step itself waited for; +0.5%)
+        cudaError_t e2 = launch_pdl(kern, dim3(L->n_tiles), dim3(LTHREADS), smem, st, p, ap);
+        if (e2 != cudaSuccess) return set_cuda_error(e2, "learner launch");
+        return BE_OK;
     }
     kern<<<L->n_tiles, LTHREADS, smem, st>>>(p, ap);
     // fused: tile reduction + optimizer step in one launch; else tile reduction -> grad
