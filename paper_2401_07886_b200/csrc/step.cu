@@ -105,7 +105,7 @@ struct StepParams {
     int64_t eps_decay;
     int32_t pending_P;
     const double* qpack;  // packed fp64 weights (QLayout) in global memory, read through L1
-    // decision on the tensor cores (env_step_tc_kernel): the router's packed image
+    // decision on the tensor cores (env_step_commit_kernel<M, true>): the router's packed image
     // (TcLayout, rebuilt by prep_kernel every iteration) and the TMEM columns to allocate
     const float* tc_img;
     int32_t tc_ncols;
@@ -308,7 +308,7 @@ __device__ __forceinline__ int64_t group_max64(int64_t v) {
     return v;
 }
 
-// Per-CTA tensor-core decision context of env_step_tc_kernel (shared memory + TMEM).
+// Per-CTA tensor-core decision context of env_step_commit_kernel<M, true> (shared memory + TMEM).
 struct TcStepCtx {
     const float* img;  // TcLayout image in shared memory
     float* Ah;         // A operand, tf32 hi: [128 rows][TC_K] UMMA K-major (rows >= 16 stay 0)
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(256, SC_MINB) env_step_commit_kernel(const Ste
     Score& sc = *reinterpret_cast<Score*>(smem_raw);
     __shared__ CommitShared cs;
     // TCQ: one TMEM allocation (H columns; two CTAs per SM) and one bulk copy of the
-    // packed router image per CTA, for all rounds (env_step_tc_kernel's setup)
+    // packed router image per CTA, for all rounds
     TcStepCtx cx;
     uint64_t* bars = nullptr;
     if constexpr (TCQ) {
@@ -779,61 +779,6 @@ __device__ __forceinline__ int tc_decide(TcStepCtx& cx, bool live, bool explore,
     return tier;
 }
 
-// Shared-memory plan of env_step_tc_kernel: [Score | image | A hi | A lo | partials | barriers]
-
-// The training env step with the greedy decision on the tensor cores (be_train_iteration,
-// router = BE_ROUTER_TC).  256 threads = 16 envs (16 lanes each) per CTA round, rounds
-// CTA-uniform (every thread reaches the two MMA barriers); per CTA: one TMEM allocation
-// of H columns and one bulk copy of the packed image for all rounds.
-template <int M>
-__global__ void __launch_bounds__(256) env_step_tc_kernel(const StepParams p) {
-    pdl_wait();  // prep_kernel (weights image, workload) has completed
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
-    const TcStepSmem S(p.H);
-    Score& sc = *reinterpret_cast<Score*>(smem_raw);
-    TcStepCtx cx;
-    cx.img = reinterpret_cast<const float*>(smem_raw + S.img);
-    cx.Ah = reinterpret_cast<float*>(smem_raw + S.ah);
-    cx.Al = reinterpret_cast<float*>(smem_raw + S.al);
-    cx.part = reinterpret_cast<float2*>(smem_raw + S.part);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + S.bars);
-    uint32_t* tmem_sh = reinterpret_cast<uint32_t*>(bars + 2);
-    cx.bar = &bars[1];
-    cx.img_bar = &bars[0];
-    cx.phase = 0;
-    cx.img_ready = false;
-    const int T = p.cfg.n_tasks, H = p.H, D = T + M + 1;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    if (tid < 32) load_score(sc, p.cfg, p.aux);
-    for (int k = tid; k < 2 * 128 * TC_K; k += blockDim.x) cx.Ah[k] = 0.f;  // Ah, Al: rows >= 16 stay 0
-    if (tid == 0) {
-        tc::mbar_init(&bars[0], 1);
-        tc::mbar_init(&bars[1], 1);
-        tc::fence_mbar_init();
-    }
-    if (warp == 0) tc::tmem_alloc(tmem_sh, (uint32_t)p.tc_ncols);
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    cx.tmem = *tmem_sh;
-    if (tid == 0) {
-        const uint32_t nb = (uint32_t)TcLayout{H}.bytes();
-        tc::mbar_expect_tx(&bars[0], nb);
-        tc::bulk_g2s(const_cast<float*>(cx.img), p.tc_img, nb, &bars[0]);
-    }
-    const int grp = (tid & 31) >> 4;
-    const int per_round = 16 * gridDim.x;
-    const int rounds = (p.E + per_round - 1) / per_round;
-    for (int k = 0; k < rounds; ++k) {
-        const int e = (k * gridDim.x + blockIdx.x) * 16 + warp * 2 + grp;
-        step_env<M, 16, true>(p, e < p.E ? e : p.E - 1, e < p.E, sc, p.qpack, true, T, H, D, &cx);
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(cx.tmem, (uint32_t)p.tc_ncols);
-    pdl_trigger();
-}
-
 size_t step_tc_smem_bytes(int H) { return TcStepSmem(H).bytes; }
 
 void step_tc_prepare(int M, int H) {
@@ -841,7 +786,6 @@ void step_tc_prepare(int M, int H) {
     switch (M) {
 #define BE_TCP(MM)                                                                                          \
     case MM:                                                                                                \
-        cudaFuncSetAttribute(env_step_tc_kernel<MM>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);     \
         cudaFuncSetAttribute(env_step_commit_kernel<MM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
         cudaFuncSetAttribute(env_step_commit_kernel<MM, true>, cudaFuncAttributePreferredSharedMemoryCarveout,   \
                              (int)cudaSharedmemCarveoutMaxShared); /* two CTAs per SM (shared TMEM) */       \
@@ -1127,16 +1071,7 @@ static int launch_step_m(const StepParams& p, size_t smem, cudaStream_t st, cons
                            st, q);
             return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step + commit (tensor cores) launch");
         }
-        if (tc_img) {  // the decision on the tensor cores (attribute set by step_tc_prepare)
-            int dev = 0, sms = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            long long blocks = ((long long)p.E + 15) / 16;
-            if (blocks > 2LL * sms) blocks = 2LL * sms;  // two CTAs per SM share its TMEM
-            cudaError_t e = launch_pdl(env_step_tc_kernel<M>, dim3((unsigned)blocks), dim3(256),
-                                       step_tc_smem_bytes(p.H), st, p);
-            return e == cudaSuccess ? BE_OK : set_cuda_error(e, "env step (tensor cores) launch");
-        }
+        if (tc_img) return set_error(BE_EINVAL, "the tensor-core env step runs fused with the replay commit");
     }
     if (p.fuse_commit) {  // the training step + replay commit (two envs per warp)
         if (!two) return set_error(BE_EINVAL, "fused commit needs <= 16 replicas and input dim <= 16");
